@@ -1,0 +1,223 @@
+"""ctypes wrapper of the plain-C fp64 oracle (oracle/pfem_oracle.c).
+
+TEST INFRASTRUCTURE ONLY — only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / ``--impl reference`` legs may import this module.  It shares no
+code with the CUDA path.  Every function follows PAPER.md as cited in
+pfem_oracle.c; numpy is used only for argument marshalling.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "pfem_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+OK, ERR_ARG, ERR_DEGENERATE, ERR_INVERTED, ERR_NOT_CONVERGED, ERR_BREAKDOWN, ERR_CAPACITY = \
+    0, -1, -2, -3, -4, -5, -6
+MODELS = {"linear": 0, "neohookean": 1}
+PARAM_KINDS = {"lame": 0, "young_poisson": 1, "young_poisson_plane_stress": 2}
+
+
+class OracleError(RuntimeError):
+    def __init__(self, status, index, what):
+        super().__init__(f"oracle {what}: status {status}, index {index}")
+        self.status = status
+        self.index = index
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (-O2 -ffp-contract=off: no FMA contraction, plain)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-shared",
+               "-fPIC", "-std=c11", "-o", _LIB, _SRC, "-lm"]
+        subprocess.check_call(cmd)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        _lib = C.CDLL(_LIB)
+        _lib.oracle_last_error_index.restype = C.c_int64
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _check(st, what):
+    if st != OK:
+        raise OracleError(st, lib().oracle_last_error_index(), what)
+
+
+I64 = C.c_int64
+
+
+def lame(kind: str, p0, p1, n: int):
+    """(mu, lambda) per element from (E, nu) or (mu, lambda); uniform arrays of length 1 broadcast."""
+    p0 = _f64(np.atleast_1d(p0))
+    p1 = _f64(np.atleast_1d(p1))
+    mu = np.empty(n)
+    lam = np.empty(n)
+    st = lib().oracle_lame(C.c_int(PARAM_KINDS[kind]), I64(n), _p(p0), I64(0 if len(p0) == 1 else 1),
+                           _p(p1), I64(0 if len(p1) == 1 else 1), _p(mu), _p(lam))
+    _check(st, "lame")
+    return mu, lam
+
+
+def geometry(coords, conn):
+    """grad [E, d, d] (grad[e, a-1, j] = dN_a/dX_j, a = 1..d), vol [E], sign [E]."""
+    coords = _f64(coords)
+    conn = _i32(conn)
+    N, d = coords.shape
+    E = conn.shape[0]
+    grad = np.zeros((E, d, d))
+    vol = np.zeros(E)
+    sign = np.zeros(E, np.int32)
+    st = lib().oracle_geometry(C.c_int(d), I64(N), I64(E), _p(coords), _p(conn), _p(grad), _p(vol), _p(sign))
+    _check(st, "geometry")
+    return grad, vol, sign
+
+
+def csr(conn, n_nodes: int):
+    conn = _i32(conn)
+    E, nv = conn.shape
+    ptr = np.zeros(n_nodes + 1, np.int32)
+    ent = np.zeros(E * nv, np.int32)
+    _check(lib().oracle_csr(C.c_int(nv - 1), I64(n_nodes), I64(E), _p(conn), _p(ptr), _p(ent)), "csr")
+    return ptr, ent
+
+
+def colour(conn, n_nodes: int, ptr, ent, max_colours: int = 256):
+    conn = _i32(conn)
+    E, nv = conn.shape
+    col = np.zeros(E, np.int32)
+    nc = C.c_int32(0)
+    st = lib().oracle_colour(C.c_int(nv - 1), I64(n_nodes), I64(E), _p(conn), _p(_i32(ptr)),
+                             _p(_i32(ent)), _p(col), C.c_int32(max_colours), C.byref(nc))
+    _check(st, "colour")
+    return col, nc.value
+
+
+def colour_sort(col, n_colours: int):
+    col = _i32(col)
+    elems = np.zeros(len(col), np.int32)
+    cptr = np.zeros(n_colours + 1, np.int32)
+    _check(lib().oracle_colour_sort(I64(len(col)), _p(col), C.c_int32(n_colours), _p(elems), _p(cptr)),
+           "colour_sort")
+    return elems, cptr
+
+
+@dataclass
+class Mesh:
+    """Oracle-side prepared mesh (fp64 geometry + per-element Lame parameters)."""
+    coords: np.ndarray
+    conn: np.ndarray
+    grad: np.ndarray
+    vol: np.ndarray
+    mu: np.ndarray
+    lam: np.ndarray
+    model: str
+    part_elem: np.ndarray
+    part_node: np.ndarray
+
+    @property
+    def dim(self):
+        return self.coords.shape[1]
+
+    @property
+    def n_nodes(self):
+        return self.coords.shape[0]
+
+    @property
+    def n_elems(self):
+        return self.conn.shape[0]
+
+    def _args(self):
+        return (C.c_int(self.dim), I64(self.n_nodes), I64(self.n_elems), _p(self.conn),
+                _p(self.grad), _p(self.vol), C.c_int(MODELS[self.model]), _p(self.mu), _p(self.lam))
+
+    def energy(self, u, f_ext=None, want_elem=True):
+        """(W_e [S, E] or None, totals [S, K])."""
+        u = _f64(u).reshape(-1, self.n_nodes, self.dim)
+        S = u.shape[0]
+        K = len(self.part_elem) - 1
+        W = np.zeros((S, self.n_elems)) if want_elem else None
+        tot = np.zeros((S, K))
+        fe = None if f_ext is None else _f64(f_ext)
+        a = self._args()
+        st = lib().oracle_energy(a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7], a[8],
+                                 C.c_int(S), _p(u), C.c_int(K), _p(self.part_elem), _p(self.part_node),
+                                 _p(fe), _p(W), _p(tot))
+        _check(st, "energy")
+        return W, tot
+
+    def residual(self, u):
+        """internal force f_int(u) [S, N, d]."""
+        u = _f64(u).reshape(-1, self.n_nodes, self.dim)
+        r = np.zeros_like(u)
+        st = lib().oracle_residual(*self._args(), C.c_int(u.shape[0]), _p(u), _p(r))
+        _check(st, "residual")
+        return r
+
+    def tangent(self, v, u=None, mask=None):
+        """K(u) v  [S, N, d]; with mask: (I-M) K (I-M) v + M v."""
+        v = _f64(v).reshape(-1, self.n_nodes, self.dim)
+        uu = None if u is None else _f64(u).reshape(v.shape)
+        m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
+        out = np.zeros_like(v)
+        st = lib().oracle_tangent(*self._args(), C.c_int(v.shape[0]), _p(uu), _p(v), _p(m), _p(out))
+        _check(st, "tangent")
+        return out
+
+    def cg(self, f, mask, x0, tol=1e-8, max_iter=50000, u_state=None, history=True):
+        """Warm-started masked CG; returns (x, report dict)."""
+        x = _f64(x0).copy().reshape(-1)
+        f = _f64(f).reshape(-1)
+        m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8).reshape(-1)
+        us = None if u_state is None else _f64(u_state).reshape(-1)
+        hist = np.zeros(max_iter + 1) if history else None
+        it = C.c_int32(0)
+        r0, rf, tr = C.c_double(0), C.c_double(0), C.c_double(0)
+        st = lib().oracle_cg(*self._args(), _p(us), _p(f), _p(m), _p(x), C.c_double(tol),
+                             C.c_int32(max_iter), _p(hist), C.byref(it), C.byref(r0), C.byref(rf),
+                             C.byref(tr))
+        rep = {"status": st, "iterations": it.value, "converged": st == OK, "rel_res0": r0.value,
+               "rel_res_final": rf.value, "true_rel_res_final": tr.value,
+               "history": None if hist is None else hist[: it.value + 1].copy()}
+        return x.reshape(np.shape(x0)), rep
+
+
+def prepare(coords, conn, model: str, param_kind: str, p0, p1, part_elem=None, part_node=None) -> Mesh:
+    coords = _f64(coords)
+    conn = _i32(conn)
+    grad, vol, _ = geometry(coords, conn)
+    mu, lam = lame(param_kind, p0, p1, conn.shape[0])
+    pe = _i32(part_elem if part_elem is not None else [0, conn.shape[0]])
+    pn = _i32(part_node if part_node is not None else [0, coords.shape[0]])
+    return Mesh(coords, conn, grad, vol, mu, lam, model, pe, pn)
+
+
+def prepare_problem(prob) -> Mesh:
+    """Oracle mesh for a pfem_gen.Problem."""
+    pe, pn = prob.parts()
+    return prepare(prob.coords, prob.conn, prob.model, prob.param_kind, prob.p0, prob.p1, pe, pn)

@@ -1,0 +1,635 @@
+/*
+ * pfem_oracle.c — plain, slow, obviously-correct CPU reference ("oracle") for the
+ * PFEM explicit-FE hot path (arXiv 2601.03086).  TEST INFRASTRUCTURE ONLY: only
+ * tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+ * legs may load this library.  It shares no code, header, table or helper with
+ * the CUDA path (paper_2601_03086_b200/csrc); it follows the paper's textbook
+ * formulations, not the GPU's:
+ *
+ *   geometry       P1 shape functions, grad N_a = rows of J^{-1}      (App. B)
+ *   linear energy  Psi = 1/2 sigma:eps, sigma = E/(1+nu) eps + E nu/((1+nu)(1-2nu)) tr(eps) I   (§4.1 eq.)
+ *   Neo-Hookean    Psi = 1/2 lam (ln J)^2 - mu ln J + 1/2 mu (I1 - d)  (§4.2 eq.; reading R2: "-2" -> "-d")
+ *   Lame           lam = nu E/((1+nu)(1-2nu)), mu = E/(2(1+nu))        (§4.2)
+ *   residual       f_int_iI = int dN_I/dX_l F_ik S_kl dV0 (total Lagrangian, App. B);
+ *                  linear: f = int B^T sigma dV (virtual power)
+ *   tangent        K = int G0^T S G0 + B0^T C^SE B0 dV0                 (App. B); linear: B^T D B
+ *   CG             K U = F, stop on ||K U - F|| / ||F|| < tol            (App. B), warm start U0
+ *
+ * Everything in float64, plain loops, IEEE RN, built with -O2 -ffp-contract=off.
+ * Element-local work may run in an OpenMP parallel loop writing per-element
+ * buffers; every assembly (sum into nodes) is a single sequential loop in
+ * ascending (element, local node) order.
+ *
+ * Parity pins: see tests/test_oracle_*.py (closed forms, invariants, finite
+ * differences, brute force).  Functions without a pin say "parity unpinned" —
+ * currently none.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OR_OK 0
+#define OR_ERR_ARG (-1)
+#define OR_ERR_DEGENERATE (-2)
+#define OR_ERR_INVERTED (-3)
+#define OR_ERR_NOT_CONVERGED (-4)
+#define OR_ERR_BREAKDOWN (-5)
+#define OR_ERR_CAPACITY (-6)
+
+#define OR_LINEAR 0
+#define OR_NEOHOOKEAN 1
+
+static int64_t g_err_index = -1;
+int64_t oracle_last_error_index(void) { return g_err_index; }
+
+/* ------------------------------------------------------------------ */
+/* small dense helpers (plain textbook formulas)                       */
+/* ------------------------------------------------------------------ */
+static double det2(const double A[2][2]) { return A[0][0] * A[1][1] - A[0][1] * A[1][0]; }
+
+static double det3(const double A[3][3]) {
+    return A[0][0] * (A[1][1] * A[2][2] - A[1][2] * A[2][1])
+         - A[0][1] * (A[1][0] * A[2][2] - A[1][2] * A[2][0])
+         + A[0][2] * (A[1][0] * A[2][1] - A[1][1] * A[2][0]);
+}
+
+/* inverse by adjugate / determinant; returns det */
+static double inv_dd(int d, const double A[3][3], double Ai[3][3]) {
+    if (d == 2) {
+        double a[2][2] = {{A[0][0], A[0][1]}, {A[1][0], A[1][1]}};
+        double det = det2(a);
+        Ai[0][0] = A[1][1] / det;  Ai[0][1] = -A[0][1] / det;
+        Ai[1][0] = -A[1][0] / det; Ai[1][1] = A[0][0] / det;
+        return det;
+    }
+    double det = det3(A);
+    Ai[0][0] = (A[1][1] * A[2][2] - A[1][2] * A[2][1]) / det;
+    Ai[0][1] = (A[0][2] * A[2][1] - A[0][1] * A[2][2]) / det;
+    Ai[0][2] = (A[0][1] * A[1][2] - A[0][2] * A[1][1]) / det;
+    Ai[1][0] = (A[1][2] * A[2][0] - A[1][0] * A[2][2]) / det;
+    Ai[1][1] = (A[0][0] * A[2][2] - A[0][2] * A[2][0]) / det;
+    Ai[1][2] = (A[0][2] * A[1][0] - A[0][0] * A[1][2]) / det;
+    Ai[2][0] = (A[1][0] * A[2][1] - A[1][1] * A[2][0]) / det;
+    Ai[2][1] = (A[0][1] * A[2][0] - A[0][0] * A[2][1]) / det;
+    Ai[2][2] = (A[0][0] * A[1][1] - A[0][1] * A[1][0]) / det;
+    return det;
+}
+
+/* ------------------------------------------------------------------ */
+/* Material: Lame parameters from (E, nu)  — P:727-732                 */
+/* kind 0: (mu, lambda) given; 1: (E, nu) plane strain / 3-D;          */
+/* 2: (E, nu) plane stress lambda* = 2 mu lam / (lam + 2 mu) (reading R1) */
+/* ------------------------------------------------------------------ */
+int oracle_lame(int kind, int64_t n, const double* p0, int64_t s0, const double* p1, int64_t s1,
+                double* mu, double* lam) {
+    for (int64_t e = 0; e < n; ++e) {
+        double a = p0[e * s0], b = p1[e * s1];
+        if (kind == 0) {
+            mu[e] = a;
+            lam[e] = b;
+        } else {
+            double E = a, nu = b;
+            double m = E / (2.0 * (1.0 + nu));
+            double l = nu * E / ((1.0 + nu) * (1.0 - 2.0 * nu));
+            if (kind == 2) l = 2.0 * m * l / (l + 2.0 * m);
+            else if (kind != 1) return OR_ERR_ARG;
+            mu[e] = m;
+            lam[e] = l;
+        }
+    }
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* Geometry: J_e = [X_1-X_0 | ... | X_d-X_0] (columns), grad N_a = row  */
+/* (a-1) of J^{-1} (a = 1..d), grad N_0 = -sum_a grad N_a,             */
+/* V_e = |det J| / d!   (P1 simplex, one-point rule exact) */
+/* grad out: [E][d][d] with grad[e][a-1][j] = dN_a/dX_j                */
+/* ------------------------------------------------------------------ */
+int oracle_geometry(int dim, int64_t n_nodes, int64_t n_elems, const double* coords,
+                    const int32_t* conn, double* grad, double* vol, int32_t* sign) {
+    if (dim != 2 && dim != 3) return OR_ERR_ARG;
+    const int nv = dim + 1;
+    for (int64_t e = 0; e < n_elems; ++e)
+        for (int a = 0; a < nv; ++a) {
+            int32_t v = conn[e * nv + a];
+            if (v < 0 || v >= n_nodes) { g_err_index = e; return OR_ERR_ARG; }
+        }
+    int status = OR_OK;
+    int64_t bad = -1;
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < n_elems; ++e) {
+        double J[3][3] = {{0}}, Ji[3][3];
+        const int32_t* c = conn + e * nv;
+        double edge_prod = 1.0;
+        for (int a = 1; a <= dim; ++a) {
+            double len2 = 0.0;
+            for (int i = 0; i < dim; ++i) {
+                J[i][a - 1] = coords[(int64_t)c[a] * dim + i] - coords[(int64_t)c[0] * dim + i];
+                len2 += J[i][a - 1] * J[i][a - 1];
+            }
+            edge_prod *= sqrt(len2);
+        }
+        double det = inv_dd(dim, J, Ji);
+        if (!(fabs(det) > 64.0 * 2.220446049250313e-16 * edge_prod)) {
+#pragma omp critical
+            { if (bad < 0 || e < bad) bad = e; }
+            continue;
+        }
+        for (int a = 0; a < dim; ++a)
+            for (int j = 0; j < dim; ++j) grad[(e * dim + a) * dim + j] = Ji[a][j];
+        vol[e] = fabs(det) / (dim == 2 ? 2.0 : 6.0);
+        if (sign) sign[e] = det > 0 ? 1 : -1;
+    }
+    if (bad >= 0) { g_err_index = bad; status = OR_ERR_DEGENERATE; }
+    return status;
+}
+
+/* all d+1 gradients of element e: g[a][j], a = 0..d */
+static void elem_grads(int dim, const double* grad, int64_t e, double g[4][3]) {
+    for (int j = 0; j < dim; ++j) {
+        double s = 0.0;
+        for (int a = 1; a <= dim; ++a) {
+            g[a][j] = grad[(e * dim + (a - 1)) * dim + j];
+            s += g[a][j];
+        }
+        g[0][j] = -s;
+    }
+}
+
+/* ------------------------------------------------------------------ */
+/* node -> (element, slot) CSR: entries of node n are all (e, a) with   */
+/* conn[e][a] == n in ascending (e, a), stored as e*(d+1)+a (reading R12) */
+/* ------------------------------------------------------------------ */
+int oracle_csr(int dim, int64_t n_nodes, int64_t n_elems, const int32_t* conn,
+               int32_t* ptr, int32_t* ent) {
+    const int nv = dim + 1;
+    int64_t* fill = (int64_t*)calloc((size_t)n_nodes, sizeof(int64_t));
+    if (!fill) return OR_ERR_CAPACITY;
+    for (int64_t n = 0; n <= n_nodes; ++n) ptr[n] = 0;
+    for (int64_t k = 0; k < n_elems * nv; ++k) ptr[conn[k] + 1] += 1;
+    for (int64_t n = 0; n < n_nodes; ++n) ptr[n + 1] += ptr[n];
+    for (int64_t e = 0; e < n_elems; ++e)          /* ascending (e, a): rows come out sorted */
+        for (int a = 0; a < nv; ++a) {
+            int32_t n = conn[e * nv + a];
+            ent[ptr[n] + fill[n]] = (int32_t)(e * nv + a);
+            fill[n] += 1;
+        }
+    free(fill);
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* Greedy first-fit colouring in ascending element id (reading R12):   */
+/* colour(e) = smallest c >= 0 not used by any neighbour f < e, where   */
+/* neighbours share at least one node.                                  */
+/* ------------------------------------------------------------------ */
+int oracle_colour(int dim, int64_t n_nodes, int64_t n_elems, const int32_t* conn,
+                  const int32_t* ptr, const int32_t* ent, int32_t* colour, int32_t max_colours,
+                  int32_t* n_colours) {
+    (void)n_nodes;
+    const int nv = dim + 1;
+    unsigned char* used = (unsigned char*)calloc((size_t)max_colours + 1, 1);
+    if (!used) return OR_ERR_CAPACITY;
+    int32_t nc = 0;
+    for (int64_t e = 0; e < n_elems; ++e) {
+        memset(used, 0, (size_t)max_colours + 1);
+        for (int a = 0; a < nv; ++a) {
+            int32_t n = conn[e * nv + a];
+            for (int32_t k = ptr[n]; k < ptr[n + 1]; ++k) {
+                int64_t f = ent[k] / nv;
+                if (f < e && colour[f] <= max_colours) used[colour[f]] = 1;
+            }
+        }
+        int32_t c = 0;
+        while (c < max_colours && used[c]) ++c;
+        if (c >= max_colours) { free(used); g_err_index = e; return OR_ERR_CAPACITY; }
+        colour[e] = c;
+        if (c + 1 > nc) nc = c + 1;
+    }
+    free(used);
+    *n_colours = nc;
+    return OR_OK;
+}
+
+/* colour_elems sorted by (colour, element); colour_ptr[c] offsets */
+int oracle_colour_sort(int64_t n_elems, const int32_t* colour, int32_t n_colours,
+                       int32_t* colour_elems, int32_t* colour_ptr) {
+    for (int32_t c = 0; c <= n_colours; ++c) colour_ptr[c] = 0;
+    for (int64_t e = 0; e < n_elems; ++e) colour_ptr[colour[e] + 1] += 1;
+    for (int32_t c = 0; c < n_colours; ++c) colour_ptr[c + 1] += colour_ptr[c];
+    int32_t* fill = (int32_t*)calloc((size_t)n_colours, sizeof(int32_t));
+    if (!fill) return OR_ERR_CAPACITY;
+    for (int64_t e = 0; e < n_elems; ++e) {
+        int32_t c = colour[e];
+        colour_elems[colour_ptr[c] + fill[c]++] = (int32_t)e;
+    }
+    free(fill);
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* Kinematics: F = I + grad u, grad u = sum_{a=0..d} u_a (x) */
+/* grad N_a  (x = N_I x_I)                                 */
+/* ------------------------------------------------------------------ */
+static void elem_F(int dim, const int32_t* c, const double* u, double g[4][3], double F[3][3]) {
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) F[i][j] = (i == j) ? 1.0 : 0.0;
+    for (int a = 0; a <= dim; ++a)
+        for (int i = 0; i < dim; ++i)
+            for (int j = 0; j < dim; ++j) F[i][j] += u[(int64_t)c[a] * dim + i] * g[a][j];
+}
+
+/* Voigt strain-displacement matrix B (small strain), engineering shear.
+ * 3-D rows: eps11, eps22, eps33, 2eps23, 2eps13, 2eps12; 2-D: eps11, eps22, 2eps12.
+ * Column index a*d + i.                                               */
+static int voigt_B(int dim, double g[4][3], double B[6][12]) {
+    const int nv = dim + 1;
+    memset(B, 0, sizeof(double) * 6 * 12);
+    if (dim == 2) {
+        for (int a = 0; a < nv; ++a) {
+            B[0][a * 2 + 0] = g[a][0];
+            B[1][a * 2 + 1] = g[a][1];
+            B[2][a * 2 + 0] = g[a][1];
+            B[2][a * 2 + 1] = g[a][0];
+        }
+        return 3;
+    }
+    for (int a = 0; a < nv; ++a) {
+        B[0][a * 3 + 0] = g[a][0];
+        B[1][a * 3 + 1] = g[a][1];
+        B[2][a * 3 + 2] = g[a][2];
+        B[3][a * 3 + 1] = g[a][2];
+        B[3][a * 3 + 2] = g[a][1];
+        B[4][a * 3 + 0] = g[a][2];
+        B[4][a * 3 + 2] = g[a][0];
+        B[5][a * 3 + 0] = g[a][1];
+        B[5][a * 3 + 1] = g[a][0];
+    }
+    return 6;
+}
+
+/* isotropic elasticity matrix D (Voigt, engineering shear): sigma = 2 mu eps + lam tr(eps) I,
+ * written with the paper's coefficients 2mu = E/(1+nu), lam = E nu/((1+nu)(1-2nu));
+ * 2-D is plane strain (reading R1).                                    */
+static void voigt_D(int dim, double mu, double lam, double D[6][6]) {
+    memset(D, 0, sizeof(double) * 36);
+    int nn = dim;             /* normal components */
+    int ns = dim == 2 ? 1 : 3;
+    for (int i = 0; i < nn; ++i)
+        for (int j = 0; j < nn; ++j) D[i][j] = lam + (i == j ? 2.0 * mu : 0.0);
+    for (int k = 0; k < ns; ++k) D[nn + k][nn + k] = mu;
+}
+
+/* Voigt index pairs */
+static const int VI3[6][2] = {{0, 0}, {1, 1}, {2, 2}, {1, 2}, {0, 2}, {0, 1}};
+static const int VI2[3][2] = {{0, 0}, {1, 1}, {0, 1}};
+
+/* Neo-Hookean second Piola-Kirchhoff stress and tangent (App. B; from Psi of P:713-722):
+ * S = mu (I - C^{-1}) + lam ln J C^{-1};
+ * C^SE_IJKL = lam Ci_IJ Ci_KL + (mu - lam ln J)(Ci_IK Ci_JL + Ci_IL Ci_JK).   */
+static int nh_state(int dim, double F[3][3], double mu, double lam, double S[3][3],
+                    double Ci[3][3], double* J_out, double* lnJ_out, double* psi_out) {
+    double C[3][3] = {{0}};
+    for (int I = 0; I < dim; ++I)
+        for (int Jx = 0; Jx < dim; ++Jx)
+            for (int k = 0; k < dim; ++k) C[I][Jx] += F[k][I] * F[k][Jx];
+    double Fd[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) Fd[i][j] = F[i][j];
+    double J = dim == 2 ? (Fd[0][0] * Fd[1][1] - Fd[0][1] * Fd[1][0]) : det3(Fd);
+    if (!(J > 0.0)) return OR_ERR_INVERTED;
+    double lnJ = log(J);
+    double I1 = 0.0;
+    for (int i = 0; i < dim; ++i) I1 += C[i][i];
+    inv_dd(dim, C, Ci);
+    for (int I = 0; I < dim; ++I)
+        for (int Jx = 0; Jx < dim; ++Jx)
+            S[I][Jx] = mu * ((I == Jx ? 1.0 : 0.0) - Ci[I][Jx]) + lam * lnJ * Ci[I][Jx];
+    *J_out = J;
+    *lnJ_out = lnJ;
+    *psi_out = 0.5 * lam * lnJ * lnJ - mu * lnJ + 0.5 * mu * (I1 - (double)dim);
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* Element energy W_e = V_e Psi_e; totals W_{s,k} = sum_{e in part k} W_e; */
+/* optional Pi = W - sum_{n in part k} f_ext,n . u_n */
+/* ------------------------------------------------------------------ */
+int oracle_energy(int dim, int64_t n_nodes, int64_t n_elems, const int32_t* conn,
+                  const double* grad, const double* vol, int model, const double* mu,
+                  const double* lam, int n_samples, const double* u, int n_parts,
+                  const int32_t* part_elem, const int32_t* part_node, const double* f_ext,
+                  double* W_e, double* totals) {
+    const int nv = dim + 1;
+    double* W = W_e ? W_e : (double*)malloc(sizeof(double) * (size_t)n_elems * n_samples);
+    if (!W) return OR_ERR_CAPACITY;
+    int64_t first_bad = -1;
+    for (int s = 0; s < n_samples; ++s) {
+        const double* us = u + (int64_t)s * n_nodes * dim;
+        double* Ws = W + (int64_t)s * n_elems;
+#pragma omp parallel for schedule(static)
+        for (int64_t e = 0; e < n_elems; ++e) {
+            double g[4][3];
+            elem_grads(dim, grad, e, g);
+            const int32_t* c = conn + e * nv;
+            double psi;
+            if (model == OR_LINEAR) {
+                double B[6][12], D[6][6], eps[6] = {0}, sig[6] = {0};
+                int nvo = voigt_B(dim, g, B);
+                voigt_D(dim, mu[e], lam[e], D);
+                for (int r = 0; r < nvo; ++r)
+                    for (int a = 0; a < nv; ++a)
+                        for (int i = 0; i < dim; ++i)
+                            eps[r] += B[r][a * dim + i] * us[(int64_t)c[a] * dim + i];
+                for (int r = 0; r < nvo; ++r)
+                    for (int q = 0; q < nvo; ++q) sig[r] += D[r][q] * eps[q];
+                psi = 0.0;
+                for (int r = 0; r < nvo; ++r) psi += 0.5 * sig[r] * eps[r];   /* 1/2 sigma:eps */
+            } else {
+                double F[3][3], S[3][3], Ci[3][3], J, lnJ;
+                elem_F(dim, c, us, g, F);
+                if (nh_state(dim, F, mu[e], lam[e], S, Ci, &J, &lnJ, &psi) != OR_OK) {
+#pragma omp critical
+                    { if (first_bad < 0 || e < first_bad) first_bad = e; }
+                    psi = NAN;
+                }
+            }
+            Ws[e] = vol[e] * psi;
+        }
+    }
+    for (int s = 0; s < n_samples; ++s) {
+        const double* us = u + (int64_t)s * n_nodes * dim;
+        for (int k = 0; k < n_parts; ++k) {
+            double acc = 0.0;
+            for (int64_t e = part_elem[k]; e < part_elem[k + 1]; ++e) acc += W[(int64_t)s * n_elems + e];
+            if (f_ext) {
+                double work = 0.0;
+                for (int64_t n = part_node[k]; n < part_node[k + 1]; ++n)
+                    for (int i = 0; i < dim; ++i) work += f_ext[n * dim + i] * us[n * dim + i];
+                acc -= work;
+            }
+            totals[(int64_t)s * n_parts + k] = acc;
+        }
+    }
+    if (!W_e) free(W);
+    if (first_bad >= 0) { g_err_index = first_bad; return OR_ERR_INVERTED; }
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* Internal force (residual without f_ext; reading R7):                 */
+/*  linear: f_e = V B^T D B u_e (virtual power)            */
+/*  NH:     f_iI = V dN_I/dX_l F_ik S_kl (total Lagrangian) */
+/* assembled sequentially in ascending (e, a) order.                    */
+/* ------------------------------------------------------------------ */
+int oracle_residual(int dim, int64_t n_nodes, int64_t n_elems, const int32_t* conn,
+                    const double* grad, const double* vol, int model, const double* mu,
+                    const double* lam, int n_samples, const double* u, double* r) {
+    const int nv = dim + 1;
+    const int ne = nv * dim;
+    double* fe = (double*)malloc(sizeof(double) * (size_t)n_elems * ne);
+    if (!fe) return OR_ERR_CAPACITY;
+    int64_t first_bad = -1;
+    for (int s = 0; s < n_samples; ++s) {
+        const double* us = u + (int64_t)s * n_nodes * dim;
+        double* rs = r + (int64_t)s * n_nodes * dim;
+#pragma omp parallel for schedule(static)
+        for (int64_t e = 0; e < n_elems; ++e) {
+            double g[4][3];
+            elem_grads(dim, grad, e, g);
+            const int32_t* c = conn + e * nv;
+            double* f = fe + e * ne;
+            if (model == OR_LINEAR) {
+                double B[6][12], D[6][6], eps[6] = {0}, sig[6] = {0};
+                int nvo = voigt_B(dim, g, B);
+                voigt_D(dim, mu[e], lam[e], D);
+                for (int q = 0; q < nvo; ++q)
+                    for (int a = 0; a < nv; ++a)
+                        for (int i = 0; i < dim; ++i)
+                            eps[q] += B[q][a * dim + i] * us[(int64_t)c[a] * dim + i];
+                for (int q = 0; q < nvo; ++q)
+                    for (int p = 0; p < nvo; ++p) sig[q] += D[q][p] * eps[p];
+                for (int k = 0; k < ne; ++k) {
+                    double acc = 0.0;
+                    for (int q = 0; q < nvo; ++q) acc += B[q][k] * sig[q];
+                    f[k] = vol[e] * acc;
+                }
+            } else {
+                double F[3][3], S[3][3], Ci[3][3], J, lnJ, psi;
+                elem_F(dim, c, us, g, F);
+                if (nh_state(dim, F, mu[e], lam[e], S, Ci, &J, &lnJ, &psi) != OR_OK) {
+#pragma omp critical
+                    { if (first_bad < 0 || e < first_bad) first_bad = e; }
+                }
+                for (int a = 0; a < nv; ++a)
+                    for (int i = 0; i < dim; ++i) {
+                        double acc = 0.0;
+                        for (int k = 0; k < dim; ++k)
+                            for (int l = 0; l < dim; ++l) acc += g[a][l] * F[i][k] * S[k][l];
+                        f[a * dim + i] = vol[e] * acc;
+                    }
+            }
+        }
+        for (int64_t k = 0; k < n_nodes * dim; ++k) rs[k] = 0.0;
+        for (int64_t e = 0; e < n_elems; ++e)
+            for (int a = 0; a < nv; ++a)
+                for (int i = 0; i < dim; ++i)
+                    rs[(int64_t)conn[e * nv + a] * dim + i] += fe[e * ne + a * dim + i];
+    }
+    free(fe);
+    if (first_bad >= 0) { g_err_index = first_bad; return OR_ERR_INVERTED; }
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* Element tangent matrix K_e (ne x ne, row/col index a*d + i):          */
+/*  linear: V B^T D B;  NH: V (G0^T S G0 + B0^T C^SE B0)  */
+/* ------------------------------------------------------------------ */
+static int elem_tangent(int dim, int model, double g[4][3], double V, double mu, double lam,
+                        const int32_t* c, const double* us, double K[12][12]) {
+    const int nv = dim + 1, ne = nv * dim;
+    memset(K, 0, sizeof(double) * 144);
+    if (model == OR_LINEAR) {
+        double B[6][12], D[6][6];
+        int nvo = voigt_B(dim, g, B);
+        voigt_D(dim, mu, lam, D);
+        for (int p = 0; p < ne; ++p)
+            for (int q = 0; q < ne; ++q) {
+                double acc = 0.0;
+                for (int x = 0; x < nvo; ++x)
+                    for (int y = 0; y < nvo; ++y) acc += B[x][p] * D[x][y] * B[y][q];
+                K[p][q] = V * acc;
+            }
+        return OR_OK;
+    }
+    double F[3][3], S[3][3], Ci[3][3], J, lnJ, psi;
+    elem_F(dim, c, us, g, F);
+    int st = nh_state(dim, F, mu, lam, S, Ci, &J, &lnJ, &psi);
+    const int nvo = dim == 2 ? 3 : 6;
+    const int (*VI)[2] = dim == 2 ? VI2 : VI3;
+    /* C^SE in Voigt form (engineering shear for strains) */
+    double D[6][6];
+    for (int x = 0; x < nvo; ++x)
+        for (int y = 0; y < nvo; ++y) {
+            int I = VI[x][0], Jx = VI[x][1], K2 = VI[y][0], L = VI[y][1];
+            D[x][y] = lam * Ci[I][Jx] * Ci[K2][L] + (mu - lam * lnJ) * (Ci[I][K2] * Ci[Jx][L] + Ci[I][L] * Ci[Jx][K2]);
+        }
+    /* B0: delta E (Voigt, engineering shear) = B0 delta u;
+     * dE_KL = 1/2 (F_iK dN_a/dX_L + F_iL dN_a/dX_K) du_ia, shear rows doubled. */
+    double B0[6][12];
+    memset(B0, 0, sizeof(B0));
+    for (int x = 0; x < nvo; ++x) {
+        int Kk = VI[x][0], L = VI[x][1];
+        for (int a = 0; a < nv; ++a)
+            for (int i = 0; i < dim; ++i) {
+                double v = (Kk == L) ? F[i][Kk] * g[a][L]
+                                     : F[i][Kk] * g[a][L] + F[i][L] * g[a][Kk];
+                B0[x][a * dim + i] = v;
+            }
+    }
+    for (int p = 0; p < ne; ++p)
+        for (int q = 0; q < ne; ++q) {
+            double acc = 0.0;
+            for (int x = 0; x < nvo; ++x)
+                for (int y = 0; y < nvo; ++y) acc += B0[x][p] * D[x][y] * B0[y][q];
+            K[p][q] = V * acc;
+        }
+    /* geometric: K_geo[(a,i),(b,j)] = delta_ij grad N_a . S . grad N_b */
+    for (int a = 0; a < nv; ++a)
+        for (int b = 0; b < nv; ++b) {
+            double gsg = 0.0;
+            for (int k = 0; k < dim; ++k)
+                for (int l = 0; l < dim; ++l) gsg += g[a][k] * S[k][l] * g[b][l];
+            for (int i = 0; i < dim; ++i) K[a * dim + i][b * dim + i] += V * gsg;
+        }
+    return st;
+}
+
+/* ------------------------------------------------------------------ */
+/* Matrix-free tangent apply with optional Dirichlet mask (reading R9):  */
+/*   A v = (I - M) K (I - M) v + M v                                      */
+/* u: NH state [S][N][d] (ignored for linear, may be NULL)                */
+/* ------------------------------------------------------------------ */
+int oracle_tangent(int dim, int64_t n_nodes, int64_t n_elems, const int32_t* conn,
+                   const double* grad, const double* vol, int model, const double* mu,
+                   const double* lam, int n_samples, const double* u, const double* v,
+                   const uint8_t* mask, double* Kv) {
+    const int nv = dim + 1, ne = nv * dim;
+    double* fe = (double*)malloc(sizeof(double) * (size_t)n_elems * ne);
+    if (!fe) return OR_ERR_CAPACITY;
+    int64_t first_bad = -1;
+    for (int s = 0; s < n_samples; ++s) {
+        const double* vs = v + (int64_t)s * n_nodes * dim;
+        const double* us = u ? u + (int64_t)s * n_nodes * dim : NULL;
+        double* out = Kv + (int64_t)s * n_nodes * dim;
+#pragma omp parallel for schedule(static)
+        for (int64_t e = 0; e < n_elems; ++e) {
+            double g[4][3], K[12][12], ve[12];
+            elem_grads(dim, grad, e, g);
+            const int32_t* c = conn + e * nv;
+            if (elem_tangent(dim, model, g, vol[e], mu[e], lam[e], c, us, K) != OR_OK) {
+#pragma omp critical
+                { if (first_bad < 0 || e < first_bad) first_bad = e; }
+            }
+            for (int a = 0; a < nv; ++a)
+                for (int i = 0; i < dim; ++i) {
+                    int64_t dof = (int64_t)c[a] * dim + i;
+                    ve[a * dim + i] = (mask && mask[dof]) ? 0.0 : vs[dof];
+                }
+            for (int p = 0; p < ne; ++p) {
+                double acc = 0.0;
+                for (int q = 0; q < ne; ++q) acc += K[p][q] * ve[q];
+                fe[e * ne + p] = acc;
+            }
+        }
+        for (int64_t k = 0; k < n_nodes * dim; ++k) out[k] = 0.0;
+        for (int64_t e = 0; e < n_elems; ++e)
+            for (int a = 0; a < nv; ++a)
+                for (int i = 0; i < dim; ++i)
+                    out[(int64_t)conn[e * nv + a] * dim + i] += fe[e * ne + a * dim + i];
+        if (mask)
+            for (int64_t k = 0; k < n_nodes * dim; ++k)
+                if (mask[k]) out[k] = vs[k];
+    }
+    free(fe);
+    if (first_bad >= 0) { g_err_index = first_bad; return OR_ERR_INVERTED; }
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* Warm-started CG (App. B; warm start P:395-417; skip rule P:419-423) */
+/* Solves A x = b with A = (I-M)K(I-M) + M, b = (I-M)(f - K x_D) + M x0, x_D = M x0 */
+/* (reading R9/R10).  Hestenes-Stiefel, unpreconditioned, stop on the   */
+/* recurrence residual ||r|| < tol ||b_free|| (reading R8), k = number of */
+/* A p products in the loop (reading R11).                               */
+/* ------------------------------------------------------------------ */
+static double dot(int64_t n, const double* a, const double* b) {
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
+    return s;
+}
+
+int oracle_cg(int dim, int64_t n_nodes, int64_t n_elems, const int32_t* conn, const double* grad,
+              const double* vol, int model, const double* mu, const double* lam,
+              const double* u_state, const double* f, const uint8_t* mask, double* x, double tol,
+              int32_t max_iter, double* history, int32_t* iterations, double* rel_res0,
+              double* rel_res_final, double* true_rel_res_final) {
+    const int64_t n = n_nodes * dim;
+    double* r = (double*)malloc(sizeof(double) * n);
+    double* p = (double*)malloc(sizeof(double) * n);
+    double* q = (double*)malloc(sizeof(double) * n);
+    double* xd = (double*)malloc(sizeof(double) * n);
+    double* b = (double*)malloc(sizeof(double) * n);
+    if (!r || !p || !q || !xd || !b) return OR_ERR_CAPACITY;
+    int st = OR_OK;
+    /* b = (I - M)(f - K x_D): K x_D via the unmasked operator */
+    for (int64_t i = 0; i < n; ++i) xd[i] = (mask && mask[i]) ? x[i] : 0.0;
+    oracle_tangent(dim, n_nodes, n_elems, conn, grad, vol, model, mu, lam, 1, u_state, xd, NULL, q);
+    for (int64_t i = 0; i < n; ++i) b[i] = (mask && mask[i]) ? 0.0 : f[i] - q[i];
+    double bnorm = sqrt(dot(n, b, b));
+    /* r = b - A x over free DOFs (constrained rows of A x - (M x0) vanish) */
+    oracle_tangent(dim, n_nodes, n_elems, conn, grad, vol, model, mu, lam, 1, u_state, x, mask, q);
+    for (int64_t i = 0; i < n; ++i) r[i] = (mask && mask[i]) ? 0.0 : b[i] - q[i];
+    double rho = dot(n, r, r);
+    *iterations = 0;
+    *rel_res0 = bnorm > 0 ? sqrt(rho) / bnorm : 0.0;
+    if (history) history[0] = *rel_res0;
+    int32_t k = 0;
+    if (bnorm == 0.0) {
+        for (int64_t i = 0; i < n; ++i) x[i] = (mask && mask[i]) ? x[i] : 0.0;
+        *rel_res_final = 0.0;
+        rho = 0.0;
+    } else if (sqrt(rho) < tol * bnorm) {
+        /* skip rule: the supplied guess already satisfies the test */
+    } else {
+        memcpy(p, r, sizeof(double) * n);
+        st = OR_ERR_NOT_CONVERGED;
+        for (k = 1; k <= max_iter; ++k) {
+            oracle_tangent(dim, n_nodes, n_elems, conn, grad, vol, model, mu, lam, 1, u_state, p, mask, q);
+            double pi = dot(n, p, q);
+            if (!(pi > 0.0)) { st = OR_ERR_BREAKDOWN; break; }
+            double alpha = rho / pi;
+            for (int64_t i = 0; i < n; ++i) x[i] += alpha * p[i];
+            for (int64_t i = 0; i < n; ++i) r[i] -= alpha * q[i];
+            double rho_new = dot(n, r, r);
+            if (history) history[k] = sqrt(rho_new) / bnorm;
+            if (sqrt(rho_new) < tol * bnorm) { rho = rho_new; st = OR_OK; break; }
+            double beta = rho_new / rho;
+            for (int64_t i = 0; i < n; ++i) p[i] = r[i] + beta * p[i];
+            rho = rho_new;
+        }
+        if (k > max_iter) k = max_iter;
+    }
+    *iterations = k;
+    *rel_res_final = bnorm > 0 ? sqrt(rho) / bnorm : 0.0;
+    /* true residual ||b - A x|| / ||b|| over free DOFs */
+    oracle_tangent(dim, n_nodes, n_elems, conn, grad, vol, model, mu, lam, 1, u_state, x, mask, q);
+    double tr = 0.0;
+    for (int64_t i = 0; i < n; ++i)
+        if (!(mask && mask[i])) tr += (b[i] - q[i]) * (b[i] - q[i]);
+    *true_rel_res_final = bnorm > 0 ? sqrt(tr) / bnorm : 0.0;
+    free(r); free(p); free(q); free(xd); free(b);
+    return st;
+}
