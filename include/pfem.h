@@ -1,0 +1,248 @@
+/*
+ * pfem.h — C-ABI of the B200-native PFEM hot path (arXiv 2601.03086, "Pretrained
+ * Finite Element Method"): explicit finite-element differentiation of displacement
+ * fields on P1 simplex meshes (T3 / T4), element and total strain energy, the
+ * assembled internal force, the matrix-free tangent product and a warm-started CG.
+ *
+ * Citations are PAPER.md line numbers ("P:n") with their section; readings of
+ * ambiguous passages are numbered R1.. in DESIGN.md §3.
+ *
+ * Conventions for every call
+ *  - All array arguments are DEVICE pointers (CUDA global memory) unless a comment
+ *    says "host".  The caller owns them (e.g. torch.empty on cuda); the library only
+ *    allocates device memory inside pfem_mesh_prepare (the opaque plan, released by
+ *    pfem_mesh_release) — never on the hot path.
+ *  - `stream` is a cudaStream_t (passed as void*); every hot-path call is
+ *    asynchronous on it.  pfem_mesh_prepare and pfem_cg synchronise the stream once
+ *    to return host-side counts / reports.
+ *  - Node fields are [S][N][d] (sample-major), contiguous inside a sample, with an
+ *    explicit sample stride in ELEMENTS (not bytes).  Element arrays are SoA.
+ *  - Floating point arrays have the dtype of the call (pfem_dtype).  Integers are
+ *    int32.
+ *  - Return value: PFEM_OK (0) or a negative pfem_status.  Argument / launch errors
+ *    are returned synchronously; pfem_last_error() gives a message and
+ *    pfem_last_error_index() the offending element / node (or -1).  Both are
+ *    thread-local.  Data-dependent conditions of the asynchronous hot path (inverted
+ *    Neo-Hookean elements, non-finite values) are reported through the optional
+ *    device struct pfem_flags, written by the call.
+ *  - No floating-point atomics: every sum has a fixed order, so two runs of the same
+ *    call on the same inputs are bitwise identical.
+ */
+#ifndef PFEM_H
+#define PFEM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PFEM_ABI_VERSION 1
+
+typedef enum {
+    PFEM_OK = 0,
+    PFEM_ERR_ARG = -1,           /* bad pointer / enum / size / connectivity out of range */
+    PFEM_ERR_DEGENERATE = -2,    /* |det J_e| <= 64 eps_f64 prod |edges|; index = element */
+    PFEM_ERR_INVERTED = -3,      /* reserved (NH inversion is reported via pfem_flags)    */
+    PFEM_ERR_NOT_CONVERGED = -4, /* CG hit max_iter; x holds the partial iterate          */
+    PFEM_ERR_BREAKDOWN = -5,     /* CG: p.Ap <= 0 (operator not SPD on the free DOFs)     */
+    PFEM_ERR_CAPACITY = -6,      /* workspace / colour capacity too small                  */
+    PFEM_ERR_CUDA = -7,          /* CUDA runtime error (message in pfem_last_error)        */
+    PFEM_ERR_NOT_PREPARED = -8   /* mesh has no plan: call pfem_mesh_prepare first         */
+} pfem_status;
+
+typedef enum { PFEM_F32 = 0, PFEM_F64 = 1 } pfem_dtype;
+
+/* Strain-energy density (§4.1; §4.2). */
+typedef enum {
+    PFEM_LINEAR = 0,     /* psi = 1/2 sigma:eps, sigma = 2 mu eps + lam tr(eps) I            */
+    PFEM_NEOHOOKEAN = 1  /* psi = 1/2 lam (ln J)^2 - mu ln J + 1/2 mu (I1 - d)  (reading R2) */
+} pfem_model;
+
+/* Material parameter kind.  2-D runs are plane strain unless
+ * PFEM_YOUNG_POISSON_PLANE_STRESS (lam* = 2 mu lam / (lam + 2 mu)) — reading R1. */
+typedef enum {
+    PFEM_LAME = 0,                       /* p0 = mu, p1 = lambda */
+    PFEM_YOUNG_POISSON = 1,              /* p0 = E,  p1 = nu      */
+    PFEM_YOUNG_POISSON_PLANE_STRESS = 2  /* p0 = E,  p1 = nu      */
+} pfem_param;
+
+/* Deterministic assembly of element contributions into nodes (north star: never float
+ * atomics on the reported path). */
+typedef enum {
+    PFEM_ASSEMBLE_CSR = 0,    /* block-partitioned CSR gather: every node sums its (element,
+                                 slot) entries in ascending element order, segment by segment
+                                 over the element blocks touching it        */
+    PFEM_ASSEMBLE_COLOUR = 1  /* colour-ordered scatter: one pass per colour of the greedy
+                                 element colouring, one non-atomic read-modify-write per
+                                 (element, slot)                                              */
+} pfem_assembly;
+
+typedef struct pfem_plan pfem_plan;   /* opaque, library-owned device data */
+
+/* Mesh descriptor.  Inputs are set by the caller; pfem_mesh_prepare fills the outputs. */
+typedef struct {
+    /* ---- inputs ---- */
+    int32_t dim;                   /* 2 (T3) or 3 (T4)                                          */
+    int32_t n_nodes, n_elems;
+    int32_t n_parts;               /* >= 1: independent meshes concatenated (config 5)          */
+    int32_t dtype;                 /* pfem_dtype of grad / vol and of every field call          */
+    int32_t block_elems;           /* assembly block size (elements); 0 = library default       */
+    const double* coords;          /* [n_nodes][dim], float64 always                             */
+    const int32_t* conn;           /* [n_elems][dim+1], node ids in [0, n_nodes)                 */
+    const int32_t* part_elem;      /* [n_parts+1] element offsets (device), NULL if n_parts == 1 */
+    const int32_t* part_node;      /* [n_parts+1] node offsets (device),    NULL if n_parts == 1 */
+    /* ---- outputs of pfem_mesh_prepare (device, caller-allocated) ---- */
+    void* grad;                    /* [dim*dim][n_elems] SoA: grad[(a*dim + j)*E + e] = dN_{a+1}/dX_j,
+                                      rows of J_e^{-1}, J_e = [X_1-X_0 | .. | X_d-X_0]
+                                      (P1 shape functions, App. B; dN_0 = -sum)      */
+    void* vol;                     /* [n_elems] V_e = |det J_e| / d!                             */
+    int32_t* csr_ptr;              /* [n_nodes+1] node -> (element, slot) CSR row offsets       */
+    int32_t* csr_ent;              /* [(dim+1)*n_elems] e*(dim+1)+slot, ascending per row (R12)  */
+    int32_t* colour;               /* [n_elems] greedy first-fit colour in element order (R12)   */
+    int32_t* colour_elems;         /* [n_elems] elements sorted by (colour, element)             */
+    int32_t* colour_ptr;           /* [max_colours+1] offsets into colour_elems                  */
+    int32_t max_colours;           /* capacity of colour_ptr - 1 (<= 128)                        */
+    /* ---- host outputs of pfem_mesh_prepare ---- */
+    int32_t n_colours;
+    int32_t n_negative;            /* elements with det J_e < 0 (valid; gradients are exact)    */
+    int32_t n_blocks;              /* assembly blocks of the plan                                */
+    int32_t n_occ;                 /* (block, node) occurrences of the plan                      */
+    pfem_plan* plan;               /* set by prepare; free with pfem_mesh_release                */
+} pfem_mesh;
+
+/* Material: per-element parameters with an element stride each (stride 0 = uniform).
+ * Arrays have the call's dtype. */
+typedef struct {
+    int32_t model;                 /* pfem_model */
+    int32_t kind;                  /* pfem_param */
+    const void* p0;
+    const void* p1;
+    int64_t stride0, stride1;      /* in elements; 0 broadcasts p0[0] / p1[0] */
+} pfem_material;
+
+/* Device-side report of data-dependent conditions, written (not accumulated) by every
+ * hot-path call that receives it. */
+typedef struct {
+    int32_t n_inverted;            /* Neo-Hookean elements with J = det F <= 0 (NaN energy)  */
+    int32_t first_inverted;        /* lowest such element id, or -1                           */
+    int32_t n_nonfinite;           /* elements whose energy density or stress is not finite    */
+    int32_t reserved;
+} pfem_flags;
+
+/* ---------------------------------------------------------------------------------
+ * Mesh preparation (one-time per mesh; §8 row a1).
+ * Computes, on the GPU: shape-function gradients and volumes (fp64 arithmetic, stored
+ * in m->dtype), the node->(element,slot) CSR, the greedy element colouring and its
+ * colour-sorted list, and the assembly plan (element blocks, block-local CSR, node
+ * occurrences).  Errors: PFEM_ERR_ARG (sizes, null pointers, conn out of range, index
+ * = element), PFEM_ERR_DEGENERATE (index = lowest degenerate element),
+ * PFEM_ERR_CAPACITY (more than max_colours colours).  Synchronises `stream`.
+ * Re-preparing a mesh that already has a plan releases the old plan first.
+ * --------------------------------------------------------------------------------- */
+pfem_status pfem_mesh_prepare(pfem_mesh* m, void* stream);
+void pfem_mesh_release(pfem_mesh* m);
+
+/* Device copies of the plan arrays, for tests (host pointers to fill, each may be NULL).
+ * Sizes: blk_elem [n_blocks+1], blk_occ [n_blocks+1], occ_node [n_occ] (node id | kind
+ * bits 30..31), occ_ent_ptr [n_occ+1], loc_ent [(dim+1)*n_elems] (uint16). */
+pfem_status pfem_plan_export(const pfem_mesh* m, int32_t* blk_elem, int32_t* blk_occ,
+                             int32_t* occ_node, int32_t* occ_ent_ptr, uint16_t* loc_ent);
+
+/* Bytes of the per-call workspace of pfem_energy / pfem_residual / pfem_tangent_apply
+ * for `n_samples` fields.  The workspace must be ZERO-FILLED before its first use; the
+ * library keeps it consistent afterwards.  Calls sharing a workspace must be ordered on
+ * one stream. */
+size_t pfem_workspace_bytes(const pfem_mesh* m, int32_t n_samples);
+
+/* Material conversion (E, nu) -> (mu, lambda)  (§8 K8).  out arrays [n]. */
+pfem_status pfem_lame(int32_t dtype, int32_t kind, int64_t n, const void* p0, int64_t stride0,
+                      const void* p1, int64_t stride1, void* mu, void* lam, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * Energy (and optionally the fused residual) of S displacement fields on one mesh.
+ * §8 rows a2-a5.  Per element e and sample s:
+ *   H = sum_{a=1..d} (u_{v_a} - u_{v_0}) (x) grad N_a,  F = I + H,
+ *   W_e = V_e psi(H),   totals[s][k] = sum_{e in part k} W_e  - [f_ext given] sum_{n in part k} f_ext,n . u_n
+ *   (the potential energy Pi = W - f.u of P:518-524 when f_ext is given; reading R6)
+ * and, if residual != NULL, the internal force f_int (App. B):
+ *   residual[s][n] = sum_{(e,a): v_a(e) = n} V_e P_e grad N_a
+ * with P the first Piola-Kirchhoff stress (linear: sigma).  The solver residual is
+ * f_int - f_ext (reading R7).
+ * Arguments:
+ *   u            [S][N][d], element stride `sample_stride` between samples
+ *   f_ext        nullable [N][d] (shared by all samples)
+ *   elem_energy  nullable [S][E]
+ *   totals       [S][n_parts]
+ *   residual     nullable [S][N][d] (same sample stride as u)
+ *   mode         pfem_assembly
+ *   flags        nullable device pfem_flags
+ *   ws, ws_bytes per-call workspace (pfem_workspace_bytes), zero-filled before first use
+ * --------------------------------------------------------------------------------- */
+pfem_status pfem_energy(const pfem_mesh* m, const pfem_material* mat, int32_t n_samples,
+                        const void* u, int64_t sample_stride, const void* f_ext,
+                        void* elem_energy, void* totals, void* residual, int32_t mode,
+                        pfem_flags* flags, void* ws, size_t ws_bytes, void* stream);
+
+/* Internal force only (no energy arithmetic), see pfem_energy. */
+pfem_status pfem_residual(const pfem_mesh* m, const pfem_material* mat, int32_t n_samples,
+                          const void* u, int64_t sample_stride, void* residual, int32_t mode,
+                          pfem_flags* flags, void* ws, size_t ws_bytes, void* stream);
+
+/* Matrix-free tangent K(u) v (App. B; §8 row a6):
+ *   linear: dP = 2 mu sym(dH) + lam tr(dH) I            (u ignored, may be NULL)
+ *   NH:     dP = mu dH + (mu - lam ln J) F^-T dH^T F^-T + lam tr(F^-1 dH) F^-T,  F = I + grad u
+ *   (Kv)_n = sum_{(e,a): v_a(e)=n} V_e dP_e grad N_a,  dH = sum_a (v_{v_a} - v_{v_0}) (x) grad N_a
+ * With dirichlet_mask (nullable [N*d] uint8, 1 = constrained DOF) the call applies the
+ * SPD masked operator (I-M) K (I-M) v + M v (reading R9).
+ * u, v, Kv: [S][N][d] with the same sample stride. */
+pfem_status pfem_tangent_apply(const pfem_mesh* m, const pfem_material* mat, int32_t n_samples,
+                               const void* u, const void* v, void* Kv, int64_t sample_stride,
+                               const uint8_t* dirichlet_mask, int32_t mode, pfem_flags* flags,
+                               void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * Warm-started conjugate gradient (App. B; warm start P:395-417; skip rule
+ * P:419-423; §8 row a7).  Solves A x = b on one field (S = 1):
+ *   A = (I-M) K(u_state) (I-M) + M,   b = (I-M)(rhs - K x_D) + M x0,   x_D = M x0
+ * Hestenes-Stiefel CG, unpreconditioned (reading R9), stop when the recurrence residual
+ * satisfies ||r_k|| < tol ||b_free|| (strict, relative; reading R8).  iterations = number
+ * of A p products (R11); 0 if x0 already satisfies the test.
+ *   u_state  nullable [N][d] NH linearisation point (NULL for linear)
+ *   rhs      [N][d] external force f_ext
+ *   mask     nullable [N*d]
+ *   x        in: x0 (constrained entries = prescribed values); out: solution / partial
+ *   history  nullable device double [max_iter+1]: ||r_k|| / ||b_free||
+ *   report   host
+ * Synchronises `stream`.  Returns PFEM_OK, PFEM_ERR_NOT_CONVERGED or PFEM_ERR_BREAKDOWN
+ * (report filled in all three cases).
+ * --------------------------------------------------------------------------------- */
+typedef struct {
+    int32_t iterations;
+    int32_t converged;
+    int32_t status;
+    int32_t reserved;
+    double rel_res0;           /* ||r_0|| / ||b_free||                          */
+    double rel_res_final;      /* recurrence residual at exit                   */
+    double true_rel_res_final; /* ||b - A x|| / ||b_free|| recomputed at exit   */
+    double bnorm;              /* ||b_free||                                    */
+} pfem_cg_report;
+
+size_t pfem_cg_workspace_bytes(const pfem_mesh* m);
+pfem_status pfem_cg(const pfem_mesh* m, const pfem_material* mat, const void* u_state,
+                    const void* rhs, const uint8_t* mask, void* x, double tol, int32_t max_iter,
+                    int32_t mode, double* history, pfem_cg_report* report, void* ws,
+                    size_t ws_bytes, void* stream);
+
+/* Diagnostics */
+const char* pfem_last_error(void);
+int64_t pfem_last_error_index(void);
+int32_t pfem_abi_version(void);
+/* number of kernel launches issued by this thread since the last reset (bench evidence) */
+int64_t pfem_launch_count(int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PFEM_H */

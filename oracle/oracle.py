@@ -189,8 +189,10 @@ class Mesh:
         _check(st, "tangent")
         return out
 
-    def cg(self, f, mask, x0, tol=1e-8, max_iter=50000, u_state=None, history=True):
-        """Warm-started masked CG; returns (x, report dict)."""
+    def cg(self, f, mask, x0, tol=1e-8, max_iter=50000, u_state=None, history=True, dot_order=0):
+        """Warm-started masked CG; returns (x, report dict).  dot_order 0/1/2 = ascending /
+        descending / pairwise sums in the dot products (reading R18: the oracle's own spread)."""
+        lib().oracle_set_dot_order(C.c_int(dot_order))
         x = _f64(x0).copy().reshape(-1)
         f = _f64(f).reshape(-1)
         m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8).reshape(-1)
@@ -204,7 +206,13 @@ class Mesh:
         rep = {"status": st, "iterations": it.value, "converged": st == OK, "rel_res0": r0.value,
                "rel_res_final": rf.value, "true_rel_res_final": tr.value,
                "history": None if hist is None else hist[: it.value + 1].copy()}
+        lib().oracle_set_dot_order(C.c_int(0))
         return x.reshape(np.shape(x0)), rep
+
+    def cg_spread(self, f, mask, x0, tol=1e-8, max_iter=50000, u_state=None):
+        """Iteration counts of the oracle CG under the five dot-product orders (R18)."""
+        return [self.cg(f, mask, x0, tol, max_iter, u_state, history=False, dot_order=o)[1]["iterations"]
+                for o in (0, 1, 2, 3, 4)]
 
 
 def prepare(coords, conn, model: str, param_kind: str, p0, p1, part_elem=None, part_node=None) -> Mesh:

@@ -565,11 +565,52 @@ int oracle_tangent(int dim, int64_t n_nodes, int64_t n_elems, const int32_t* con
 /* recurrence residual ||r|| < tol ||b_free|| (reading R8), k = number of */
 /* A p products in the loop (reading R11).                               */
 /* ------------------------------------------------------------------ */
+/* dot product; order 0: sequential ascending (default), 1: sequential descending,
+ * 2: pairwise (recursive halving), 3: blocked (sums of 1024-term ascending blocks),
+ * 4: compensated (Kahan).  Orders 1-4 exist only to measure the oracle's own
+ * iteration-count spread under valid re-orderings of the sums (reading R18). */
+static int g_dot_order = 0;
+
+static double dot_pairwise(int64_t n, const double* a, const double* b) {
+    if (n <= 8) {
+        double s = 0.0;
+        for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
+        return s;
+    }
+    int64_t h = n / 2;
+    return dot_pairwise(h, a, b) + dot_pairwise(n - h, a + h, b + h);
+}
+
 static double dot(int64_t n, const double* a, const double* b) {
     double s = 0.0;
+    if (g_dot_order == 1) {
+        for (int64_t i = n - 1; i >= 0; --i) s += a[i] * b[i];
+        return s;
+    }
+    if (g_dot_order == 2) return dot_pairwise(n, a, b);
+    if (g_dot_order == 3) {
+        for (int64_t i0 = 0; i0 < n; i0 += 1024) {
+            double t = 0.0;
+            for (int64_t i = i0; i < n && i < i0 + 1024; ++i) t += a[i] * b[i];
+            s += t;
+        }
+        return s;
+    }
+    if (g_dot_order == 4) {
+        double c = 0.0;
+        for (int64_t i = 0; i < n; ++i) {
+            double y = a[i] * b[i] - c;
+            double t = s + y;
+            c = (t - s) - y;
+            s = t;
+        }
+        return s;
+    }
     for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
     return s;
 }
+
+void oracle_set_dot_order(int order) { g_dot_order = order; }
 
 int oracle_cg(int dim, int64_t n_nodes, int64_t n_elems, const int32_t* conn, const double* grad,
               const double* vol, int model, const double* mu, const double* lam,

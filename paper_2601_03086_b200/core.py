@@ -1,0 +1,253 @@
+"""Thin torch-facing wrappers of the C-ABI (same names as include/pfem.h without the
+``pfem_`` prefix).  torch supplies device memory and the current stream; every
+computation runs in libpfem's CUDA kernels.  Nothing here computes the method.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib as L
+
+_DT = {torch.float32: L.F32, torch.float64: L.F64}
+_TD = {L.F32: torch.float32, L.F64: torch.float64}
+MODES = {"csr": L.ASSEMBLE_CSR, "colour": L.ASSEMBLE_COLOUR, "color": L.ASSEMBLE_COLOUR}
+MODELS = {"linear": L.LINEAR, "neohookean": L.NEOHOOKEAN}
+KINDS = {"lame": L.LAME, "young_poisson": L.YOUNG_POISSON,
+         "young_poisson_plane_stress": L.YOUNG_POISSON_PLANE_STRESS}
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("libpfem takes CUDA tensors only (no CPU fallback)")
+
+
+class Mesh:
+    """A prepared mesh (pfem_mesh_prepare): geometry, CSR, colouring and assembly plan."""
+
+    def __init__(self, coords: torch.Tensor, conn: torch.Tensor, dtype=torch.float64, part_elem=None,
+                 part_node=None, block_elems: int = 0, max_colours: int = 128, stream=None):
+        lib = L.load()
+        _require_cuda(coords, conn)
+        dev = coords.device
+        self.coords = coords.to(torch.float64).contiguous()
+        self.conn = conn.to(torch.int32).contiguous()
+        N, d = self.coords.shape
+        E = self.conn.shape[0]
+        if self.conn.shape[1] != d + 1:
+            raise ValueError("conn must be [E, dim+1]")
+        self.dim, self.n_nodes, self.n_elems = d, N, E
+        self.dtype = dtype
+        K = 1
+        self.part_elem = self.part_node = None
+        if part_elem is not None:
+            self.part_elem = torch.as_tensor(part_elem, dtype=torch.int32, device=dev).contiguous()
+            self.part_node = torch.as_tensor(part_node, dtype=torch.int32, device=dev).contiguous()
+            K = self.part_elem.numel() - 1
+        self.n_parts = K
+        self.grad = torch.empty((d * d, E), dtype=dtype, device=dev)
+        self.vol = torch.empty(E, dtype=dtype, device=dev)
+        self.csr_ptr = torch.empty(N + 1, dtype=torch.int32, device=dev)
+        self.csr_ent = torch.empty(E * (d + 1), dtype=torch.int32, device=dev)
+        self.colour = torch.empty(E, dtype=torch.int32, device=dev)
+        self.colour_elems = torch.empty(E, dtype=torch.int32, device=dev)
+        self.colour_ptr = torch.empty(max_colours + 1, dtype=torch.int32, device=dev)
+        m = L.pfem_mesh()
+        m.dim, m.n_nodes, m.n_elems, m.n_parts = d, N, E, K
+        m.dtype = _DT[dtype]
+        m.block_elems = block_elems
+        m.coords, m.conn = self.coords.data_ptr(), self.conn.data_ptr()
+        m.part_elem = self.part_elem.data_ptr() if self.part_elem is not None else None
+        m.part_node = self.part_node.data_ptr() if self.part_node is not None else None
+        m.grad, m.vol = self.grad.data_ptr(), self.vol.data_ptr()
+        m.csr_ptr, m.csr_ent = self.csr_ptr.data_ptr(), self.csr_ent.data_ptr()
+        m.colour, m.colour_elems, m.colour_ptr = (self.colour.data_ptr(), self.colour_elems.data_ptr(),
+                                                 self.colour_ptr.data_ptr())
+        m.max_colours = max_colours
+        self._m = m
+        L.check(lib.pfem_mesh_prepare(C.byref(m), _stream(stream)))
+        self._ws = {}
+
+    # ------------------------------------------------------------------ info
+    @property
+    def n_colours(self):
+        return self._m.n_colours
+
+    @property
+    def n_negative(self):
+        return self._m.n_negative
+
+    @property
+    def n_blocks(self):
+        return self._m.n_blocks
+
+    @property
+    def n_occ(self):
+        return self._m.n_occ
+
+    def ref(self):
+        return C.byref(self._m)
+
+    def workspace(self, n_samples: int) -> torch.Tensor:
+        """Zero-filled per-call workspace, cached per sample count (pfem_workspace_bytes)."""
+        ws = self._ws.get(n_samples)
+        if ws is None:
+            nb = L.load().pfem_workspace_bytes(self.ref(), n_samples)
+            ws = torch.zeros(max(nb, 1), dtype=torch.uint8, device=self.coords.device)
+            self._ws[n_samples] = ws
+        return ws
+
+    def cg_workspace(self) -> torch.Tensor:
+        ws = self._ws.get("cg")
+        if ws is None:
+            nb = L.load().pfem_cg_workspace_bytes(self.ref())
+            ws = torch.zeros(max(nb, 1), dtype=torch.uint8, device=self.coords.device)
+            self._ws["cg"] = ws
+        return ws
+
+    def plan_export(self):
+        """Host copies of the assembly plan (tests)."""
+        import numpy as np
+        nb, no = self.n_blocks, self.n_occ
+        be = np.zeros(nb + 1, np.int32)
+        bo = np.zeros(nb + 1, np.int32)
+        on = np.zeros(no, np.int32)
+        oe = np.zeros(no + 1, np.int32)
+        le = np.zeros(self.n_elems * (self.dim + 1), np.uint16)
+        torch.cuda.synchronize()
+        L.check(L.load().pfem_plan_export(self.ref(), be.ctypes.data, bo.ctypes.data, on.ctypes.data,
+                                          oe.ctypes.data, le.ctypes.data))
+        return {"blk_elem": be, "blk_occ": bo, "occ_node": on, "occ_ent_ptr": oe, "loc_ent": le}
+
+    def release(self):
+        if getattr(self, "_m", None) is not None and self._m.plan:
+            L.load().pfem_mesh_release(C.byref(self._m))
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
+
+
+@dataclass
+class Material:
+    """pfem_material: per-element (or uniform, numel 1) parameter tensors."""
+    model: str
+    kind: str
+    p0: torch.Tensor
+    p1: torch.Tensor
+
+    def c(self):
+        m = L.pfem_material()
+        m.model = MODELS[self.model]
+        m.kind = KINDS[self.kind]
+        m.p0, m.p1 = self.p0.data_ptr(), self.p1.data_ptr()
+        m.stride0 = 0 if self.p0.numel() == 1 else 1
+        m.stride1 = 0 if self.p1.numel() == 1 else 1
+        return m
+
+
+def _field(mesh: Mesh, t: torch.Tensor):
+    if t.dtype != mesh.dtype:
+        raise TypeError(f"field dtype {t.dtype} != mesh dtype {mesh.dtype}")
+    _require_cuda(t)
+    t = t.contiguous()
+    if t.dim() == 2:
+        t = t.unsqueeze(0)
+    return t
+
+
+def lame(kind: str, p0: torch.Tensor, p1: torch.Tensor, n: int):
+    """pfem_lame: (mu, lambda) per element on the GPU."""
+    _require_cuda(p0, p1)
+    mu = torch.empty(n, dtype=p0.dtype, device=p0.device)
+    lam = torch.empty_like(mu)
+    L.check(L.load().pfem_lame(_DT[p0.dtype], KINDS[kind], n, _ptr(p0), 0 if p0.numel() == 1 else 1, _ptr(p1),
+                               0 if p1.numel() == 1 else 1, _ptr(mu), _ptr(lam), _stream()))
+    return mu, lam
+
+
+def energy(mesh: Mesh, mat: Material, u: torch.Tensor, f_ext=None, elem_energy=False, residual=False,
+           mode: str = "csr", flags=None, out=None):
+    """pfem_energy: totals [S, K] (and W_e [S, E], residual [S, N, d] if requested)."""
+    u = _field(mesh, u)
+    S = u.shape[0]
+    dev = u.device
+    totals = torch.empty((S, mesh.n_parts), dtype=mesh.dtype, device=dev) if out is None else out[0]
+    W = (torch.empty((S, mesh.n_elems), dtype=mesh.dtype, device=dev) if elem_energy else None)
+    r = torch.empty_like(u) if residual else None
+    if out is not None:
+        W = out[1] if elem_energy else None
+        r = out[2] if residual else None
+    ws = mesh.workspace(S)
+    mc = mat.c()
+    L.check(L.load().pfem_energy(mesh.ref(), C.byref(mc), S, _ptr(u), u[0].numel(), _ptr(f_ext), _ptr(W),
+                                 _ptr(totals), _ptr(r), MODES[mode], _ptr(flags), _ptr(ws), ws.numel(),
+                                 _stream()))
+    return totals, W, r
+
+
+def residual(mesh: Mesh, mat: Material, u: torch.Tensor, mode: str = "csr", flags=None, out=None):
+    """pfem_residual: internal force f_int(u) [S, N, d]."""
+    u = _field(mesh, u)
+    S = u.shape[0]
+    r = torch.empty_like(u) if out is None else out
+    ws = mesh.workspace(S)
+    mc = mat.c()
+    L.check(L.load().pfem_residual(mesh.ref(), C.byref(mc), S, _ptr(u), u[0].numel(), _ptr(r), MODES[mode],
+                                   _ptr(flags), _ptr(ws), ws.numel(), _stream()))
+    return r
+
+
+def tangent_apply(mesh: Mesh, mat: Material, v: torch.Tensor, u=None, mask=None, mode: str = "csr",
+                  flags=None, out=None):
+    """pfem_tangent_apply: K(u) v [S, N, d]; with mask: (I-M) K (I-M) v + M v."""
+    v = _field(mesh, v)
+    S = v.shape[0]
+    if u is not None:
+        u = _field(mesh, u)
+    Kv = torch.empty_like(v) if out is None else out
+    ws = mesh.workspace(S)
+    mc = mat.c()
+    L.check(L.load().pfem_tangent_apply(mesh.ref(), C.byref(mc), S, _ptr(u), _ptr(v), _ptr(Kv), v[0].numel(),
+                                        _ptr(mask), MODES[mode], _ptr(flags), _ptr(ws), ws.numel(), _stream()))
+    return Kv
+
+
+def cg(mesh: Mesh, mat: Material, f: torch.Tensor, x0: torch.Tensor, mask=None, tol: float = 1e-8,
+       max_iter: int = 50000, u_state=None, mode: str = "csr", history: bool = True):
+    """pfem_cg: warm-started CG; returns (x, report dict with history)."""
+    f = _field(mesh, f)[0]
+    x = _field(mesh, x0)[0].clone()
+    if u_state is not None:
+        u_state = _field(mesh, u_state)[0]
+    hist = torch.zeros(max_iter + 1, dtype=torch.float64, device=x.device) if history else None
+    rep = L.pfem_cg_report()
+    ws = mesh.cg_workspace()
+    mc = mat.c()
+    st = L.load().pfem_cg(mesh.ref(), C.byref(mc), _ptr(u_state), _ptr(f), _ptr(mask), _ptr(x), tol, max_iter,
+                          MODES[mode], _ptr(hist), C.byref(rep), _ptr(ws), ws.numel(), _stream())
+    report = {"status": st, "iterations": rep.iterations, "converged": bool(rep.converged),
+              "rel_res0": rep.rel_res0, "rel_res_final": rep.rel_res_final,
+              "true_rel_res_final": rep.true_rel_res_final, "bnorm": rep.bnorm,
+              "history": None if hist is None else hist[: rep.iterations + 1].cpu().numpy()}
+    if st not in (L.PFEM_OK, -4, -5):
+        L.check(st)
+    return x, report
+
+
+def launch_count(reset: bool = False) -> int:
+    return int(L.load().pfem_launch_count(1 if reset else 0))

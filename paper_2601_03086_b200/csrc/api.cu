@@ -1,0 +1,263 @@
+// api.cu — the extern "C" boundary (include/pfem.h): argument validation, thread-local
+// errors, dispatch to the kernels.  No arithmetic of the method happens on the host.
+#include <cstdio>
+#include <cstring>
+
+#include "launch.cuh"
+
+namespace pfem {
+
+static thread_local std::string g_err;
+static thread_local int64_t g_err_index = -1;
+static thread_local int64_t g_launches = 0;
+
+void set_error(const std::string& msg, int64_t index) {
+    g_err = msg;
+    g_err_index = index;
+}
+
+pfem_status cuda_status(cudaError_t e, const char* what) {
+    set_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+    return PFEM_ERR_CUDA;
+}
+
+void count_launch(int n) { g_launches += n; }
+
+pfem_status prepare_impl(pfem_mesh* m, cudaStream_t s);
+void release_impl(pfem_mesh* m);
+size_t cg_ws_bytes(const Plan& P, int dtype);
+pfem_status run_cg(const pfem_mesh* m, const pfem_material* mat, const void* u_state, const void* rhs,
+                   const uint8_t* mask, void* x, double tol, int max_iter, int mode, double* history,
+                   pfem_cg_report* rep, void* ws, cudaStream_t s);
+
+template <class T>
+__global__ void k_lame(int64_t n, int kind, const T* p0, int64_t s0, const T* p1, int64_t s1, T* mu, T* lam) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    T m, l;
+    lame_of<T>(kind, p0[i * s0], p1[i * s1], m, l);
+    mu[i] = m;
+    lam[i] = l;
+}
+
+static pfem_status check_mesh(const pfem_mesh* m, bool need_plan) {
+    (void)cudaGetLastError();   // clear stale non-sticky runtime errors of earlier calls
+    if (!m) { set_error("mesh is NULL"); return PFEM_ERR_ARG; }
+    if (m->dim != 2 && m->dim != 3) { set_error("dim must be 2 or 3"); return PFEM_ERR_ARG; }
+    if (m->dtype != PFEM_F32 && m->dtype != PFEM_F64) { set_error("bad dtype"); return PFEM_ERR_ARG; }
+    if (m->n_nodes <= 0 || m->n_elems <= 0 || m->n_parts <= 0) {
+        set_error("n_nodes, n_elems and n_parts must be positive");
+        return PFEM_ERR_ARG;
+    }
+    if (need_plan && !m->plan) { set_error("mesh not prepared"); return PFEM_ERR_NOT_PREPARED; }
+    return PFEM_OK;
+}
+
+static pfem_status check_mat(const pfem_material* mat) {
+    if (!mat || !mat->p0 || !mat->p1) { set_error("material arrays are NULL"); return PFEM_ERR_ARG; }
+    if (mat->model != PFEM_LINEAR && mat->model != PFEM_NEOHOOKEAN) { set_error("bad model"); return PFEM_ERR_ARG; }
+    if (mat->kind < 0 || mat->kind > 2) { set_error("bad material kind"); return PFEM_ERR_ARG; }
+    if (mat->stride0 < 0 || mat->stride1 < 0) { set_error("negative material stride"); return PFEM_ERR_ARG; }
+    return PFEM_OK;
+}
+
+static pfem_status run(const Call& c) {
+    const int D = c.m->dim;
+    if (D == 2) return c.m->dtype == PFEM_F32 ? run_assemble<2, float>(c) : run_assemble<2, double>(c);
+    return c.m->dtype == PFEM_F32 ? run_assemble<3, float>(c) : run_assemble<3, double>(c);
+}
+
+static pfem_status common_checks(const pfem_mesh* m, const pfem_material* mat, int S, int64_t sstride, int mode,
+                                 void* ws, size_t ws_bytes) {
+    pfem_status st = check_mesh(m, true);
+    if (st) return st;
+    if ((st = check_mat(mat))) return st;
+    if (S <= 0) { set_error("n_samples must be positive"); return PFEM_ERR_ARG; }
+    if (sstride < (int64_t)m->n_nodes * m->dim && S > 1) {
+        set_error("sample_stride smaller than n_nodes*dim");
+        return PFEM_ERR_ARG;
+    }
+    if (mode != PFEM_ASSEMBLE_CSR && mode != PFEM_ASSEMBLE_COLOUR) { set_error("bad assembly mode"); return PFEM_ERR_ARG; }
+    if (!ws) { set_error("workspace is NULL"); return PFEM_ERR_ARG; }
+    const Plan* P = reinterpret_cast<const Plan*>(m->plan);
+    if (ws_bytes < ws_layout(*P, S, m->dtype == PFEM_F64 ? 8 : 4).total) {
+        set_error("workspace too small (pfem_workspace_bytes)");
+        return PFEM_ERR_CAPACITY;
+    }
+    return PFEM_OK;
+}
+
+}  // namespace pfem
+
+using namespace pfem;
+
+extern "C" {
+
+const char* pfem_last_error(void) { return g_err.c_str(); }
+int64_t pfem_last_error_index(void) { return g_err_index; }
+int32_t pfem_abi_version(void) { return PFEM_ABI_VERSION; }
+int64_t pfem_launch_count(int32_t reset) {
+    int64_t v = g_launches;
+    if (reset) g_launches = 0;
+    return v;
+}
+
+pfem_status pfem_mesh_prepare(pfem_mesh* m, void* stream) {
+    pfem_status st = check_mesh(m, false);
+    if (st) return st;
+    if (!m->coords || !m->conn || !m->grad || !m->vol || !m->csr_ptr || !m->csr_ent || !m->colour ||
+        !m->colour_elems || !m->colour_ptr) {
+        set_error("prepare: NULL input or output array");
+        return PFEM_ERR_ARG;
+    }
+    if (m->n_parts > 1 && (!m->part_elem || !m->part_node)) {
+        set_error("prepare: part offsets required when n_parts > 1");
+        return PFEM_ERR_ARG;
+    }
+    if (m->n_nodes >= (1 << 29)) { set_error("n_nodes >= 2^29 not supported"); return PFEM_ERR_ARG; }
+    if ((int64_t)m->n_elems * (m->dim + 1) >= INT32_MAX) { set_error("too many elements"); return PFEM_ERR_ARG; }
+    if (m->max_colours < 1 || m->max_colours > 128) { set_error("max_colours must be in [1, 128]"); return PFEM_ERR_ARG; }
+    if (m->block_elems < 0) { set_error("block_elems must be >= 0"); return PFEM_ERR_ARG; }
+    if (m->dim == 3 && ((uintptr_t)m->conn & 15)) { set_error("conn must be 16-byte aligned for dim 3"); return PFEM_ERR_ARG; }
+    if (m->plan) release_impl(m);
+    return prepare_impl(m, (cudaStream_t)stream);
+}
+
+void pfem_mesh_release(pfem_mesh* m) { release_impl(m); }
+
+pfem_status pfem_plan_export(const pfem_mesh* m, int32_t* blk_elem, int32_t* blk_occ, int32_t* occ_node,
+                             int32_t* occ_ent_ptr, uint16_t* loc_ent) {
+    pfem_status st = check_mesh(m, true);
+    if (st) return st;
+    const Plan* P = reinterpret_cast<const Plan*>(m->plan);
+    cudaError_t e = cudaSuccess;
+    if (blk_elem && e == cudaSuccess) e = cudaMemcpy(blk_elem, P->blk_elem, sizeof(int32_t) * (P->n_blocks + 1), cudaMemcpyDeviceToHost);
+    if (blk_occ && e == cudaSuccess) e = cudaMemcpy(blk_occ, P->blk_occ, sizeof(int32_t) * (P->n_blocks + 1), cudaMemcpyDeviceToHost);
+    if (occ_node && e == cudaSuccess) e = cudaMemcpy(occ_node, P->occ_node, sizeof(int32_t) * P->n_occ, cudaMemcpyDeviceToHost);
+    if (occ_ent_ptr && e == cudaSuccess) e = cudaMemcpy(occ_ent_ptr, P->occ_ent_ptr, sizeof(int32_t) * (P->n_occ + 1), cudaMemcpyDeviceToHost);
+    if (loc_ent && e == cudaSuccess)
+        e = cudaMemcpy(loc_ent, P->loc_ent, sizeof(uint16_t) * (size_t)P->n_elems * (P->dim + 1), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_status(e, "pfem_plan_export");
+    return PFEM_OK;
+}
+
+size_t pfem_workspace_bytes(const pfem_mesh* m, int32_t n_samples) {
+    if (check_mesh(m, true) != PFEM_OK || n_samples <= 0) return 0;
+    const Plan* P = reinterpret_cast<const Plan*>(m->plan);
+    return ws_layout(*P, n_samples, m->dtype == PFEM_F64 ? 8 : 4).total;
+}
+
+pfem_status pfem_lame(int32_t dtype, int32_t kind, int64_t n, const void* p0, int64_t stride0, const void* p1,
+                      int64_t stride1, void* mu, void* lam, void* stream) {
+    if (!p0 || !p1 || !mu || !lam || n < 0 || kind < 0 || kind > 2) { set_error("pfem_lame: bad argument"); return PFEM_ERR_ARG; }
+    if (n == 0) return PFEM_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const unsigned g = (unsigned)((n + 255) / 256);
+    if (dtype == PFEM_F32)
+        k_lame<float><<<g, 256, 0, s>>>(n, kind, (const float*)p0, stride0, (const float*)p1, stride1, (float*)mu, (float*)lam);
+    else if (dtype == PFEM_F64)
+        k_lame<double><<<g, 256, 0, s>>>(n, kind, (const double*)p0, stride0, (const double*)p1, stride1, (double*)mu, (double*)lam);
+    else { set_error("bad dtype"); return PFEM_ERR_ARG; }
+    PFEM_LAUNCH_CHECK("k_lame");
+    return PFEM_OK;
+}
+
+pfem_status pfem_energy(const pfem_mesh* m, const pfem_material* mat, int32_t n_samples, const void* u,
+                        int64_t sample_stride, const void* f_ext, void* elem_energy, void* totals, void* residual,
+                        int32_t mode, pfem_flags* flags, void* ws, size_t ws_bytes, void* stream) {
+    pfem_status st = common_checks(m, mat, n_samples, sample_stride, mode, ws, ws_bytes);
+    if (st) return st;
+    if (!u || !totals) { set_error("pfem_energy: u and totals are required"); return PFEM_ERR_ARG; }
+    Call c{};
+    c.m = m;
+    c.P = reinterpret_cast<const Plan*>(m->plan);
+    c.op = residual ? OP_ENERGY_RESIDUAL : OP_ENERGY;
+    c.model = mat->model;
+    c.mode = mode;
+    c.S = n_samples;
+    c.sstride = sample_stride;
+    c.mat = *mat;
+    c.u = u;
+    c.f_ext = f_ext;
+    c.W_e = elem_energy;
+    c.totals = totals;
+    c.out = residual;
+    c.flags = flags;
+    c.ws = ws;
+    c.ws_bytes = ws_bytes;
+    c.stream = (cudaStream_t)stream;
+    return run(c);
+}
+
+pfem_status pfem_residual(const pfem_mesh* m, const pfem_material* mat, int32_t n_samples, const void* u,
+                          int64_t sample_stride, void* residual, int32_t mode, pfem_flags* flags, void* ws,
+                          size_t ws_bytes, void* stream) {
+    pfem_status st = common_checks(m, mat, n_samples, sample_stride, mode, ws, ws_bytes);
+    if (st) return st;
+    if (!u || !residual) { set_error("pfem_residual: u and residual are required"); return PFEM_ERR_ARG; }
+    Call c{};
+    c.m = m;
+    c.P = reinterpret_cast<const Plan*>(m->plan);
+    c.op = OP_RESIDUAL;
+    c.model = mat->model;
+    c.mode = mode;
+    c.S = n_samples;
+    c.sstride = sample_stride;
+    c.mat = *mat;
+    c.u = u;
+    c.out = residual;
+    c.flags = flags;
+    c.ws = ws;
+    c.ws_bytes = ws_bytes;
+    c.stream = (cudaStream_t)stream;
+    return run(c);
+}
+
+pfem_status pfem_tangent_apply(const pfem_mesh* m, const pfem_material* mat, int32_t n_samples, const void* u,
+                               const void* v, void* Kv, int64_t sample_stride, const uint8_t* dirichlet_mask,
+                               int32_t mode, pfem_flags* flags, void* ws, size_t ws_bytes, void* stream) {
+    pfem_status st = common_checks(m, mat, n_samples, sample_stride, mode, ws, ws_bytes);
+    if (st) return st;
+    if (!v || !Kv) { set_error("pfem_tangent_apply: v and Kv are required"); return PFEM_ERR_ARG; }
+    if (mat->model == PFEM_NEOHOOKEAN && !u) { set_error("pfem_tangent_apply: Neo-Hookean needs u"); return PFEM_ERR_ARG; }
+    Call c{};
+    c.m = m;
+    c.P = reinterpret_cast<const Plan*>(m->plan);
+    c.op = OP_TANGENT;
+    c.model = mat->model;
+    c.mode = mode;
+    c.S = n_samples;
+    c.sstride = sample_stride;
+    c.mat = *mat;
+    c.u = u;
+    c.v = v;
+    c.mask = dirichlet_mask;
+    c.out = Kv;
+    c.flags = flags;
+    c.ws = ws;
+    c.ws_bytes = ws_bytes;
+    c.stream = (cudaStream_t)stream;
+    return run(c);
+}
+
+size_t pfem_cg_workspace_bytes(const pfem_mesh* m) {
+    if (check_mesh(m, true) != PFEM_OK) return 0;
+    return cg_ws_bytes(*reinterpret_cast<const Plan*>(m->plan), m->dtype);
+}
+
+pfem_status pfem_cg(const pfem_mesh* m, const pfem_material* mat, const void* u_state, const void* rhs,
+                    const uint8_t* mask, void* x, double tol, int32_t max_iter, int32_t mode, double* history,
+                    pfem_cg_report* report, void* ws, size_t ws_bytes, void* stream) {
+    pfem_status st = check_mesh(m, true);
+    if (st) return st;
+    if ((st = check_mat(mat))) return st;
+    if (!rhs || !x || !report || !ws) { set_error("pfem_cg: NULL argument"); return PFEM_ERR_ARG; }
+    if (mat->model == PFEM_NEOHOOKEAN && !u_state) { set_error("pfem_cg: Neo-Hookean needs u_state"); return PFEM_ERR_ARG; }
+    if (!(tol >= 0.0) || max_iter < 0) { set_error("pfem_cg: bad tol / max_iter"); return PFEM_ERR_ARG; }
+    if (mode != PFEM_ASSEMBLE_CSR && mode != PFEM_ASSEMBLE_COLOUR) { set_error("bad assembly mode"); return PFEM_ERR_ARG; }
+    if (ws_bytes < pfem_cg_workspace_bytes(m)) { set_error("pfem_cg: workspace too small"); return PFEM_ERR_CAPACITY; }
+    memset(report, 0, sizeof(*report));
+    return run_cg(m, mat, u_state, rhs, mask, x, tol, max_iter, mode, history, report, ws, (cudaStream_t)stream);
+}
+
+}  // extern "C"

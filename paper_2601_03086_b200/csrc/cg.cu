@@ -1,0 +1,366 @@
+// cg.cu — warm-started conjugate gradient on the GPU (§8 row a7; App. B P:1021-1036,
+// warm start P:395-417, skip rule P:419-423).
+//
+// Hestenes-Stiefel CG on A = (I-M) K (I-M) + M with b = (I-M)(f - K x_D), x_D = M x0.
+// Scalars (rho, alpha, beta, the convergence test, the iteration count, the history)
+// live on the device; every dot product is a fixed-grid, fixed-order reduction (no float
+// atomics).  One iteration = 3 kernels:
+//   k_assemble<TANGENT> (q = A p, fused p.q -> alpha in its last block)
+//   k_cg_update          (x += alpha p, r -= alpha q, rho' = r.r -> test, beta in last block)
+//   k_cg_dir             (p = r + beta p)
+// captured B at a time in a CUDA graph and replayed until the device flag says done;
+// converged / broken-down iterations exit at their first instruction.
+#include <algorithm>
+
+#include "launch.cuh"
+
+namespace pfem {
+
+constexpr int VEC_NT = 256;
+
+struct VecRed {
+    int32_t counter;
+    int32_t pad[63];
+    double part[1024];
+};
+
+__device__ __forceinline__ bool vec_last_block(VecRed* vr, double v, double* s_red, int* s_flag) {
+    const double t = cta_sum<VEC_NT>(v, s_red);
+    if (threadIdx.x == 0) {
+        vr->part[blockIdx.x] = t;
+        __threadfence();
+        *s_flag = (atomicAdd(&vr->counter, 1) == (int)gridDim.x - 1);
+    }
+    __syncthreads();
+    return *s_flag;
+}
+
+// fixed-order sum of the per-CTA partials (called by the last CTA, valid in thread 0)
+__device__ __forceinline__ double vec_final(VecRed* vr, double* s_red) {
+    __threadfence();
+    double v = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += VEC_NT) v += ld_relaxed(vr->part + i);
+    const double t = cta_sum<VEC_NT>(v, s_red);
+    if (threadIdx.x == 0) vr->counter = 0;
+    return t;
+}
+
+template <class T>
+__global__ void __launch_bounds__(VEC_NT)
+k_cg_masked_copy(int64_t n, const uint8_t* __restrict__ mask, const T* __restrict__ x, T* __restrict__ xd) {
+    for (int64_t i = (int64_t)blockIdx.x * VEC_NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * VEC_NT)
+        xd[i] = (mask && mask[i]) ? x[i] : T(0);
+}
+
+// b = (I-M)(f - K x_D); bnorm2 = b.b
+template <class T>
+__global__ void __launch_bounds__(VEC_NT)
+k_cg_rhs(int64_t n, const uint8_t* __restrict__ mask, const T* __restrict__ f, const T* __restrict__ kxd,
+         T* __restrict__ b, CgState* cg, VecRed* vr) {
+    __shared__ double s_red[VEC_NT / 32];
+    __shared__ int s_flag;
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * VEC_NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * VEC_NT) {
+        T v = (mask && mask[i]) ? T(0) : f[i] - kxd[i];
+        b[i] = v;
+        acc += (double)v * (double)v;
+    }
+    if (!vec_last_block(vr, acc, s_red, &s_flag)) return;
+    const double t = vec_final(vr, s_red);
+    if (threadIdx.x == 0) cg->bnorm2 = t;
+}
+
+// r = b - A x (free DOFs), p = r, rho = r.r; skip rule / zero rhs
+template <class T>
+__global__ void __launch_bounds__(VEC_NT)
+k_cg_r0(int64_t n, const uint8_t* __restrict__ mask, const T* __restrict__ b, const T* __restrict__ ax,
+        T* __restrict__ r, T* __restrict__ p, T* __restrict__ x, CgState* cg, VecRed* vr, double* history) {
+    __shared__ double s_red[VEC_NT / 32];
+    __shared__ int s_flag;
+    double acc = 0.0;
+    const bool zero_rhs = cg->bnorm2 == 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * VEC_NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * VEC_NT) {
+        const bool c = mask && mask[i];
+        T v = c ? T(0) : b[i] - ax[i];
+        r[i] = v;
+        p[i] = v;
+        if (zero_rhs && !c) x[i] = T(0);
+        acc += (double)v * (double)v;
+    }
+    if (!vec_last_block(vr, acc, s_red, &s_flag)) return;
+    const double t = vec_final(vr, s_red);
+    if (threadIdx.x == 0) {
+        cg->rho = t;
+        cg->k = 0;
+        const double bn2 = cg->bnorm2;
+        cg->pad0 = bn2 > 0 ? sqrt(t / bn2) : 0.0;   // rel_res0
+        if (history) history[0] = cg->pad0;
+        if (bn2 == 0.0) {
+            cg->rho = 0.0;
+            cg->status = 1;
+            cg->done = 1;
+        } else if (t < cg->tol2 * bn2) {   // ||r|| < tol ||b||  (strict)
+            cg->status = 1;
+            cg->done = 1;
+        } else if (cg->max_iter <= 0) {
+            cg->status = 3;
+            cg->done = 1;
+        }
+    }
+}
+
+template <class T>
+__global__ void __launch_bounds__(VEC_NT)
+k_cg_update(int64_t n, T* __restrict__ x, T* __restrict__ r, const T* __restrict__ p, const T* __restrict__ q,
+            CgState* cg, VecRed* vr, double* history) {
+    __shared__ double s_red[VEC_NT / 32];
+    __shared__ int s_flag;
+    if (ld_relaxed_i(&cg->done)) return;
+    const T alpha = (T)cg->alpha;
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * VEC_NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * VEC_NT) {
+        x[i] = fma(alpha, p[i], x[i]);
+        const T v = fma(-alpha, q[i], r[i]);
+        r[i] = v;
+        acc += (double)v * (double)v;
+    }
+    if (!vec_last_block(vr, acc, s_red, &s_flag)) return;
+    const double t = vec_final(vr, s_red);
+    if (threadIdx.x == 0) {
+        const int k = cg->k + 1;
+        cg->k = k;
+        cg->rho_new = t;
+        const double bn2 = cg->bnorm2;
+        if (history) history[k] = sqrt(t / bn2);
+        cg->beta = t / cg->rho;
+        cg->rho = t;
+        if (t < cg->tol2 * bn2) {
+            cg->status = 1;
+            cg->done = 1;
+        } else if (k >= cg->max_iter) {
+            cg->status = 3;
+            cg->done = 1;
+        }
+    }
+}
+
+template <class T>
+__global__ void __launch_bounds__(VEC_NT)
+k_cg_dir(int64_t n, const T* __restrict__ r, T* __restrict__ p, const CgState* cg) {
+    if (ld_relaxed_i(&cg->done)) return;
+    const T beta = (T)cg->beta;
+    for (int64_t i = (int64_t)blockIdx.x * VEC_NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * VEC_NT)
+        p[i] = fma(beta, p[i], r[i]);
+}
+
+// COLOUR-mode CG: p.q and alpha as a separate pass
+template <class T>
+__global__ void __launch_bounds__(VEC_NT)
+k_cg_pq(int64_t n, const T* __restrict__ p, const T* __restrict__ q, CgState* cg, VecRed* vr) {
+    __shared__ double s_red[VEC_NT / 32];
+    __shared__ int s_flag;
+    if (ld_relaxed_i(&cg->done)) return;
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * VEC_NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * VEC_NT)
+        acc += (double)p[i] * (double)q[i];
+    if (!vec_last_block(vr, acc, s_red, &s_flag)) return;
+    const double t = vec_final(vr, s_red);
+    if (threadIdx.x == 0) {
+        cg->pq = t;
+        if (!(t > 0.0)) {
+            cg->status = 2;
+            cg->done = 1;
+        } else {
+            cg->alpha = cg->rho / t;
+        }
+    }
+}
+
+// ||b - A x|| over free DOFs -> pq slot (true residual)
+template <class T>
+__global__ void __launch_bounds__(VEC_NT)
+k_cg_true(int64_t n, const uint8_t* __restrict__ mask, const T* __restrict__ b, const T* __restrict__ ax,
+          CgState* cg, VecRed* vr) {
+    __shared__ double s_red[VEC_NT / 32];
+    __shared__ int s_flag;
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * VEC_NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * VEC_NT) {
+        if (mask && mask[i]) continue;
+        const double d = (double)b[i] - (double)ax[i];
+        acc += d * d;
+    }
+    if (!vec_last_block(vr, acc, s_red, &s_flag)) return;
+    const double t = vec_final(vr, s_red);
+    if (threadIdx.x == 0) cg->pq = t;
+}
+
+struct CgWs {
+    size_t state, vr, r, p, q, b, asmws, total;
+};
+
+inline CgWs cg_layout(const Plan& P, size_t tsize) {
+    CgWs L;
+    size_t o = 0;
+    const size_t nvec = align_up(tsize * (size_t)P.n_nodes * P.dim, 256);
+    L.state = o; o += align_up(sizeof(CgState), 256);
+    L.vr = o;    o += align_up(sizeof(VecRed), 256);
+    L.r = o;     o += nvec;
+    L.p = o;     o += nvec;
+    L.q = o;     o += nvec;
+    L.b = o;     o += nvec;
+    L.asmws = o; o += ws_layout(P, 1, tsize).total;
+    L.total = o;
+    return L;
+}
+
+size_t cg_ws_bytes(const Plan& P, int dtype) {
+    return cg_layout(P, dtype == PFEM_F64 ? 8 : 4).total;
+}
+
+template <int D, class T>
+static pfem_status tangent(const pfem_mesh* m, const Plan* P, const pfem_material* mat, const void* u,
+                           const void* v, void* out, const uint8_t* mask, int mode, void* asmws, CgState* cg,
+                           cudaStream_t s) {
+    Call c{};
+    c.m = m;
+    c.P = P;
+    c.op = OP_TANGENT;
+    c.model = mat->model;
+    c.mode = mode;
+    c.S = 1;
+    c.sstride = (int64_t)P->n_nodes * D;
+    c.mat = *mat;
+    c.u = u;
+    c.v = v;
+    c.mask = mask;
+    c.out = out;
+    c.ws = asmws;
+    c.stream = s;
+    c.cg = mode == PFEM_ASSEMBLE_CSR ? cg : nullptr;
+    return run_assemble<D, T>(c);
+}
+
+template <int D, class T>
+pfem_status cg_impl(const pfem_mesh* m, const pfem_material* mat, const void* u_state, const void* rhs,
+                    const uint8_t* mask, void* xv, double tol, int max_iter, int mode, double* history,
+                    pfem_cg_report* rep, void* ws, cudaStream_t s) {
+    const Plan* P = reinterpret_cast<const Plan*>(m->plan);
+    const CgWs L = cg_layout(*P, sizeof(T));
+    char* w = (char*)ws;
+    CgState* st = (CgState*)(w + L.state);
+    VecRed* vr = (VecRed*)(w + L.vr);
+    T* r = (T*)(w + L.r);
+    T* p = (T*)(w + L.p);
+    T* q = (T*)(w + L.q);
+    T* b = (T*)(w + L.b);
+    T* x = (T*)xv;
+    void* asmws = w + L.asmws;
+    const int64_t n = (int64_t)P->n_nodes * D;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int G = std::min(1024, 2 * nsm);   // fixed grid => fixed reduction order
+    CgState h{};
+    h.tol2 = tol * tol;
+    h.max_iter = max_iter;
+    PFEM_CUDA_TRY(cudaMemcpyAsync(st, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+    PFEM_CUDA_TRY(cudaMemsetAsync(vr, 0, sizeof(int32_t), s));
+    // b = (I-M)(f - K x_D)
+    k_cg_masked_copy<T><<<G, VEC_NT, 0, s>>>(n, mask, x, p);
+    PFEM_LAUNCH_CHECK("k_cg_masked_copy");
+    pfem_status e = tangent<D, T>(m, P, mat, u_state, p, q, nullptr, mode, asmws, nullptr, s);
+    if (e != PFEM_OK) return e;
+    k_cg_rhs<T><<<G, VEC_NT, 0, s>>>(n, mask, (const T*)rhs, q, b, st, vr);
+    PFEM_LAUNCH_CHECK("k_cg_rhs");
+    // r0 = b - A x0
+    e = tangent<D, T>(m, P, mat, u_state, x, q, mask, mode, asmws, nullptr, s);
+    if (e != PFEM_OK) return e;
+    k_cg_r0<T><<<G, VEC_NT, 0, s>>>(n, mask, b, q, r, p, x, st, vr, history);
+    PFEM_LAUNCH_CHECK("k_cg_r0");
+    PFEM_CUDA_TRY(cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, s));
+    PFEM_CUDA_TRY(cudaStreamSynchronize(s));
+    if (!h.done) {
+        // capture B iterations into a graph on a private stream, replay on `s`
+        const int B = std::max(1, std::min(32, max_iter));
+        cudaStream_t cs;
+        PFEM_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        int64_t launches_before = pfem_launch_count(0);
+        pfem_status ce = PFEM_OK;
+        cudaError_t cerr = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+        if (cerr != cudaSuccess) { cudaStreamDestroy(cs); return cuda_status(cerr, "cudaStreamBeginCapture"); }
+        for (int it = 0; it < B && ce == PFEM_OK; ++it) {
+            ce = tangent<D, T>(m, P, mat, u_state, p, q, mask, mode, asmws, st, cs);
+            if (ce != PFEM_OK) break;
+            if (mode != PFEM_ASSEMBLE_CSR) {
+                k_cg_pq<T><<<G, VEC_NT, 0, cs>>>(n, p, q, st, vr);
+                count_launch();
+            }
+            k_cg_update<T><<<G, VEC_NT, 0, cs>>>(n, x, r, p, q, st, vr, history);
+            k_cg_dir<T><<<G, VEC_NT, 0, cs>>>(n, r, p, st);
+            count_launch(2);
+        }
+        cerr = cudaStreamEndCapture(cs, &graph);
+        const int64_t per_graph = pfem_launch_count(0) - launches_before;
+        if (ce == PFEM_OK && cerr == cudaSuccess) cerr = cudaGraphInstantiate(&exec, graph, 0);
+        if (ce != PFEM_OK || cerr != cudaSuccess) {
+            if (graph) cudaGraphDestroy(graph);
+            cudaStreamDestroy(cs);
+            if (ce != PFEM_OK) return ce;
+            return cuda_status(cerr, "cg graph capture");
+        }
+        // the captured launches were counted at capture; count replays instead
+        count_launch((int)-per_graph);
+        int launched = 0;
+        while (true) {
+            cerr = cudaGraphLaunch(exec, s);
+            if (cerr != cudaSuccess) break;
+            count_launch((int)per_graph);
+            launched += B;
+            cerr = cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, s);
+            if (cerr != cudaSuccess) break;
+            cerr = cudaStreamSynchronize(s);
+            if (cerr != cudaSuccess || h.done || launched >= max_iter + B) break;
+        }
+        cudaGraphExecDestroy(exec);
+        cudaGraphDestroy(graph);
+        cudaStreamDestroy(cs);
+        if (cerr != cudaSuccess) return cuda_status(cerr, "cg loop");
+    }
+    // true residual ||b - A x|| / ||b||
+    e = tangent<D, T>(m, P, mat, u_state, x, q, mask, mode, asmws, nullptr, s);
+    if (e != PFEM_OK) return e;
+    k_cg_true<T><<<G, VEC_NT, 0, s>>>(n, mask, b, q, st, vr);
+    PFEM_LAUNCH_CHECK("k_cg_true");
+    PFEM_CUDA_TRY(cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, s));
+    PFEM_CUDA_TRY(cudaStreamSynchronize(s));
+    rep->iterations = h.k;
+    rep->status = h.status;
+    rep->converged = h.status == 1;
+    rep->bnorm = sqrt(h.bnorm2);
+    rep->rel_res_final = h.bnorm2 > 0 ? sqrt(h.rho / h.bnorm2) : 0.0;
+    rep->true_rel_res_final = h.bnorm2 > 0 ? sqrt(h.pq / h.bnorm2) : 0.0;
+    rep->rel_res0 = h.pad0;
+    if (h.status == 2) {
+        set_error("CG breakdown: p.Ap <= 0");
+        return PFEM_ERR_BREAKDOWN;
+    }
+    if (h.status != 1) {
+        set_error("CG did not converge within max_iter");
+        return PFEM_ERR_NOT_CONVERGED;
+    }
+    return PFEM_OK;
+}
+
+pfem_status run_cg(const pfem_mesh* m, const pfem_material* mat, const void* u_state, const void* rhs,
+                   const uint8_t* mask, void* x, double tol, int max_iter, int mode, double* history,
+                   pfem_cg_report* rep, void* ws, cudaStream_t s) {
+    if (m->dim == 2)
+        return m->dtype == PFEM_F32 ? cg_impl<2, float>(m, mat, u_state, rhs, mask, x, tol, max_iter, mode, history, rep, ws, s)
+                                    : cg_impl<2, double>(m, mat, u_state, rhs, mask, x, tol, max_iter, mode, history, rep, ws, s);
+    return m->dtype == PFEM_F32 ? cg_impl<3, float>(m, mat, u_state, rhs, mask, x, tol, max_iter, mode, history, rep, ws, s)
+                                : cg_impl<3, double>(m, mat, u_state, rhs, mask, x, tol, max_iter, mode, history, rep, ws, s);
+}
+
+}  // namespace pfem

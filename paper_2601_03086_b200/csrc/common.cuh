@@ -1,0 +1,120 @@
+// common.cuh — shared host/device plumbing of libpfem (errors, plan layout, workspace
+// layout, memory-model helpers).  Product code; no oracle code is included anywhere.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/pfem.h"
+
+namespace pfem {
+
+// ------------------------------------------------------------------ errors
+void set_error(const std::string& msg, int64_t index = -1);
+pfem_status cuda_status(cudaError_t e, const char* what);
+void count_launch(int n = 1);
+
+#define PFEM_CUDA_TRY(expr)                                             \
+    do {                                                                \
+        cudaError_t _e = (expr);                                        \
+        if (_e != cudaSuccess) return ::pfem::cuda_status(_e, #expr);   \
+    } while (0)
+
+#define PFEM_LAUNCH_CHECK(name)                                         \
+    do {                                                                \
+        ::pfem::count_launch();                                         \
+        cudaError_t _e = cudaGetLastError();                            \
+        if (_e != cudaSuccess) return ::pfem::cuda_status(_e, name);    \
+    } while (0)
+
+// ------------------------------------------------------------------ plan
+// Occurrence kind bits packed in occ_node (node ids < 2^30).
+constexpr int32_t OCC_NODE_MASK = 0x1fffffff;  // prepare rejects n_nodes >= 2^29
+constexpr int32_t OCC_NONOWNER = 0x40000000;   // another (later) block owns the node
+constexpr int32_t OCC_EARLIER = 0x20000000;    // owner, and earlier blocks hold partials
+
+struct Plan {
+    int32_t dim = 0, n_nodes = 0, n_elems = 0, n_parts = 0;
+    int32_t n_blocks = 0, n_occ = 0, eb_max = 0;
+    int32_t* blk_elem = nullptr;      // [n_blocks+1]
+    int32_t* blk_occ = nullptr;       // [n_blocks+1]
+    int32_t* blk_min_dep = nullptr;   // [n_blocks] lowest block holding a partial this block
+                                      // needs (== b if none); the block waits for [min_dep, b)
+    int32_t* part_blk = nullptr;      // [n_parts+1]
+    int32_t n_chunks = 0;             // reduction chunks (<= CHUNK consecutive blocks, inside a part)
+    int32_t* blk_chunk = nullptr;     // [n_blocks]
+    int32_t* chunk_blk = nullptr;     // [n_chunks+1]
+    int32_t* part_chunk = nullptr;    // [n_parts+1]
+    std::vector<int32_t> colour_ptr_host;  // [n_colours+1] (colour-mode launches)
+    int32_t* part_node = nullptr;     // [n_parts+1] (device copy, always present)
+    int32_t* part_elem = nullptr;     // [n_parts+1] (device copy, always present)
+    int32_t* occ_node = nullptr;      // [n_occ] node | kind bits
+    int32_t* occ_ent_ptr = nullptr;   // [n_occ+1] offsets into loc_ent
+    uint16_t* loc_ent = nullptr;      // [(dim+1)*n_elems] local entry ids, grouped by occurrence
+    int32_t* node_occ_ptr = nullptr;  // [n_nodes+1]
+    int32_t* node_occ = nullptr;      // [n_occ] occurrence ids sorted by (node, block)
+    void* pool = nullptr;             // single allocation backing all of the above
+};
+
+// ------------------------------------------------------------------ workspace layout
+// [ Counters | blk_flag[n_blocks] | blk_sum[2S+1][n_blocks] (double) | chunk_done[n_chunks] |
+//   chunk_sum[2S+1][n_chunks] (double) | partial[S][n_occ][d] (T) | colour-mode W [S][E] (T) ]
+struct Counters {
+    int32_t ticket;
+    int32_t done;
+    int32_t epoch;
+    int32_t n_inv;
+    int32_t first_inv;     // stored as INT32_MAX - first (atomicMax; 0 = none) so zero-fill is valid
+    int32_t n_nonfinite;
+    int32_t pad[10];
+};
+
+struct WsLayout {
+    size_t counters, flags, blk_sum, chunk_done, chunk_sum, partial, wtmp, total;
+};
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+inline WsLayout ws_layout(const Plan& p, int S, size_t tsize) {
+    WsLayout L;
+    size_t o = 0;
+    L.counters = o; o += align_up(sizeof(Counters), 256);
+    L.flags = o;    o += align_up(sizeof(int32_t) * (size_t)(p.n_blocks + 1), 256);
+    L.blk_sum = o;  o += align_up(sizeof(double) * (2 * (size_t)S + 1) * (p.n_blocks + 1), 256);
+    L.chunk_done = o; o += align_up(sizeof(int32_t) * (size_t)(p.n_chunks + 1), 256);
+    L.chunk_sum = o;  o += align_up(sizeof(double) * (2 * (size_t)S + 1) * (p.n_chunks + 1), 256);
+    L.partial = o;  o += align_up(tsize * (size_t)S * p.n_occ * p.dim, 256);
+    L.wtmp = o;     o += align_up(tsize * (size_t)S * p.n_elems, 256);
+    L.total = o;
+    return L;
+}
+
+// ------------------------------------------------------------------ device helpers
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ float ld_relaxed(const float* p) {
+    float v;
+    asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ double ld_relaxed(const double* p) {
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int ld_relaxed_i(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+}  // namespace pfem

@@ -1,0 +1,180 @@
+// launch.cuh — host-side dispatch of the element kernels (template selection, smem
+// sizing, grid), instantiated per (dim, dtype) in asm_{2,3}{f,d}.cu.
+#pragma once
+
+#include "assemble.cuh"
+
+namespace pfem {
+
+struct Call {
+    const pfem_mesh* m;
+    const Plan* P;
+    int op, model, mode, S;
+    int64_t sstride;
+    pfem_material mat;
+    const void* u;
+    const void* v;
+    const uint8_t* mask;
+    const void* f_ext;
+    void* W_e;
+    void* totals;
+    void* out;
+    pfem_flags* flags;
+    void* ws;
+    size_t ws_bytes;
+    cudaStream_t stream;
+    CgState* cg;
+};
+
+template <class T>
+AsmParams<T> make_params(const Call& c) {
+    const Plan& P = *c.P;
+    AsmParams<T> p;
+    p.E = P.n_elems;
+    p.N = P.n_nodes;
+    p.S = c.S;
+    p.K = P.n_parts;
+    p.sstride = c.sstride;
+    p.conn = c.m->conn;
+    p.grad = (const T*)c.m->grad;
+    p.vol = (const T*)c.m->vol;
+    p.mat.kind = c.mat.kind;
+    p.mat.p0 = (const T*)c.mat.p0;
+    p.mat.p1 = (const T*)c.mat.p1;
+    p.mat.s0 = c.mat.stride0;
+    p.mat.s1 = c.mat.stride1;
+    p.u = (const T*)c.u;
+    p.v = (const T*)c.v;
+    p.mask = c.mask;
+    p.f_ext = (const T*)c.f_ext;
+    p.W_e = (T*)c.W_e;
+    p.totals = (T*)c.totals;
+    p.out = (T*)c.out;
+    p.uflags = c.flags;
+    p.n_blocks = P.n_blocks;
+    p.n_occ = P.n_occ;
+    p.eb_max = P.eb_max;
+    p.n_chunks = P.n_chunks;
+    p.blk_elem = P.blk_elem;
+    p.blk_chunk = P.blk_chunk;
+    p.chunk_blk = P.chunk_blk;
+    p.part_chunk = P.part_chunk;
+    p.blk_occ = P.blk_occ;
+    p.blk_min_dep = P.blk_min_dep;
+    p.part_blk = P.part_blk;
+    p.occ_node = P.occ_node;
+    p.occ_ent_ptr = P.occ_ent_ptr;
+    p.loc_ent = P.loc_ent;
+    p.node_occ_ptr = P.node_occ_ptr;
+    p.node_occ = P.node_occ;
+    const WsLayout L = ws_layout(P, c.S, sizeof(T));
+    char* w = (char*)c.ws;
+    p.ctr = (Counters*)(w + L.counters);
+    p.flag = (int32_t*)(w + L.flags);
+    p.blk_sum = (double*)(w + L.blk_sum);
+    p.chunk_done = (int32_t*)(w + L.chunk_done);
+    p.chunk_sum = (double*)(w + L.chunk_sum);
+    p.partial = (T*)(w + L.partial);
+    p.cg = c.cg;
+    return p;
+}
+
+template <int D, int MODEL, class T, int OP, int ST, bool MASKED>
+pfem_status launch_csr(const AsmParams<T>& p, cudaStream_t s) {
+    constexpr bool HAS_FORCE = OP != OP_ENERGY;
+    const size_t smem = HAS_FORCE ? (size_t)ST * D * (D + 1) * p.eb_max * sizeof(T) : 0;
+    static size_t configured = 0;   // per instantiation
+    auto kern = k_assemble<D, MODEL, T, OP, ST, MASKED>;
+    if (smem > 40 * 1024 && smem > configured) {   // dynamic + static smem beyond the 48 KB default
+        PFEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = smem;
+    }
+    kern<<<p.n_blocks, ASM_NT, smem, s>>>(p);
+    PFEM_LAUNCH_CHECK("k_assemble");
+    return PFEM_OK;
+}
+
+template <int D, int MODEL, class T, int OP, bool MASKED>
+pfem_status dispatch_st(const AsmParams<T>& p, cudaStream_t s) {
+    constexpr bool HAS_FORCE = OP != OP_ENERGY;
+    int dev = 0, maxs = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&maxs, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const size_t per = HAS_FORCE ? (size_t)D * (D + 1) * p.eb_max * sizeof(T) : 0;
+    constexpr int STBIG = sizeof(T) == 4 ? 4 : 2;
+    if (p.S > 1 && per * STBIG + 1024 <= (size_t)maxs) return launch_csr<D, MODEL, T, OP, STBIG, MASKED>(p, s);
+    if (per + 1024 <= (size_t)maxs) return launch_csr<D, MODEL, T, OP, 1, MASKED>(p, s);
+    set_error("block_elems too large for shared memory");
+    return PFEM_ERR_CAPACITY;
+}
+
+template <int D, int MODEL, class T, int OP, bool MASKED>
+pfem_status run_colour(const Call& c, AsmParams<T> p) {
+    constexpr bool HAS_FORCE = OP != OP_ENERGY;
+    constexpr bool HAS_PSI = OP == OP_ENERGY || OP == OP_ENERGY_RESIDUAL;
+    cudaStream_t s = c.stream;
+    const Plan& P = *c.P;
+    const WsLayout L = ws_layout(P, c.S, sizeof(T));
+    T* wtmp = c.W_e ? (T*)c.W_e : (T*)((char*)c.ws + L.wtmp);
+    if (HAS_FORCE) {
+        const size_t row = sizeof(T) * (size_t)P.n_nodes * D;
+        if (c.sstride == (int64_t)P.n_nodes * D) {
+            PFEM_CUDA_TRY(cudaMemsetAsync(c.out, 0, row * c.S, s));
+        } else {
+            for (int q = 0; q < c.S; ++q)
+                PFEM_CUDA_TRY(cudaMemsetAsync((char*)c.out + sizeof(T) * c.sstride * q, 0, row, s));
+        }
+    }
+    const std::vector<int32_t>& cp = P.colour_ptr_host;
+    for (size_t col = 0; col + 1 < cp.size(); ++col) {
+        const int i0 = cp[col], i1 = cp[col + 1];
+        if (i1 <= i0) continue;
+        k_colour_pass<D, MODEL, T, OP, MASKED><<<(i1 - i0 + ASM_NT - 1) / ASM_NT, ASM_NT, 0, s>>>(
+            p, c.m->colour_elems, i0, i1, wtmp);
+        PFEM_LAUNCH_CHECK("k_colour_pass");
+    }
+    if (OP == OP_TANGENT && MASKED) {
+        const int64_t n = (int64_t)P.n_nodes * D;
+        k_mask_rows<D, T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c.S, P.n_nodes, c.sstride, c.mask, (const T*)c.v,
+                                                                        (T*)c.out);
+        PFEM_LAUNCH_CHECK("k_mask_rows");
+    }
+    const int want = HAS_PSI && c.totals ? 1 : 0;
+    k_colour_totals<D, T><<<want ? c.S * P.n_parts : 1, ASM_NT, 0, s>>>(p, P.part_elem, P.part_node, wtmp, want);
+    PFEM_LAUNCH_CHECK("k_colour_totals");
+    return PFEM_OK;
+}
+
+template <int D, int MODEL, class T, int OP, bool MASKED>
+pfem_status run_op(const Call& c) {
+    AsmParams<T> p = make_params<T>(c);
+    if (c.mode == PFEM_ASSEMBLE_COLOUR && OP != OP_ENERGY) return run_colour<D, MODEL, T, OP, MASKED>(c, p);
+    if (c.mode == PFEM_ASSEMBLE_COLOUR) return run_colour<D, MODEL, T, OP, MASKED>(c, p);
+    return dispatch_st<D, MODEL, T, OP, MASKED>(p, c.stream);
+}
+
+template <int D, int MODEL, class T>
+pfem_status run_model(const Call& c) {
+    switch (c.op) {
+        case OP_ENERGY: return run_op<D, MODEL, T, OP_ENERGY, false>(c);
+        case OP_ENERGY_RESIDUAL: return run_op<D, MODEL, T, OP_ENERGY_RESIDUAL, false>(c);
+        case OP_RESIDUAL: return run_op<D, MODEL, T, OP_RESIDUAL, false>(c);
+        case OP_TANGENT:
+            return c.mask ? run_op<D, MODEL, T, OP_TANGENT, true>(c) : run_op<D, MODEL, T, OP_TANGENT, false>(c);
+    }
+    set_error("bad op");
+    return PFEM_ERR_ARG;
+}
+
+template <int D, class T>
+pfem_status run_assemble(const Call& c) {
+    return c.model == MODEL_NH ? run_model<D, MODEL_NH, T>(c) : run_model<D, MODEL_LINEAR, T>(c);
+}
+
+// explicit instantiations live in asm_*.cu
+extern template pfem_status run_assemble<2, float>(const Call&);
+extern template pfem_status run_assemble<2, double>(const Call&);
+extern template pfem_status run_assemble<3, float>(const Call&);
+extern template pfem_status run_assemble<3, double>(const Call&);
+
+}  // namespace pfem

@@ -1,0 +1,601 @@
+// prep.cu — one-time mesh preparation on the GPU (§8 row a1):
+//   K1 geometry (J_e^{-1} rows = grad N_a, V_e = |det J_e|/d!; App. B)
+//   K2 node -> (element, slot) CSR (count / scan / fill / per-row sort -> ascending (e, a))
+//   K3 greedy first-fit colouring in element order (ticketed warps, dependency-driven)
+//      + colour-sorted element list (stable radix sort on the colour key)
+//   plan: element blocks, block-local CSR (smem bitonic sort of (node, entry) keys),
+//      node occurrences with ownership / earlier-partial kinds, node-major occurrence list.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace pfem {
+
+// ------------------------------------------------------------------ validation
+__global__ void k_check_conn(int nv, int E, int N, const int32_t* __restrict__ conn, int* bad) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= (int64_t)E * nv) return;
+    int v = conn[k];
+    if (v < 0 || v >= N) atomicMin(bad, (int)(k / nv));
+}
+
+// ------------------------------------------------------------------ K1 geometry
+template <int D, class T>
+__global__ void k_geometry(int E, const double* __restrict__ X, const int32_t* __restrict__ conn,
+                           T* __restrict__ grad, T* __restrict__ vol, int* n_negative,
+                           int* first_degenerate) {
+    int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    int v[D + 1];
+#pragma unroll
+    for (int a = 0; a <= D; ++a) v[a] = conn[(int64_t)e * (D + 1) + a];
+    double J[D][D];
+    double eprod = 1.0;
+#pragma unroll
+    for (int a = 1; a <= D; ++a) {
+        double l2 = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            J[i][a - 1] = X[(int64_t)v[a] * D + i] - X[(int64_t)v[0] * D + i];
+            l2 += J[i][a - 1] * J[i][a - 1];
+        }
+        eprod *= sqrt(l2);
+    }
+    double det, inv[D][D];
+    if (D == 2) {
+        det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+        double r = 1.0 / det;
+        inv[0][0] = J[1][1] * r;
+        inv[0][1] = -J[0][1] * r;
+        inv[1][0] = -J[1][0] * r;
+        inv[1][1] = J[0][0] * r;
+    } else {
+        // cofactors of J: C_ij; inverse = C^T / det
+        double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+        double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+        double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+        det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+        double r = 1.0 / det;
+        inv[0][0] = c00 * r;
+        inv[1][0] = c01 * r;
+        inv[2][0] = c02 * r;
+        inv[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * r;
+        inv[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * r;
+        inv[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * r;
+        inv[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * r;
+        inv[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * r;
+        inv[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * r;
+    }
+    if (!(fabs(det) > 64.0 * 2.220446049250313e-16 * eprod)) {
+        atomicMin(first_degenerate, e);
+        return;
+    }
+    if (det < 0) atomicAdd(n_negative, 1);
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int j = 0; j < D; ++j) grad[(int64_t)(a * D + j) * E + e] = (T)inv[a][j];
+    vol[e] = (T)(fabs(det) / (D == 2 ? 2.0 : 6.0));
+}
+
+// ------------------------------------------------------------------ K2 CSR
+__global__ void k_count(int64_t n, const int32_t* __restrict__ conn, int32_t* cnt) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) atomicAdd(&cnt[conn[k]], 1);
+}
+
+__global__ void k_csr_fill(int64_t n, const int32_t* __restrict__ conn, const int32_t* __restrict__ ptr,
+                           int32_t* fill, int32_t* ent) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    int v = conn[k];
+    int pos = atomicAdd(&fill[v], 1);
+    ent[ptr[v] + pos] = (int32_t)k;       // k = e*(d+1) + a
+}
+
+// per-row insertion sort -> ascending (e, a); rows hold at most a few dozen entries
+__global__ void k_csr_sort_rows(int N, const int32_t* __restrict__ ptr, int32_t* ent) {
+    int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    int b = ptr[n], e = ptr[n + 1];
+    for (int i = b + 1; i < e; ++i) {
+        int x = ent[i];
+        int j = i - 1;
+        while (j >= b && ent[j] > x) {
+            ent[j + 1] = ent[j];
+            --j;
+        }
+        ent[j + 1] = x;
+    }
+}
+
+// ------------------------------------------------------------------ K3 colouring
+// Greedy first-fit in ascending element id == Jones-Plassmann with priority -e.
+// Warps take 32 consecutive elements by ticket; lane e resolves its lower neighbours
+// (a prefix of each sorted CSR row) with a resumable cursor, waiting on lower ids that
+// belong to earlier tickets (resident or finished) or lower lanes of the same warp, so
+// the loop always progresses.  The colour value itself is the only payload (volatile).
+__global__ void k_colour_greedy(int nv, int E, const int32_t* __restrict__ conn,
+                                const int32_t* __restrict__ ptr, const int32_t* __restrict__ ent,
+                                int32_t* colour, int* ticket, int max_colours, int* overflow) {
+    const int lane = threadIdx.x & 31;
+    volatile int32_t* vcol = colour;
+    while (true) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(ticket, 32);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base >= E) return;
+        const int e = base + lane;
+        bool done = e >= E;
+        unsigned long long used0 = 0ull, used1 = 0ull;
+        int a = 0, k = -1;
+        while (__any_sync(0xffffffffu, !done)) {
+            bool blocked = false;
+            if (!done) {
+                while (a < nv) {
+                    int n = conn[(int64_t)e * nv + a];
+                    if (k < 0) k = ptr[n];
+                    int kend = ptr[n + 1];
+                    for (; k < kend; ++k) {
+                        int f = ent[k] / nv;
+                        if (f >= e) { k = kend; break; }
+                        int c = vcol[f];
+                        if (c < 0) { blocked = true; break; }
+                        if (c < 64) used0 |= 1ull << c;
+                        else used1 |= 1ull << (c - 64);
+                    }
+                    if (blocked) break;
+                    ++a;
+                    k = -1;
+                }
+                if (!blocked) {
+                    int c = (~used0) ? __ffsll((long long)~used0) - 1 : 64 + __ffsll((long long)~used1) - 1;
+                    if (c >= max_colours || c < 0) {
+                        atomicMin(overflow, e);
+                        c = max_colours - 1;       // keep going; prepare reports CAPACITY
+                    }
+                    vcol[e] = c;
+                    done = true;
+                }
+            }
+            __syncwarp();
+            if (blocked) __nanosleep(64);
+        }
+    }
+}
+
+__global__ void k_colour_hist(int E, const int32_t* __restrict__ colour, int32_t* hist, int* maxc) {
+    int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    int c = colour[e];
+    atomicAdd(&hist[c], 1);
+    atomicMax(maxc, c);
+}
+
+// exclusive scan of the (<= 129) colour counts; single thread, integer
+__global__ void k_colour_ptr(int nc, const int32_t* __restrict__ hist, int32_t* cptr) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int s = 0;
+    for (int c = 0; c < nc; ++c) {
+        cptr[c] = s;
+        s += hist[c];
+    }
+    cptr[nc] = s;
+}
+
+__global__ void k_iota(int n, int32_t* out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = i;
+}
+
+// ------------------------------------------------------------------ plan
+__device__ __forceinline__ int block_of(int e, const int32_t* __restrict__ blk_elem, int nb) {
+    int lo = 0, hi = nb;     // blk_elem[lo] <= e < blk_elem[hi]
+    while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (blk_elem[mid] <= e) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// number of distinct blocks touching each node (its CSR row is sorted by element)
+__global__ void k_node_occ_count(int N, int nv, const int32_t* __restrict__ ptr,
+                                 const int32_t* __restrict__ ent, const int32_t* __restrict__ blk_elem,
+                                 int nb, int32_t* cnt) {
+    int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    int c = 0, last = -1;
+    for (int k = ptr[n]; k < ptr[n + 1]; ++k) {
+        int b = block_of(ent[k] / nv, blk_elem, nb);
+        if (b != last) { ++c; last = b; }
+    }
+    cnt[n] = c;
+}
+
+constexpr int PLAN_THREADS = 512;
+constexpr int PLAN_MAX_KEYS = 4096;
+constexpr int CHUNK_BLOCKS = 32;   // == CHUNK of assemble.cuh
+
+// Per block: bitonic-sort the (node << 16 | local entry) keys of its elements in shared
+// memory; runs of equal node = occurrences, in ascending node order; inside a run the
+// local entries ascend = CSR order restricted to the block.
+// mode 0: count occurrences -> occ_cnt[b], min_dep[b]
+// mode 1: fill occ_node, occ_ent_ptr, loc_ent, node_occ
+__global__ void __launch_bounds__(PLAN_THREADS)
+k_block_build(int mode, int nv, int nb, const int32_t* __restrict__ blk_elem,
+              const int32_t* __restrict__ conn, const int32_t* __restrict__ csr_ptr,
+              const int32_t* __restrict__ csr_ent, int32_t* occ_cnt, int32_t* min_dep,
+              const int32_t* __restrict__ blk_occ, int32_t* occ_node, int32_t* occ_ent_ptr,
+              uint16_t* loc_ent, const int32_t* __restrict__ node_occ_ptr, int32_t* node_occ) {
+    __shared__ unsigned long long key[PLAN_MAX_KEYS];
+    __shared__ uint16_t runid[PLAN_MAX_KEYS];
+    __shared__ int32_t s_scan[PLAN_THREADS];
+    __shared__ int32_t s_mindep;
+    const int b = blockIdx.x;
+    const int e0 = blk_elem[b], e1 = blk_elem[b + 1];
+    const int cnt = (e1 - e0) * nv;
+    int P = 1;
+    while (P < cnt) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += PLAN_THREADS) {
+        if (i < cnt) {
+            int node = conn[(int64_t)e0 * nv + i];
+            key[i] = ((unsigned long long)(unsigned)node << 16) | (unsigned)i;
+        } else {
+            key[i] = ~0ull;
+        }
+    }
+    if (threadIdx.x == 0) s_mindep = b;
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < P; i += PLAN_THREADS) {
+                int ixj = i ^ j;
+                if (ixj > i) {
+                    unsigned long long x = key[i], y = key[ixj];
+                    bool up = (i & k) == 0;
+                    if ((x > y) == up) {
+                        key[i] = y;
+                        key[ixj] = x;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // run starts and their ranks (block-wide scan over per-thread chunk counts)
+    const int per = (cnt + PLAN_THREADS - 1) / PLAN_THREADS;
+    const int lo = threadIdx.x * per, hi = min(cnt, lo + per);
+    int local = 0;
+    for (int i = lo; i < hi; ++i)
+        local += (i == 0 || (key[i] >> 16) != (key[i - 1] >> 16)) ? 1 : 0;
+    s_scan[threadIdx.x] = local;
+    __syncthreads();
+    for (int off = 1; off < PLAN_THREADS; off <<= 1) {
+        int v = threadIdx.x >= off ? s_scan[threadIdx.x - off] : 0;
+        __syncthreads();
+        s_scan[threadIdx.x] += v;
+        __syncthreads();
+    }
+    int r = s_scan[threadIdx.x] - local;     // exclusive
+    for (int i = lo; i < hi; ++i) {
+        if (i == 0 || (key[i] >> 16) != (key[i - 1] >> 16)) ++r;
+        runid[i] = (uint16_t)(r - 1);
+    }
+    const int n_occ_b = s_scan[PLAN_THREADS - 1];
+    __syncthreads();
+    // per occurrence: kind, earlier-block rank, min dep
+    for (int i = threadIdx.x; i < cnt; i += PLAN_THREADS) {
+        bool start = (i == 0 || (key[i] >> 16) != (key[i - 1] >> 16));
+        int node = (int)(key[i] >> 16);
+        if (mode == 1) loc_ent[(int64_t)e0 * nv + i] = (uint16_t)(key[i] & 0xffffu);
+        if (!start) continue;
+        int kb = csr_ptr[node], ke = csr_ptr[node + 1];
+        int first = csr_ent[kb] / nv, last = csr_ent[ke - 1] / nv;
+        bool earlier = first < e0;
+        bool nonowner = last >= e1;
+        if (mode == 0) {
+            if (earlier && !nonowner) atomicMin(&s_mindep, block_of(first, blk_elem, nb));
+        } else {
+            int o = blk_occ[b] + runid[i];
+            occ_node[o] = node | (nonowner ? OCC_NONOWNER : 0) | (earlier && !nonowner ? OCC_EARLIER : 0);
+            occ_ent_ptr[o] = e0 * nv + i;
+            // rank of this block among the node's blocks = distinct blocks with elements < e0
+            int rank = 0, lastb = -1;
+            for (int k = kb; k < ke; ++k) {
+                int f = csr_ent[k] / nv;
+                if (f >= e0) break;
+                int bb = block_of(f, blk_elem, nb);
+                if (bb != lastb) { ++rank; lastb = bb; }
+            }
+            node_occ[node_occ_ptr[node] + rank] = o;
+        }
+    }
+    __syncthreads();
+    if (mode == 0 && threadIdx.x == 0) {
+        occ_cnt[b] = n_occ_b;
+        min_dep[b] = s_mindep;
+    }
+}
+
+// ------------------------------------------------------------------ host driver
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    cudaStream_t s = nullptr;
+    ~DevBuf() {
+        if (p) cudaFreeAsync(p, s);
+    }
+};
+
+pfem_status exclusive_scan_i32(const int32_t* in, int32_t* out, int n, cudaStream_t s) {
+    size_t tb = 0;
+    PFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n, s));
+    DevBuf tmp;
+    tmp.s = s;
+    PFEM_CUDA_TRY(cudaMallocAsync(&tmp.p, tb, s));
+    PFEM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, out, n, s));
+    count_launch();
+    return PFEM_OK;
+}
+
+inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+pfem_status prepare_impl(pfem_mesh* m, cudaStream_t s) {
+    const int D = m->dim, nv = D + 1, N = m->n_nodes, E = m->n_elems;
+    const int K = m->n_parts;
+    // ---------------- validation of connectivity
+    DevBuf scratch;
+    scratch.s = s;
+    const size_t n_int_scratch = 8 + (size_t)std::max(N + 1, m->max_colours + 1);
+    PFEM_CUDA_TRY(cudaMallocAsync(&scratch.p, sizeof(int32_t) * n_int_scratch, s));
+    int32_t* sc = (int32_t*)scratch.p;            // [0]=bad conn [1]=n_neg [2]=degenerate [3]=overflow [4]=maxc [5]=ticket
+    int32_t* cnt = sc + 8;                        // [N+1]
+    int32_t init[8] = {INT32_MAX, 0, INT32_MAX, INT32_MAX, -1, 0, 0, 0};
+    PFEM_CUDA_TRY(cudaMemcpyAsync(sc, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    k_check_conn<<<nblk((int64_t)E * nv, 256), 256, 0, s>>>(nv, E, N, m->conn, sc + 0);
+    PFEM_LAUNCH_CHECK("k_check_conn");
+    // ---------------- K1 geometry
+    if (D == 2) {
+        if (m->dtype == PFEM_F32)
+            k_geometry<2, float><<<nblk(E, 256), 256, 0, s>>>(E, m->coords, m->conn, (float*)m->grad,
+                                                                (float*)m->vol, sc + 1, sc + 2);
+        else
+            k_geometry<2, double><<<nblk(E, 256), 256, 0, s>>>(E, m->coords, m->conn, (double*)m->grad,
+                                                                 (double*)m->vol, sc + 1, sc + 2);
+    } else {
+        if (m->dtype == PFEM_F32)
+            k_geometry<3, float><<<nblk(E, 256), 256, 0, s>>>(E, m->coords, m->conn, (float*)m->grad,
+                                                                (float*)m->vol, sc + 1, sc + 2);
+        else
+            k_geometry<3, double><<<nblk(E, 256), 256, 0, s>>>(E, m->coords, m->conn, (double*)m->grad,
+                                                                 (double*)m->vol, sc + 1, sc + 2);
+    }
+    PFEM_LAUNCH_CHECK("k_geometry");
+    int32_t h[8];
+    PFEM_CUDA_TRY(cudaMemcpyAsync(h, sc, sizeof(h), cudaMemcpyDeviceToHost, s));
+    PFEM_CUDA_TRY(cudaStreamSynchronize(s));
+    if (h[0] != INT32_MAX) {
+        set_error("conn: node id out of range [0, n_nodes)", h[0]);
+        return PFEM_ERR_ARG;
+    }
+    if (h[2] != INT32_MAX) {
+        set_error("degenerate element (|det J| <= 64 eps prod |edges|)", h[2]);
+        return PFEM_ERR_DEGENERATE;
+    }
+    m->n_negative = h[1];
+    // ---------------- K2 CSR
+    const int64_t nent = (int64_t)E * nv;
+    PFEM_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (N + 1), s));
+    k_count<<<nblk(nent, 256), 256, 0, s>>>(nent, m->conn, cnt);
+    PFEM_LAUNCH_CHECK("k_count");
+    {
+        pfem_status st = exclusive_scan_i32(cnt, m->csr_ptr, N + 1, s);
+        if (st != PFEM_OK) return st;
+    }
+    PFEM_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (N + 1), s));
+    k_csr_fill<<<nblk(nent, 256), 256, 0, s>>>(nent, m->conn, m->csr_ptr, cnt, m->csr_ent);
+    PFEM_LAUNCH_CHECK("k_csr_fill");
+    k_csr_sort_rows<<<nblk(N, 128), 128, 0, s>>>(N, m->csr_ptr, m->csr_ent);
+    PFEM_LAUNCH_CHECK("k_csr_sort_rows");
+    // ---------------- K3 colouring
+    PFEM_CUDA_TRY(cudaMemsetAsync(m->colour, 0xff, sizeof(int32_t) * E, s));
+    {
+        int dev = 0, nsm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        k_colour_greedy<<<nsm * 8, 256, 0, s>>>(nv, E, m->conn, m->csr_ptr, m->csr_ent, m->colour, sc + 5,
+                                                  m->max_colours, sc + 3);
+        PFEM_LAUNCH_CHECK("k_colour_greedy");
+    }
+    PFEM_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (m->max_colours + 1), s));
+    k_colour_hist<<<nblk(E, 256), 256, 0, s>>>(E, m->colour, cnt, sc + 4);
+    PFEM_LAUNCH_CHECK("k_colour_hist");
+    PFEM_CUDA_TRY(cudaMemcpyAsync(h, sc, sizeof(h), cudaMemcpyDeviceToHost, s));
+    PFEM_CUDA_TRY(cudaStreamSynchronize(s));
+    if (h[3] != INT32_MAX) {
+        set_error("more colours than max_colours", h[3]);
+        return PFEM_ERR_CAPACITY;
+    }
+    m->n_colours = h[4] + 1;
+    k_colour_ptr<<<1, 32, 0, s>>>(m->n_colours, cnt, m->colour_ptr);
+    PFEM_LAUNCH_CHECK("k_colour_ptr");
+    {
+        // stable radix sort of (colour, element) pairs -> colour_elems
+        DevBuf tmp;
+        tmp.s = s;
+        int end_bit = 1;
+        while ((1 << end_bit) <= m->n_colours) ++end_bit;
+        size_t tb = 0;
+        int32_t* keys_out = nullptr;
+        int32_t* vals_in = nullptr;
+        PFEM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, m->colour, keys_out, vals_in,
+                                                      m->colour_elems, E, 0, end_bit, s));
+        size_t extra = align_up(sizeof(int32_t) * (size_t)E, 256);
+        PFEM_CUDA_TRY(cudaMallocAsync(&tmp.p, tb + 2 * extra, s));
+        keys_out = (int32_t*)tmp.p;
+        vals_in = (int32_t*)((char*)tmp.p + extra);
+        void* t2 = (char*)tmp.p + 2 * extra;
+        k_iota<<<nblk(E, 256), 256, 0, s>>>(E, vals_in);
+        PFEM_LAUNCH_CHECK("k_iota");
+        PFEM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(t2, tb, m->colour, keys_out, vals_in,
+                                                      m->colour_elems, E, 0, end_bit, s));
+        count_launch();
+    }
+    // ---------------- plan: element blocks (host bookkeeping on the part offsets)
+    std::vector<int32_t> pe(K + 1), pn(K + 1);
+    if (K == 1 || !m->part_elem) {
+        pe = {0, E};
+        pn = {0, N};
+    } else {
+        PFEM_CUDA_TRY(cudaMemcpyAsync(pe.data(), m->part_elem, sizeof(int32_t) * (K + 1), cudaMemcpyDeviceToHost, s));
+        PFEM_CUDA_TRY(cudaMemcpyAsync(pn.data(), m->part_node, sizeof(int32_t) * (K + 1), cudaMemcpyDeviceToHost, s));
+        PFEM_CUDA_TRY(cudaStreamSynchronize(s));
+        if (pe[0] != 0 || pe[K] != E || pn[0] != 0 || pn[K] != N) {
+            set_error("part offsets must start at 0 and end at n_elems / n_nodes");
+            return PFEM_ERR_ARG;
+        }
+        for (int k = 0; k < K; ++k)
+            if (pe[k + 1] < pe[k] || pn[k + 1] < pn[k]) {
+                set_error("part offsets must be non-decreasing", k);
+                return PFEM_ERR_ARG;
+            }
+    }
+    int eb = m->block_elems > 0 ? m->block_elems : (D == 3 ? 512 : 1024);
+    eb = std::min(eb, PLAN_MAX_KEYS / nv);
+    std::vector<int32_t> blk_elem{0}, part_blk{0};
+    for (int k = 0; k < K; ++k) {
+        int n = pe[k + 1] - pe[k];
+        int nbk = (n + eb - 1) / eb;
+        for (int i = 1; i <= nbk; ++i) blk_elem.push_back(pe[k] + (int)((int64_t)n * i / nbk));
+        part_blk.push_back((int)blk_elem.size() - 1);
+    }
+    const int nb = (int)blk_elem.size() - 1;
+    int eb_max = 0;
+    for (int b = 0; b < nb; ++b) eb_max = std::max(eb_max, blk_elem[b + 1] - blk_elem[b]);
+
+    // reduction chunks: <= CHUNK consecutive blocks inside one part
+    std::vector<int32_t> blk_chunk(nb), chunk_blk{0}, part_chunk{0};
+    for (int k = 0; k < K; ++k) {
+        for (int b0 = part_blk[k]; b0 < part_blk[k + 1]; b0 += CHUNK_BLOCKS) {
+            int b1 = std::min(part_blk[k + 1], b0 + CHUNK_BLOCKS);
+            for (int b = b0; b < b1; ++b) blk_chunk[b] = (int)chunk_blk.size() - 1;
+            chunk_blk.push_back(b1);
+        }
+        part_chunk.push_back((int)chunk_blk.size() - 1);
+    }
+    const int nch = (int)chunk_blk.size() - 1;
+
+    Plan* P = new Plan();
+    P->dim = D; P->n_nodes = N; P->n_elems = E; P->n_parts = K;
+    P->n_blocks = nb; P->eb_max = eb_max; P->n_chunks = nch;
+    // first allocation: everything whose size is known now
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t at = o; o += align_up(bytes, 256); return at; };
+    size_t o_be = take(sizeof(int32_t) * (nb + 1)), o_bo = take(sizeof(int32_t) * (nb + 1)),
+           o_md = take(sizeof(int32_t) * (nb + 1)), o_pb = take(sizeof(int32_t) * (K + 1)),
+           o_pn = take(sizeof(int32_t) * (K + 1)), o_pe = take(sizeof(int32_t) * (K + 1)),
+           o_bc = take(sizeof(int32_t) * (nb + 1)), o_cb = take(sizeof(int32_t) * (nch + 1)),
+           o_pc = take(sizeof(int32_t) * (K + 1)), o_le = take(sizeof(uint16_t) * (size_t)nent),
+           o_np = take(sizeof(int32_t) * ((size_t)N + 1)), o_cnt = take(sizeof(int32_t) * (nb + 1));
+    size_t fixed = o;
+    void* pool1 = nullptr;
+    cudaError_t ce = cudaMallocAsync(&pool1, fixed, s);
+    if (ce != cudaSuccess) { delete P; return cuda_status(ce, "plan alloc"); }
+    auto bind = [&](char* pb) {
+        P->blk_elem = (int32_t*)(pb + o_be);
+        P->blk_occ = (int32_t*)(pb + o_bo);
+        P->blk_min_dep = (int32_t*)(pb + o_md);
+        P->part_blk = (int32_t*)(pb + o_pb);
+        P->part_node = (int32_t*)(pb + o_pn);
+        P->part_elem = (int32_t*)(pb + o_pe);
+        P->blk_chunk = (int32_t*)(pb + o_bc);
+        P->chunk_blk = (int32_t*)(pb + o_cb);
+        P->part_chunk = (int32_t*)(pb + o_pc);
+        P->loc_ent = (uint16_t*)(pb + o_le);
+        P->node_occ_ptr = (int32_t*)(pb + o_np);
+    };
+    bind((char*)pool1);
+    int32_t* occ_cnt = (int32_t*)((char*)pool1 + o_cnt);
+    P->pool = pool1;
+    auto fail = [&](pfem_status st) { cudaFreeAsync(P->pool, s); delete P; return st; };
+#define PLAN_TRY(expr) do { cudaError_t _e = (expr); if (_e != cudaSuccess) return fail(cuda_status(_e, #expr)); } while (0)
+    PLAN_TRY(cudaMemcpyAsync(P->blk_elem, blk_elem.data(), sizeof(int32_t) * (nb + 1), cudaMemcpyHostToDevice, s));
+    PLAN_TRY(cudaMemcpyAsync(P->part_blk, part_blk.data(), sizeof(int32_t) * (K + 1), cudaMemcpyHostToDevice, s));
+    PLAN_TRY(cudaMemcpyAsync(P->part_node, pn.data(), sizeof(int32_t) * (K + 1), cudaMemcpyHostToDevice, s));
+    PLAN_TRY(cudaMemcpyAsync(P->part_elem, pe.data(), sizeof(int32_t) * (K + 1), cudaMemcpyHostToDevice, s));
+    PLAN_TRY(cudaMemcpyAsync(P->blk_chunk, blk_chunk.data(), sizeof(int32_t) * nb, cudaMemcpyHostToDevice, s));
+    PLAN_TRY(cudaMemcpyAsync(P->chunk_blk, chunk_blk.data(), sizeof(int32_t) * (nch + 1), cudaMemcpyHostToDevice, s));
+    PLAN_TRY(cudaMemcpyAsync(P->part_chunk, part_chunk.data(), sizeof(int32_t) * (K + 1), cudaMemcpyHostToDevice, s));
+    P->colour_ptr_host.resize(m->n_colours + 1);
+    PLAN_TRY(cudaMemcpyAsync(P->colour_ptr_host.data(), m->colour_ptr, sizeof(int32_t) * (m->n_colours + 1),
+                             cudaMemcpyDeviceToHost, s));
+    // node-major occurrence counts -> node_occ_ptr
+    k_node_occ_count<<<nblk(N, 256), 256, 0, s>>>(N, nv, m->csr_ptr, m->csr_ent, P->blk_elem, nb, cnt);
+    count_launch();
+    PLAN_TRY(cudaGetLastError());
+    {
+        pfem_status st = exclusive_scan_i32(cnt, P->node_occ_ptr, N + 1, s);
+        if (st != PFEM_OK) return fail(st);
+    }
+    k_block_build<<<nb, PLAN_THREADS, 0, s>>>(0, nv, nb, P->blk_elem, m->conn, m->csr_ptr, m->csr_ent,
+                                              occ_cnt, P->blk_min_dep, nullptr, nullptr, nullptr,
+                                              nullptr, nullptr, nullptr);
+    count_launch();
+    PLAN_TRY(cudaGetLastError());
+    PLAN_TRY(cudaMemsetAsync(occ_cnt + nb, 0, sizeof(int32_t), s));
+    {
+        pfem_status st = exclusive_scan_i32(occ_cnt, P->blk_occ, nb + 1, s);
+        if (st != PFEM_OK) return fail(st);
+    }
+    int32_t n_occ = 0;
+    PLAN_TRY(cudaMemcpyAsync(&n_occ, P->blk_occ + nb, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    PLAN_TRY(cudaStreamSynchronize(s));
+    P->n_occ = n_occ;
+    // second allocation: occurrence arrays
+    size_t o2 = 0;
+    auto take2 = [&](size_t bytes) { size_t at = o2; o2 += align_up(bytes, 256); return at; };
+    size_t q_on = take2(sizeof(int32_t) * (size_t)n_occ), q_oe = take2(sizeof(int32_t) * ((size_t)n_occ + 1)),
+           q_no = take2(sizeof(int32_t) * (size_t)n_occ);
+    // grow the pool: allocate a new pool of fixed + o2 and copy the fixed part
+    void* pool2 = nullptr;
+    PLAN_TRY(cudaMallocAsync(&pool2, fixed + o2, s));
+    PLAN_TRY(cudaMemcpyAsync(pool2, pool1, fixed, cudaMemcpyDeviceToDevice, s));
+    PLAN_TRY(cudaFreeAsync(pool1, s));
+    P->pool = pool2;
+    char* pb = (char*)pool2;
+    bind(pb);
+    P->occ_node = (int32_t*)(pb + fixed + q_on);
+    P->occ_ent_ptr = (int32_t*)(pb + fixed + q_oe);
+    P->node_occ = (int32_t*)(pb + fixed + q_no);
+    occ_cnt = (int32_t*)(pb + o_cnt);
+    k_block_build<<<nb, PLAN_THREADS, 0, s>>>(1, nv, nb, P->blk_elem, m->conn, m->csr_ptr, m->csr_ent,
+                                              nullptr, nullptr, P->blk_occ, P->occ_node, P->occ_ent_ptr,
+                                              P->loc_ent, P->node_occ_ptr, P->node_occ);
+    count_launch();
+    PLAN_TRY(cudaGetLastError());
+    int32_t tail = (int32_t)nent;
+    PLAN_TRY(cudaMemcpyAsync(P->occ_ent_ptr + n_occ, &tail, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    PLAN_TRY(cudaStreamSynchronize(s));
+#undef PLAN_TRY
+    m->n_blocks = nb;
+    m->n_occ = n_occ;
+    m->plan = reinterpret_cast<pfem_plan*>(P);
+    return PFEM_OK;
+}
+
+void release_impl(pfem_mesh* m) {
+    if (!m || !m->plan) return;
+    Plan* P = reinterpret_cast<Plan*>(m->plan);
+    if (P->pool) cudaFree(P->pool);
+    delete P;
+    m->plan = nullptr;
+}
+
+}  // namespace pfem

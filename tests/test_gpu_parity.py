@@ -1,0 +1,301 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the fp64 CPU oracle on the same
+seeded inputs.  Bars (BASELINE.json north star): bit-exact CSR / colouring; rel-L2 <= 1e-12
+(fp64) and <= 2e-5 (fp32) for energies, residuals and K.v."""
+import numpy as np
+import pytest
+import torch
+
+from helpers import TOL, gpu_problem, max_rel, oracle_problem, rel_l2, rounded
+from pfem_gen import (config1, config2, config3, config4, config5, fourier_field, kuhn_cube, plate_with_holes,
+                      square_t3)
+from pfem_gen.configs import Problem
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2601_03086_b200 as pf
+    pf.load()
+
+
+def small_problems():
+    """Several tiles + ragged tails, both dims, both models, multi-part."""
+    rng = np.random.default_rng(77)
+    c, t, _ = plate_with_holes(40, np.random.default_rng(3))
+    u = rng.normal(0, 0.02, (3,) + c.shape)
+    yield Problem("plate40-lin-f64", 2, c, t, "linear", "young_poisson",
+                  np.exp(0.5 * rng.standard_normal(len(t))), np.array([0.3]), u, "f64")
+    un = np.stack([0.05 * fourier_field(c, rng) for _ in range(3)])
+    yield Problem("plate40-nh-f32", 2, c, t, "neohookean", "lame", rng.uniform(0.3, 1, len(t)),
+                  rng.uniform(0.3, 1, len(t)), un, "f32")
+    c3, t3 = kuhn_cube(13, brick=4)
+    u3 = rng.normal(0, 0.01, (5,) + c3.shape)
+    u3n = np.stack([0.1 * fourier_field(c3, rng) + rng.normal(0, 1e-3, c3.shape) for _ in range(5)])
+    yield Problem("cube13-nh-f32", 3, c3, t3, "neohookean", "lame", np.array([0.4]), np.array([0.6]), u3n, "f32")
+    yield Problem("cube13-lin-f64", 3, c3, t3, "linear", "young_poisson", rng.uniform(1, 10, len(t3)),
+                  np.array([0.3]), u3[:2], "f64")
+    # two parts (ragged), NH 2-D
+    ca, ta = square_t3(23, 17)
+    cb, tb = square_t3(9, 31)
+    coords = np.concatenate([ca, cb + 3.0])
+    conn = np.concatenate([ta, tb + len(ca)]).astype(np.int32)
+    up = 0.003 * rng.standard_normal((1,) + coords.shape)
+    yield Problem("two-parts-nh-f64", 2, coords, conn, "neohookean", "lame", np.array([0.4]), np.array([0.6]),
+                  up, "f64", part_elem=np.array([0, len(ta), len(conn)], np.int32),
+                  part_node=np.array([0, len(ca), len(coords)], np.int32))
+
+
+SMALL = list(small_problems())
+
+
+# ------------------------------------------------------------------ prep
+@pytest.mark.parametrize("prob", SMALL + [config1()], ids=lambda p: p.name)
+def test_prepare_bitexact(orc, prob):
+    mesh, _, _ = gpu_problem(prob)
+    ptr, ent = orc.csr(prob.conn, prob.n_nodes)
+    assert np.array_equal(mesh.csr_ptr.cpu().numpy(), ptr)
+    assert np.array_equal(mesh.csr_ent.cpu().numpy(), ent)
+    col, nc = orc.colour(prob.conn, prob.n_nodes, ptr, ent)
+    assert mesh.n_colours == nc
+    assert np.array_equal(mesh.colour.cpu().numpy(), col)
+    elems, cptr = orc.colour_sort(col, nc)
+    assert np.array_equal(mesh.colour_elems.cpu().numpy(), elems)
+    assert np.array_equal(mesh.colour_ptr[: nc + 1].cpu().numpy(), cptr)
+    g, v, sgn = orc.geometry(prob.coords, prob.conn)
+    d = prob.dim
+    G = mesh.grad.double().cpu().numpy().reshape(d, d, -1).transpose(2, 0, 1)
+    tol = 1e-14 if prob.dtype == "f64" else 1e-7
+    assert rel_l2(G, g) < tol and rel_l2(mesh.vol.double().cpu().numpy(), v) < tol
+    assert mesh.n_negative == int((sgn < 0).sum())
+
+
+@pytest.mark.parametrize("prob", SMALL[:3], ids=lambda p: p.name)
+def test_plan_is_a_partition_of_the_csr(orc, prob):
+    """Every (element, slot) entry appears exactly once, under the occurrence of its own
+    node, inside its own block; occurrences of a block are sorted by node; exactly one
+    owner per node (the block of its highest element)."""
+    mesh, _, _ = gpu_problem(prob, block_elems=97)    # small blocks -> many boundaries
+    P = mesh.plan_export()
+    nv = prob.dim + 1
+    be, bo, on, oe, le = P["blk_elem"], P["blk_occ"], P["occ_node"], P["occ_ent_ptr"], P["loc_ent"]
+    seen = np.zeros(prob.n_elems * nv, np.int32)
+    owners = np.zeros(prob.n_nodes, np.int32)
+    for b in range(len(be) - 1):
+        nodes = on[bo[b]:bo[b + 1]] & 0x1FFFFFFF
+        assert np.all(np.diff(nodes) > 0)
+        for o in range(bo[b], bo[b + 1]):
+            n = on[o] & 0x1FFFFFFF
+            if not (on[o] & 0x40000000):
+                owners[n] += 1
+            ents = le[oe[o]:oe[o + 1]].astype(np.int64)
+            assert np.all(np.diff(ents) > 0)
+            glob = be[b] * nv + ents
+            assert np.all(glob < be[b + 1] * nv)
+            assert np.all(prob.conn.reshape(-1)[glob] == n)
+            seen[glob] += 1
+    assert np.all(seen == 1)
+    used = np.unique(prob.conn)
+    assert np.all(owners[used] == 1)
+
+
+# ------------------------------------------------------------------ energy / residual
+def check_energy(orc, prob, mode, block_elems=0, f_ext=None):
+    mesh, mat, u = gpu_problem(prob, block_elems=block_elems)
+    om = oracle_problem(orc, prob)
+    ur = rounded(prob.u, prob.dtype)
+    fe = None if f_ext is None else rounded(f_ext, prob.dtype)
+    W_ref, tot_ref = om.energy(ur, f_ext=fe)
+    r_ref = om.residual(ur)
+    import paper_2601_03086_b200 as pf
+    ft = None if fe is None else torch.as_tensor(fe, dtype=u.dtype, device="cuda")
+    tot, W, r = pf.energy(mesh, mat, u, f_ext=ft, elem_energy=True, residual=True, mode=mode)
+    torch.cuda.synchronize()
+    tol = TOL[prob.dtype]
+    assert rel_l2(W.cpu().numpy(), W_ref) < tol, rel_l2(W.cpu().numpy(), W_ref)
+    assert max_rel(tot.cpu().numpy(), tot_ref) < (tol if prob.dtype == "f64" else 1e-5)
+    assert rel_l2(r.cpu().numpy(), r_ref) < tol, rel_l2(r.cpu().numpy(), r_ref)
+    r2 = pf.residual(mesh, mat, u, mode=mode)
+    torch.cuda.synchronize()
+    assert torch.equal(r2, r) or rel_l2(r2.cpu().numpy(), r_ref) < tol
+    return mesh, mat, u
+
+
+@pytest.mark.parametrize("mode", ["csr", "colour"])
+@pytest.mark.parametrize("prob", SMALL + [config1()], ids=lambda p: p.name)
+def test_energy_residual_small(orc, prob, mode):
+    rng = np.random.default_rng(5)
+    f = rng.standard_normal(prob.coords.shape) * 1e-2
+    check_energy(orc, prob, mode, f_ext=f)
+    check_energy(orc, prob, mode, block_elems=61)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_config2_full(orc, dtype):
+    p = config2(dtype=dtype)
+    check_energy(orc, p, "csr")
+
+
+def test_config3_full(orc):
+    check_energy(orc, config3(), "csr")
+
+
+def test_config5_full(orc):
+    check_energy(orc, config5(), "csr")
+
+
+def test_config5_colour(orc):
+    check_energy(orc, config5(), "colour")
+
+
+# ------------------------------------------------------------------ tangent
+def check_tangent(orc, prob, mode, mask=None, seed=9, block_elems=0):
+    import paper_2601_03086_b200 as pf
+    mesh, mat, u = gpu_problem(prob, block_elems=block_elems)
+    om = oracle_problem(orc, prob)
+    rng = np.random.default_rng(seed)
+    v = rounded(rng.standard_normal(prob.u.shape), prob.dtype)
+    ur = rounded(prob.u, prob.dtype)
+    ref = om.tangent(v, u=ur if prob.model == "neohookean" else None, mask=mask)
+    vt = torch.as_tensor(v, dtype=u.dtype, device="cuda")
+    mt = None if mask is None else torch.as_tensor(mask, dtype=torch.uint8, device="cuda")
+    Kv = pf.tangent_apply(mesh, mat, vt, u=u if prob.model == "neohookean" else None, mask=mt, mode=mode)
+    torch.cuda.synchronize()
+    err = rel_l2(Kv.cpu().numpy(), ref)
+    assert err < TOL[prob.dtype], err
+
+
+@pytest.mark.parametrize("mode", ["csr", "colour"])
+@pytest.mark.parametrize("prob", SMALL, ids=lambda p: p.name)
+def test_tangent_small(orc, prob, mode):
+    check_tangent(orc, prob, mode)
+    check_tangent(orc, prob, mode, block_elems=53)
+    mask = (np.random.default_rng(2).random(prob.n_nodes * prob.dim) < 0.2).astype(np.uint8)
+    check_tangent(orc, prob, mode, mask=mask)
+
+
+def test_config4_tangent_full(orc):
+    p = config4()
+    check_tangent(orc, p, "csr")
+    check_tangent(orc, p, "csr", mask=p.mask)
+
+
+def test_config3_tangent_full(orc):
+    check_tangent(orc, config3(), "csr")
+
+
+# ------------------------------------------------------------------ determinism, flags
+@pytest.mark.parametrize("mode", ["csr", "colour"])
+def test_bitwise_deterministic(mode):
+    import paper_2601_03086_b200 as pf
+    p = SMALL[2]
+    mesh, mat, u = gpu_problem(p, block_elems=100)
+    outs = []
+    for _ in range(3):
+        tot, W, r = pf.energy(mesh, mat, u, elem_energy=True, residual=True, mode=mode)
+        Kv = pf.tangent_apply(mesh, mat, u, u=u, mode=mode)
+        torch.cuda.synchronize()
+        outs.append((tot.clone(), W.clone(), r.clone(), Kv.clone()))
+    for o in outs[1:]:
+        for a, b in zip(o, outs[0]):
+            assert torch.equal(a, b)
+
+
+def test_inversion_flags():
+    import paper_2601_03086_b200 as pf
+    coords = np.array([[0., 0], [1, 0], [0, 1], [1, 1]])
+    conn = np.array([[0, 1, 2], [1, 3, 2]], np.int32)
+    u = np.zeros((1, 4, 2))
+    u[0, 3] = [-1.5, -1.5]
+    p = Problem("inv", 2, coords, conn, "neohookean", "lame", np.array([0.4]), np.array([0.6]), u, "f64")
+    mesh, mat, ut = gpu_problem(p)
+    flags = torch.zeros(4, dtype=torch.int32, device="cuda")
+    tot, W, r = pf.energy(mesh, mat, ut, elem_energy=True, residual=True, flags=flags)
+    torch.cuda.synchronize()
+    f = flags.cpu().numpy()
+    assert f[0] == 1 and f[1] == 1
+    assert not np.isfinite(W[0, 1].item())
+    # a following clean call reports zero
+    tot, W, r = pf.energy(mesh, mat, torch.zeros_like(ut), residual=True, flags=flags)
+    torch.cuda.synchronize()
+    assert flags.cpu().numpy()[0] == 0 and flags.cpu().numpy()[1] == -1
+
+
+# ------------------------------------------------------------------ invariants through the GPU path
+def test_gpu_invariants_translation_and_patch():
+    import paper_2601_03086_b200 as pf
+    c3, t3 = kuhn_cube(9, brick=4)
+    u = np.tile([0.3, -0.2, 0.1], (len(c3), 1))[None]
+    p = Problem("tr", 3, c3, t3, "neohookean", "lame", np.array([0.4]), np.array([0.6]), u, "f64")
+    mesh, mat, ut = gpu_problem(p)
+    tot, W, r = pf.energy(mesh, mat, ut, elem_energy=True, residual=True)
+    torch.cuda.synchronize()
+    assert torch.all(W == 0) and torch.all(r == 0)
+    A = np.array([[0.01, 0.02, 0.0], [-0.01, 0.03, 0.005], [0.0, 0.01, -0.02]])
+    ua = torch.as_tensor((c3 @ A.T)[None], device="cuda")
+    tot, W, r = pf.energy(mesh, mat, ua, residual=True)
+    torch.cuda.synchronize()
+    F = np.eye(3) + A
+    J = np.linalg.det(F)
+    psi = 0.3 * np.log(J) ** 2 - 0.4 * np.log(J) + 0.2 * (np.sum(F * F) - 3)
+    assert abs(tot.item() - psi) < 1e-13 * psi
+    rs = r[0].cpu().numpy()
+    assert np.max(np.abs(rs.sum(0))) < 1e-15
+    interior = np.all((c3 > 1e-9) & (c3 < 1 - 1e-9), axis=1)
+    assert np.max(np.abs(rs[interior])) < 1e-15
+
+
+# ------------------------------------------------------------------ CG
+def test_cg_tiny_matches_oracle_and_dense(orc):
+    import paper_2601_03086_b200 as pf
+    p = config1()
+    mesh, mat, _ = gpu_problem(p)
+    om = oracle_problem(orc, p)
+    f = torch.as_tensor(p.f_ext, device="cuda")
+    mask = torch.as_tensor(p.mask, device="cuda")
+    x0 = torch.zeros_like(f)
+    for tol in (1e-8, 1e-12):
+        x, rep = pf.cg(mesh, mat, f, x0, mask=mask, tol=tol)
+        xo, ro = om.cg(p.f_ext, p.mask, np.zeros_like(p.f_ext), tol=tol)
+        assert rep["converged"] and abs(rep["iterations"] - ro["iterations"]) <= 1
+        assert rel_l2(x.cpu().numpy(), xo) < 10 * tol
+        h = rep["history"]
+        assert np.max(np.abs(h[:20] - ro["history"][:20]) / ro["history"][:20]) < 1e-6
+    # exact start -> 0 iterations (skip rule)
+    x1, rep1 = pf.cg(mesh, mat, f, x, mask=mask, tol=1e-8)
+    assert rep1["iterations"] == 0 and rep1["converged"]
+
+
+def assert_cg_count(rep, ro, spread):
+    """Reading R18: |dk| <= 1 vs the default oracle, or inside the oracle's own spread over
+    5 valid dot-product orderings (+-1); first 50 residual-history entries agree to 1e-6."""
+    k = rep["iterations"]
+    ok = abs(k - ro["iterations"]) <= 1 or (min(spread) - 1 <= k <= max(spread) + 1)
+    assert ok, (k, ro["iterations"], spread)
+    h, ho = rep["history"], ro["history"]
+    m = min(50, len(h), len(ho))
+    assert np.max(np.abs(h[:m] - ho[:m]) / ho[:m]) < 1e-6
+
+
+@pytest.mark.parametrize("n", [12, 20])
+def test_cg_config4_scaled(orc, n):
+    """Config-4 recipe at n^3 nodes: iteration count vs the oracle (R18), zero and warm start."""
+    import paper_2601_03086_b200 as pf
+    from pfem_gen import small_cube_problem, warm_start
+    p = small_cube_problem(n_nodes=n, brick=4)
+    mesh, mat, _ = gpu_problem(p)
+    om = oracle_problem(orc, p)
+    f = torch.as_tensor(p.f_ext, device="cuda")
+    mask = torch.as_tensor(p.mask, device="cuda")
+    xs, _ = om.cg(p.f_ext, p.mask, np.zeros_like(p.f_ext), tol=1e-12, history=False)
+    x0w = warm_start(xs, p.mask, seed=4004)
+    for x0 in (np.zeros_like(p.f_ext), x0w):
+        for mode in ("csr", "colour"):
+            x, rep = pf.cg(mesh, mat, f, torch.as_tensor(x0, device="cuda"), mask=mask, tol=1e-8, mode=mode)
+            xo, ro = om.cg(p.f_ext, p.mask, x0, tol=1e-8)
+            assert rep["converged"] and ro["converged"]
+            assert_cg_count(rep, ro, om.cg_spread(p.f_ext, p.mask, x0, tol=1e-8))
+            assert rep["true_rel_res_final"] < 2e-8
+            assert rel_l2(x.cpu().numpy(), xo) < 1e-6
