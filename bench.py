@@ -1,0 +1,477 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the PFEM explicit-FE hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--no-extras]
+
+Workload: BASELINE.json config 3 — unit cube, 64^3 nodes, Kuhn T4
+(1,500,282 tets), compressible Neo-Hookean mu=0.4 lambda=0.6, S=4 displacement fields,
+fp32.  One STEP = one pass of §8 rows a2-a6 over the batch: the fused
+energy+residual kernel (pfem_energy with W_e and r) followed by the matrix-free tangent
+K(u).v (pfem_tangent_apply) on the same 4 fields.  value = element-samples per second
+(E*S per step / step time), whole job over all ranks.  Inputs rotate over 3 independent
+copies (mesh + fields, ~0.5 GB) so every step reads HBM, not L2 (no flush in the timed
+region).  Row a7 (warm-started CG, config 4) and config 5 are reported under "extras".
+
+--impl reference times the CPU oracle (oracle/, fp64) on a bounded sample of the same
+workload on this box's host cores (the reference arm of this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "element-samples/s through fused energy+residual and K(u)v (config 3)"
+UNIT = "element-samples/s"
+N_COPIES = 3
+
+
+def dist_info():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- bytes model
+def bytes_energy_residual(E, N, d, S, s, want_W=True, mat_per_elem=0, K=1):
+    """Algorithmic bytes of one fused energy+residual launch: conn, grad, vol,
+    material read once; u read once; r written once; W_e written once; totals."""
+    return (E * ((d + 1) * 4 + (d * d + 1) * s + mat_per_elem * s) +
+            S * (N * d * s * 2 + (E * s if want_W else 0)) + S * K * s)
+
+
+def bytes_tangent(E, N, d, S, s, nh, mat_per_elem=0, masked=False):
+    """K(u).v: element arrays once; v read, Kv written, u read (NH), mask read (1 B/DOF)."""
+    return (E * ((d + 1) * 4 + (d * d + 1) * s + mat_per_elem * s) +
+            S * N * d * s * (3 if nh else 2) + (N * d if masked else 0))
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def build_workload(torch, pf, dev, prob, copies):
+    """`copies` independent (mesh, material, u, v, outputs) sets on the device."""
+    sets = []
+    rng = np.random.default_rng(3005)
+    v_host = rng.standard_normal(prob.u.shape)
+    for _ in range(copies):
+        mesh = pf.Mesh(torch.as_tensor(prob.coords, device=dev), torch.as_tensor(prob.conn, device=dev),
+                       dtype=torch.float32)
+        mat = pf.Material(prob.model, prob.param_kind,
+                          torch.as_tensor(np.asarray(prob.p0), dtype=torch.float32, device=dev),
+                          torch.as_tensor(np.asarray(prob.p1), dtype=torch.float32, device=dev))
+        u = torch.as_tensor(prob.u, dtype=torch.float32, device=dev).contiguous()
+        v = torch.as_tensor(v_host, dtype=torch.float32, device=dev).contiguous()
+        S = u.shape[0]
+        outs = (torch.empty((S, 1), dtype=torch.float32, device=dev),
+                torch.empty((S, prob.n_elems), dtype=torch.float32, device=dev),
+                torch.empty_like(u))
+        Kv = torch.empty_like(u)
+        mesh.workspace(S)
+        sets.append({"mesh": mesh, "mat": mat, "u": u, "v": v, "outs": outs, "Kv": Kv})
+    return sets
+
+
+def step(pf, st, ev=None):
+    if ev is not None:
+        ev[0].record()
+    pf.energy(st["mesh"], st["mat"], st["u"], elem_energy=True, residual=True, out=st["outs"])
+    if ev is not None:
+        ev[1].record()
+    pf.tangent_apply(st["mesh"], st["mat"], st["v"], u=st["u"], out=st["Kv"])
+    if ev is not None:
+        ev[2].record()
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as tdist
+    import paper_2601_03086_b200 as pf
+    from pfem_gen import config3
+
+    world, rank, local = dist_info()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (there is no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=dev)
+    pf.load()
+    prob = config3()
+    E, N, d, S = prob.n_elems, prob.n_nodes, prob.dim, prob.n_samples
+    t_prep0 = time.perf_counter()
+    sets = build_workload(torch, pf, dev, prob, N_COPIES)
+    torch.cuda.synchronize()
+    prep_s = (time.perf_counter() - t_prep0) / N_COPIES
+
+    for i in range(args.warmup):
+        step(pf, sets[i % N_COPIES])
+    torch.cuda.synchronize()
+
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.2)
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    pf.launch_count(reset=True)
+    t_start.record()
+    for i in range(K):
+        step(pf, sets[i % N_COPIES], evs[i])
+    t_end.record()
+    torch.cuda.synchronize()
+    launches = pf.launch_count()
+    if world > 1:
+        tdist.barrier()
+    clk = clocks.stop()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    er_ms = np.array([e[0].elapsed_time(e[1]) for e in evs])
+    tg_ms = np.array([e[1].elapsed_time(e[2]) for e in evs])
+    if world > 1:
+        t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    ms_per_step = elapsed_ms / K
+    value = world * E * S / (ms_per_step * 1e-3)
+
+    peak, peak_src = load_peaks()
+    B_er = bytes_energy_residual(E, N, d, S, 4)
+    B_tg = bytes_tangent(E, N, d, S, 4, nh=True)
+    er_avg = float(er_ms.mean())
+    traffic = load_traffic().get("config3_energy_residual")
+    roofline = {"bound": "hbm", "achieved": B_er / (er_avg * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                "frac": B_er / (er_avg * 1e-3) / 1e9 / peak,
+                "traffic": None if traffic is None else traffic.get("dram_bytes_per_launch"),
+                "kernel": "k_assemble<3,NH,f32,ENERGY_RESIDUAL,ST=4> (pfem_energy)",
+                "algorithmic_bytes": B_er, "avg_launch_us": er_avg * 1e3, "peak_source": peak_src,
+                "tangent": {"kernel": "k_assemble<3,NH,f32,TANGENT,ST=4> (pfem_tangent_apply)",
+                            "algorithmic_bytes": B_tg, "avg_launch_us": float(tg_ms.mean()) * 1e3,
+                            "achieved": B_tg / (tg_ms.mean() * 1e-3) / 1e9,
+                            "frac": B_tg / (tg_ms.mean() * 1e-3) / 1e9 / peak}}
+
+    # ---------------- e2e: host buffers through the public API, copies inside the timed region
+    st = sets[0]
+    u_h = st["u"].cpu().pin_memory()
+    v_h = st["v"].cpu().pin_memory()
+    tot_h = torch.empty(st["outs"][0].shape, dtype=torch.float32).pin_memory()
+    r_h = torch.empty(st["u"].shape, dtype=torch.float32).pin_memory()
+    kv_h = torch.empty(st["u"].shape, dtype=torch.float32).pin_memory()
+    Ke = max(5, min(50, K // 10))
+
+    def e2e_step():
+        st["u"].copy_(u_h, non_blocking=True)
+        st["v"].copy_(v_h, non_blocking=True)
+        step(pf, st)
+        tot_h.copy_(st["outs"][0], non_blocking=True)
+        r_h.copy_(st["outs"][2], non_blocking=True)
+        kv_h.copy_(st["Kv"], non_blocking=True)
+
+    for _ in range(3):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        tdist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(Ke):
+        e2e_step()
+    b.record()
+    torch.cuda.synchronize()
+    e2e_ms = a.elapsed_time(b) / Ke
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = {"value": world * E * S / (e2e_ms * 1e-3), "unit": UNIT,
+           "h2d_bytes_per_step": int(u_h.numel() * 4 + v_h.numel() * 4),
+           "d2h_bytes_per_step": int(tot_h.numel() * 4 + r_h.numel() * 4 + kv_h.numel() * 4),
+           "ms_per_step": e2e_ms}
+
+    extras = {}
+    if rank == 0 and not args.no_extras:
+        del sets
+        torch.cuda.empty_cache()
+        extras = run_extras(torch, pf, dev, peak)
+        extras["config3_prepare_s"] = prep_s
+
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+           "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded generators, pfem_gen)",
+           "config": {"workload": "config3", "mesh": "unit cube 64^3 nodes, Kuhn T4", "n_elems": E, "n_nodes": N,
+                      "model": "neohookean mu=0.4 lam=0.6", "samples_per_rank": S, "global_batch": S * world,
+                      "step": "pfem_energy(W_e, totals, residual) + pfem_tangent_apply(K(u)v)",
+                      "assembly": "csr", "parallelism": f"replicas x{world} (independent batches, no collective)",
+                      "l2": f"inputs larger than L2: {N_COPIES} rotating copies (~{N_COPIES * (B_er + B_tg) / 1e9:.2f} GB)"},
+           "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(prob)
+    if extras:
+        out["extras"] = extras
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
+
+
+def time_events(torch, fn, reps):
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def run_extras(torch, pf, dev, peak):
+    """Config 4 (K.v roofline, warm-started CG) and config 5 (64-part fused E+R)."""
+    from pfem_gen import config4, config5, warm_start
+    ex = {}
+    # ---------------- config 4: K.v fp64 + CG from zero / perturbed-exact warm start
+    p4 = config4()
+    E, N = p4.n_elems, p4.n_nodes
+    t0 = time.perf_counter()
+    m4 = pf.Mesh(torch.as_tensor(p4.coords, device=dev), torch.as_tensor(p4.conn, device=dev), dtype=torch.float64)
+    torch.cuda.synchronize()
+    prep = time.perf_counter() - t0
+    mat4 = pf.Material("linear", "young_poisson", torch.as_tensor(p4.p0, device=dev), torch.as_tensor(p4.p1, device=dev))
+    mask = torch.as_tensor(p4.mask, device=dev)
+    f = torch.as_tensor(p4.f_ext, device=dev)
+    vs = [torch.as_tensor(np.random.default_rng(i).standard_normal((1, N, 3)), device=dev) for i in range(3)]
+    kv = torch.empty_like(vs[0])
+    for i in range(5):
+        pf.tangent_apply(m4, mat4, vs[i % 3], mask=mask, out=kv)
+    torch.cuda.synchronize()
+    it = [0]
+
+    def kv_call():
+        pf.tangent_apply(m4, mat4, vs[it[0] % 3], mask=mask, out=kv)
+        it[0] += 1
+    # a second mesh copy would double memory; config 4 arrays (~355 MB) exceed L2 on their own
+    t_kv = time_events(torch, kv_call, 50)
+    B_kv = bytes_tangent(E, N, 3, 1, 8, nh=False, mat_per_elem=1, masked=True)
+    ex["config4_Kv"] = {"E": E, "us": t_kv * 1e3, "algorithmic_bytes": B_kv, "GBps": B_kv / (t_kv * 1e-3) / 1e9,
+                        "frac": B_kv / (t_kv * 1e-3) / 1e9 / peak, "elements_per_s": E / (t_kv * 1e-3),
+                        "prepare_s": prep}
+    x0 = torch.zeros_like(f)
+    pf.cg(m4, mat4, f, x0, mask=mask, tol=1e-8, max_iter=200)    # warm-up (graph build paths)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    xz, rz = pf.cg(m4, mat4, f, x0, mask=mask, tol=1e-8, max_iter=20000, history=False)
+    tz = time.perf_counter() - t0
+    us, _ = pf.cg(m4, mat4, f, xz, mask=mask, tol=1e-12, max_iter=20000, history=False)
+    xw = torch.as_tensor(warm_start(us.cpu().numpy(), p4.mask, seed=4004), device=dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    xw_out, rw = pf.cg(m4, mat4, f, xw, mask=mask, tol=1e-8, max_iter=20000, history=True)
+    tw = time.perf_counter() - t0
+    h = rw["history"]
+    ex["config4_cg"] = {"tol": 1e-8, "zero": {"iterations": rz["iterations"], "time_to_tol_s": tz,
+                                              "iterations_per_s": rz["iterations"] / tz,
+                                              "ms_per_iteration": tz / max(1, rz["iterations"]) * 1e3,
+                                              "true_rel_res": rz["true_rel_res_final"]},
+                        "warm": {"iterations": rw["iterations"], "time_to_tol_s": tw,
+                                 "rel_res0": rw["rel_res0"], "true_rel_res": rw["true_rel_res_final"],
+                                 "iterations_to_1e-3": int(np.argmax(h < 1e-3)) if np.any(h < 1e-3) else None,
+                                 "iterations_to_1e-6": int(np.argmax(h < 1e-6)) if np.any(h < 1e-6) else None},
+                        "speedup_iterations": rz["iterations"] / max(1, rw["iterations"]),
+                        "warm_start": "u* (GPU CG to 1e-12) + 0.01 rms(u*) N(0,1) on free DOFs"}
+    del m4, vs, kv
+    torch.cuda.empty_cache()
+    # ---------------- config 5: 64 ragged parts, NH fp32, fused E+R in one launch
+    p5 = config5()
+    E5, N5 = p5.n_elems, p5.n_nodes
+    pe, pn = p5.parts()
+    m5 = pf.Mesh(torch.as_tensor(p5.coords, device=dev), torch.as_tensor(p5.conn, device=dev), dtype=torch.float32,
+                 part_elem=pe, part_node=pn)
+    mat5 = pf.Material("neohookean", "lame", torch.as_tensor(p5.p0, dtype=torch.float32, device=dev),
+                       torch.as_tensor(p5.p1, dtype=torch.float32, device=dev))
+    u5 = torch.as_tensor(p5.u, dtype=torch.float32, device=dev)
+    outs = (torch.empty((1, 64), dtype=torch.float32, device=dev), torch.empty((1, E5), dtype=torch.float32, device=dev),
+            torch.empty_like(u5))
+    for _ in range(5):
+        pf.energy(m5, mat5, u5, elem_energy=True, residual=True, out=outs)
+    t5 = time_events(torch, lambda: pf.energy(m5, mat5, u5, elem_energy=True, residual=True, out=outs), 50)
+    B5 = bytes_energy_residual(E5, N5, 2, 1, 4, mat_per_elem=2, K=64)
+    ex["config5_energy_residual"] = {"E": E5, "us": t5 * 1e3, "algorithmic_bytes": B5,
+                                     "GBps": B5 / (t5 * 1e-3) / 1e9, "frac": B5 / (t5 * 1e-3) / 1e9 / peak,
+                                     "note": "timed back-to-back on one copy: partly L2-resident (upper bound)"}
+    return ex
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(prob, samples=1):
+    """The oracle as it stands (fp64, OpenMP on all host cores) on a bounded sample of the
+    workload: the first `samples` field(s) of config 3, full mesh, energy+residual+tangent."""
+    from oracle import oracle
+    om = oracle.prepare_problem(prob)
+    u = prob.u[:samples]
+    v = np.random.default_rng(3005).standard_normal(u.shape)
+    t0 = time.perf_counter()
+    om.energy(u)
+    om.residual(u)
+    om.tangent(v, u=u)
+    dt = time.perf_counter() - t0
+    return {"value": prob.n_elems * samples / dt, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
+            "sample": f"config 3, {samples} of {prob.n_samples} fields, full mesh ({prob.n_elems} tets): "
+                      f"energy + residual + tangent, fp64, {dt:.1f} s"}
+
+
+def submesh(prob, n_elems):
+    """First n_elems elements of a problem (a valid mesh: unused nodes carry no stiffness)."""
+    from pfem_gen.configs import Problem
+    return Problem(prob.name + f"[:{n_elems}]", prob.dim, prob.coords, prob.conn[:n_elems], prob.model,
+                   prob.param_kind, prob.p0 if len(prob.p0) == 1 else prob.p0[:n_elems],
+                   prob.p1 if len(prob.p1) == 1 else prob.p1[:n_elems], prob.u, prob.dtype)
+
+
+def run_reference(args, budget_s=150.0):
+    """The reference arm of this tier: the CPU oracle as it stands, timed on this box's host
+    cores on the same workload / metric; each step is a bounded sample (1 field, and a
+    leading sub-mesh sized so that the W + K steps fit in ~budget_s)."""
+    world, rank, _ = dist_info()
+    if rank != 0:
+        return
+    from pfem_gen import config3
+    from oracle import oracle
+    prob = config3()
+    probe = submesh(prob, 100_000)
+    om = oracle.prepare_problem(probe)
+    u = prob.u[:1]
+    v = np.random.default_rng(3005).standard_normal(u.shape)
+    t0 = time.perf_counter()
+    om.energy(u); om.residual(u); om.tangent(v, u=u)
+    per_elem = (time.perf_counter() - t0) / probe.n_elems
+    n_el = int(min(prob.n_elems, max(10_000, budget_s / max(1, args.steps + args.warmup) / per_elem)))
+    sub = submesh(prob, n_el)
+    om = oracle.prepare_problem(sub)
+
+    def one():
+        om.energy(u)
+        om.residual(u)
+        om.tangent(v, u=u)
+
+    for _ in range(args.warmup):
+        one()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one()
+    dt = (time.perf_counter() - t0) / args.steps
+    value = n_el / dt
+    sample = (f"config 3, 1 of 4 fields per step, leading {n_el} of {prob.n_elems} tets: "
+              "oracle energy + residual + tangent (fp64, OpenMP)")
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generators, pfem_gen)", "impl": "reference",
+           "config": {"workload": "config3", "n_elems": prob.n_elems, "n_nodes": prob.n_nodes, "sample": sample},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle", "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -36,6 +36,33 @@ constexpr int32_t OCC_NODE_MASK = 0x1fffffff;  // prepare rejects n_nodes >= 2^2
 constexpr int32_t OCC_NONOWNER = 0x40000000;   // another (later) block owns the node
 constexpr int32_t OCC_EARLIER = 0x20000000;    // owner, and earlier blocks hold partials
 
+// ------------------------------------------------------------------ packed block records
+// The plan keeps, per element block, one contiguous 16-byte-aligned record holding
+// everything phase 1 and phase 2 read from HBM about the block, so a single TMA bulk copy
+// (cp.async.bulk) stages it into shared memory:
+//   conn [EB][d+1] int32 | grad [d*d][EB] T | vol [EB] T | occ_node [OCAP] int32 |
+//   occ_ent [OCAP+1] uint16 (block-relative entry offsets) | loc_ent [(d+1) EB] uint16
+struct RecLayout {
+    int eb = 0, ocap = 0;
+    uint32_t conn = 0, g = 0, vol = 0, occ_node = 0, occ_ent = 0, loc_ent = 0, bytes = 0;
+};
+
+inline RecLayout rec_layout(int D, size_t tsize, int eb, int ocap) {
+    RecLayout L;
+    L.eb = eb;
+    L.ocap = ocap;
+    size_t o = 0;
+    auto take = [&](size_t b) { size_t at = o; o += (b + 15) / 16 * 16; return (uint32_t)at; };
+    L.conn = take(4 * (size_t)(D + 1) * eb);
+    L.g = take(tsize * D * D * (size_t)eb);
+    L.vol = take(tsize * (size_t)eb);
+    L.occ_node = take(4 * (size_t)ocap);
+    L.occ_ent = take(2 * (size_t)(ocap + 1));
+    L.loc_ent = take(2 * (size_t)(D + 1) * eb);
+    L.bytes = (uint32_t)o;
+    return L;
+}
+
 struct Plan {
     int32_t dim = 0, n_nodes = 0, n_elems = 0, n_parts = 0;
     int32_t n_blocks = 0, n_occ = 0, eb_max = 0;
@@ -56,12 +83,23 @@ struct Plan {
     uint16_t* loc_ent = nullptr;      // [(dim+1)*n_elems] local entry ids, grouped by occurrence
     int32_t* node_occ_ptr = nullptr;  // [n_nodes+1]
     int32_t* node_occ = nullptr;      // [n_occ] occurrence ids sorted by (node, block)
+    int32_t n_fix = 0;                // owned nodes with partials in earlier blocks
+    int32_t* blk_fix = nullptr;       // [n_blocks+1] offsets into fix_occ
+    int32_t* fix_occ = nullptr;       // [n_fix] occurrence ids (fix-up list of each block)
+    int32_t* fix_node = nullptr;      // [n_fix] node id of each fix entry
+    int32_t* fix_src_ptr = nullptr;   // [n_fix+1] offsets into fix_src
+    int32_t* fix_src = nullptr;       // all occurrences of the node, ascending block (own last)
+    void* pool_fix = nullptr;
+    void* pool_src = nullptr;
+    RecLayout rec;                    // packed block records (one bulk copy per block)
+    unsigned char* recs = nullptr;    // [n_blocks][rec.bytes]
+    void* pool_rec = nullptr;
     void* pool = nullptr;             // single allocation backing all of the above
 };
 
 // ------------------------------------------------------------------ workspace layout
-// [ Counters | blk_flag[n_blocks] | blk_sum[2S+1][n_blocks] (double) | chunk_done[n_chunks] |
-//   chunk_sum[2S+1][n_chunks] (double) | partial[S][n_occ][d] (T) | colour-mode W [S][E] (T) ]
+// [ Counters | blk_flag[n_blocks] | blk_sum[2S+2][n_blocks] (double) | chunk_done[n_chunks] |
+//   chunk_sum[2S+1][n_chunks] (double) | partial[n_occ][S][d] (T) | colour-mode W [S][E] (T) ]
 struct Counters {
     int32_t ticket;
     int32_t done;
@@ -69,7 +107,9 @@ struct Counters {
     int32_t n_inv;
     int32_t first_inv;     // stored as INT32_MAX - first (atomicMax; 0 = none) so zero-fill is valid
     int32_t n_nonfinite;
-    int32_t pad[10];
+    int32_t exit_count;
+    int32_t fix_ticket;
+    int32_t pad[8];
 };
 
 struct WsLayout {
@@ -83,7 +123,7 @@ inline WsLayout ws_layout(const Plan& p, int S, size_t tsize) {
     size_t o = 0;
     L.counters = o; o += align_up(sizeof(Counters), 256);
     L.flags = o;    o += align_up(sizeof(int32_t) * (size_t)(p.n_blocks + 1), 256);
-    L.blk_sum = o;  o += align_up(sizeof(double) * (2 * (size_t)S + 1) * (p.n_blocks + 1), 256);
+    L.blk_sum = o;  o += align_up(sizeof(double) * (2 * (size_t)S + 2) * (p.n_blocks + 1), 256);
     L.chunk_done = o; o += align_up(sizeof(int32_t) * (size_t)(p.n_chunks + 1), 256);
     L.chunk_sum = o;  o += align_up(sizeof(double) * (2 * (size_t)S + 1) * (p.n_chunks + 1), 256);
     L.partial = o;  o += align_up(tsize * (size_t)S * p.n_occ * p.dim, 256);

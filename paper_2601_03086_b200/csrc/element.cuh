@@ -8,12 +8,17 @@
 //   forces      f_a = V P grad N_a (App. B P:1086 / P:1096), f_0 = -sum_{a>=1} f_a
 //   tangent     dP = mu dH + (mu - lam ln J) F^-T dH^T F^-T + lam (F^-T : dH) F^-T
 //
-// Cancellation-free evaluation near F = I (exact algebra, so the fp64
-// values agree with the plain formulas to rounding):
-//   x = J - 1 = tr H + i2(H) + det H (3-D) or tr H + det H (2-D), ln J = log1p(x)
-//   psi_NH = lam/2 ln^2 J + mu (|H|^2/2 - i2 - det H + g(x)),  g(x) = x - log1p(x)
-//   adj(I+H) = (1 + t + i2) I - (1 + t) H + H^2   (3-D Cayley-Hamilton), (1+t) I - H (2-D)
-//   F - F^-T = [det H I + (1+x) H + (1+t) H^T - (H^T)^2] / J  (3-D), [det H I + (1+x) H + H^T] / J (2-D)
+// Evaluation near F = I (exact algebra, so fp64 agrees with the plain
+// formulas to rounding; fp32 avoids the catastrophic cancellation of the energy):
+//   x = J - 1 = tr H + i2(H) + det H (3-D) or tr H + det H (2-D)
+//   ln J = log1p(x) = 2 atanh(z), z = x / (2 + x);   g(x) = x - log1p(x) = x^2/(2+x) - 2 (z^3/3 + z^5/5 + ..)
+//   psi_NH = lam/2 ln^2 J + mu (|H|^2/2 - i2 - det H + g(x))
+//   P = mu F + (lam ln J - mu) cof(F) / J        (F^-T = cof(F) / J)
+// One-point quadrature: V_e is folded into (mu, lambda) at load time.
+//
+// The arithmetic is written once for a value type V: double, float, or F2 (two samples
+// that share the element's geometry in one sm_100a FFMA2 / FADD2 / FMUL2 register pair;
+// the geometry stays a scalar operand, which FFMA2 broadcasts for free).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -23,6 +28,100 @@ namespace pfem {
 
 enum { MODEL_LINEAR = 0, MODEL_NH = 1 };
 enum { KIND_LAME = 0, KIND_YP = 1, KIND_YP_PLANE_STRESS = 2 };
+
+// ------------------------------------------------------------------ F2: 2 x fp32 lanes
+struct F2 {
+    float2 v;
+    __device__ __forceinline__ F2() {}
+    __device__ __forceinline__ explicit F2(float s) : v(make_float2(s, s)) {}
+    __device__ __forceinline__ F2(float a, float b) : v(make_float2(a, b)) {}
+};
+__device__ __forceinline__ F2 operator+(F2 a, F2 b) { F2 r; r.v = __fadd2_rn(a.v, b.v); return r; }
+__device__ __forceinline__ F2 operator-(F2 a, F2 b) { F2 r; r.v = __fadd2_rn(a.v, make_float2(-b.v.x, -b.v.y)); return r; }
+__device__ __forceinline__ F2 operator-(F2 a) { return F2(-a.v.x, -a.v.y); }
+__device__ __forceinline__ F2 operator*(F2 a, F2 b) { F2 r; r.v = __fmul2_rn(a.v, b.v); return r; }
+__device__ __forceinline__ F2 operator+(F2 a, float b) { return a + F2(b); }
+__device__ __forceinline__ F2 operator+(float a, F2 b) { return F2(a) + b; }
+__device__ __forceinline__ F2 operator-(F2 a, float b) { return a - F2(b); }
+__device__ __forceinline__ F2 operator-(float a, F2 b) { return F2(a) - b; }
+__device__ __forceinline__ F2 operator*(F2 a, float b) { return a * F2(b); }
+__device__ __forceinline__ F2 operator*(float a, F2 b) { return F2(a) * b; }
+__device__ __forceinline__ F2& operator+=(F2& a, F2 b) { a = a + b; return a; }
+__device__ __forceinline__ F2 fma(F2 a, F2 b, F2 c) { F2 r; r.v = __ffma2_rn(a.v, b.v, c.v); return r; }
+__device__ __forceinline__ F2 fma(F2 a, float b, F2 c) { return fma(a, F2(b), c); }
+__device__ __forceinline__ F2 fma(float a, F2 b, F2 c) { return fma(F2(a), b, c); }
+using ::fma;   // keep the float / double overloads visible next to the F2 ones
+
+template <class V> struct VTraits;
+template <> struct VTraits<float> { using S = float; static constexpr int L = 1; };
+template <> struct VTraits<double> { using S = double; static constexpr int L = 1; };
+template <> struct VTraits<F2> { using S = float; static constexpr int L = 2; };
+
+__device__ __forceinline__ float lane(float x, int) { return x; }
+__device__ __forceinline__ double lane(double x, int) { return x; }
+__device__ __forceinline__ float lane(F2 x, int k) { return k ? x.v.y : x.v.x; }
+__device__ __forceinline__ void set_lane(float& x, int, float s) { x = s; }
+__device__ __forceinline__ void set_lane(double& x, int, double s) { x = s; }
+__device__ __forceinline__ void set_lane(F2& x, int k, float s) { if (k) x.v.y = s; else x.v.x = s; }
+
+// reciprocal: fp32 MUFU.RCP + one Newton step (~0.5 ulp); fp64 IEEE division
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ double vrcp(double x) { return 1.0 / x; }
+__device__ __forceinline__ float vrcp(float x) {
+    float r = rcp_approx(x);
+    return fmaf(r, fmaf(-x, r, 1.0f), r);
+}
+__device__ __forceinline__ F2 vrcp(F2 x) {
+    F2 r(rcp_approx(x.v.x), rcp_approx(x.v.y));
+    return fma(r, fma(-x, r, F2(1.0f)), r);
+}
+
+// ln J = log1p(x) and g(x) = x - log1p(x) >= 0 together, cancellation-free.
+// |x| < 1/2: z = x/(2+x) (|z| < 1/3), log1p = 2 z (1 + z^2 s(z^2)), g = x^2/(2+x) - 2 z^3 s(z^2),
+// s = 1/3 + z^2/5 + ...; else the library log1p.
+__device__ __forceinline__ void log1p_g(double x, double& l, double& g) {
+    if (fabs(x) < 0.5) {
+        const double r = 1.0 / (2.0 + x), z = x * r, z2 = z * z;
+        double s = 1.0 / 41;
+#pragma unroll
+        for (int k = 39; k >= 3; k -= 2) s = fma(s, z2, 1.0 / k);
+        const double zs = z * z2 * s;
+        l = 2.0 * (z + zs);
+        g = fma(x * x, r, -2.0 * zs);
+    } else {
+        l = log1p(x);
+        g = x - l;
+    }
+}
+template <class V>
+__device__ __forceinline__ void log1p_g(V x, V& l, V& g) {   // float / F2
+    bool small = true;
+#pragma unroll
+    for (int k = 0; k < VTraits<V>::L; ++k) small = small && fabsf(lane(x, k)) < 0.5f;
+    if (small) {
+        const V r = vrcp(x + 2.0f), z = x * r, z2 = z * z;
+        V s = fma(z2, 1.0f / 15, V(1.0f / 13));
+        s = fma(s, z2, V(1.0f / 11));
+        s = fma(s, z2, V(1.0f / 9));
+        s = fma(s, z2, V(1.0f / 7));
+        s = fma(s, z2, V(1.0f / 5));
+        s = fma(s, z2, V(1.0f / 3));
+        const V zs = z * z2 * s;
+        l = 2.0f * (z + zs);
+        g = fma(x * x, r, -2.0f * zs);
+    } else {
+#pragma unroll
+        for (int k = 0; k < VTraits<V>::L; ++k) {
+            const float xl = lane(x, k), ll = log1pf(xl);
+            set_lane(l, k, ll);
+            set_lane(g, k, xl - ll);
+        }
+    }
+}
 
 template <class T>
 struct MatArgs {
@@ -37,11 +136,8 @@ struct Geo {
     int v[D + 1];
     T g[D][D];      // g[a][j] = dN_{a+1}/dX_j
     T V;
-    T mu, lam;
+    T mu, lam;      // V_e * mu, V_e * lambda after load_geo
 };
-
-template <class T>
-__device__ __forceinline__ T tone() { return T(1); }
 
 // (E, nu) -> (mu, lambda)
 template <class T>
@@ -60,9 +156,9 @@ template <int D, class T>
 __device__ __forceinline__ void load_geo(int e, int E, const int32_t* __restrict__ conn,
                                          const T* __restrict__ grad, const T* __restrict__ vol,
                                          const MatArgs<T>& m, Geo<D, T>& G) {
-    if (D == 3) {
+    if constexpr (D == 3) {
         int4 c = __ldg(reinterpret_cast<const int4*>(conn) + e);
-        G.v[0] = c.x; G.v[1] = c.y; G.v[2] = c.z; G.v[D == 3 ? 3 : 0] = c.w;
+        G.v[0] = c.x; G.v[1] = c.y; G.v[2] = c.z; G.v[3] = c.w;
     } else {
 #pragma unroll
         for (int a = 0; a <= D; ++a) G.v[a] = __ldg(conn + (int64_t)e * (D + 1) + a);
@@ -75,39 +171,47 @@ __device__ __forceinline__ void load_geo(int e, int E, const int32_t* __restrict
     T p0 = __ldg(m.p0 + (int64_t)e * m.s0);
     T p1 = __ldg(m.p1 + (int64_t)e * m.s1);
     lame_of<T>(m.kind, p0, p1, G.mu, G.lam);
+    // one-point quadrature: fold V_e into the moduli, so psi -> W_e = V_e psi and
+    // P -> V_e P (forces f_a = (V_e P) grad N_a need no further scaling)
+    G.mu *= G.V;
+    G.lam *= G.V;
 }
 
-// gather the d+1 nodal vectors of one sample; masked DOFs read as 0
-template <int D, class T, bool MASKED>
-__device__ __forceinline__ void gather(const T* __restrict__ f, const uint8_t* __restrict__ mask,
-                                       const Geo<D, T>& G, T x[D + 1][D]) {
+// gather the d+1 nodal vectors of L consecutive samples (stride sstride); masked DOFs -> 0
+template <int D, class T, class V, bool MASKED>
+__device__ __forceinline__ void gather(const T* __restrict__ f, int64_t sstride, const uint8_t* __restrict__ mask,
+                                       const Geo<D, T>& G, V x[D + 1][D]) {
 #pragma unroll
     for (int a = 0; a <= D; ++a) {
-        const int64_t base = (int64_t)G.v[a] * D;
-        if (D == 2 && sizeof(T) == 8) {
-            double2 q = __ldg(reinterpret_cast<const double2*>(f + base));
-            x[a][0] = (T)q.x;
-            x[a][D - 1] = (T)q.y;
-        } else if (D == 2 && sizeof(T) == 4) {
-            float2 q = __ldg(reinterpret_cast<const float2*>(f + base));
-            x[a][0] = (T)q.x;
-            x[a][D - 1] = (T)q.y;
-        } else {
+        const int base = G.v[a] * D;
 #pragma unroll
-            for (int i = 0; i < D; ++i) x[a][i] = __ldg(f + base + i);
+        for (int k = 0; k < VTraits<V>::L; ++k) {
+            const T* fk = f + k * sstride + base;
+            if constexpr (D == 2 && sizeof(T) == 8) {
+                double2 q = __ldg(reinterpret_cast<const double2*>(fk));
+                set_lane(x[a][0], k, q.x);
+                set_lane(x[a][D - 1], k, q.y);
+            } else if constexpr (D == 2 && sizeof(T) == 4) {
+                float2 q = __ldg(reinterpret_cast<const float2*>(fk));
+                set_lane(x[a][0], k, q.x);
+                set_lane(x[a][D - 1], k, q.y);
+            } else {
+#pragma unroll
+                for (int i = 0; i < D; ++i) set_lane(x[a][i], k, __ldg(fk + i));
+            }
         }
         if (MASKED) {
 #pragma unroll
             for (int i = 0; i < D; ++i)
-                if (__ldg(mask + base + i)) x[a][i] = T(0);
+                if (__ldg(mask + base + i)) x[a][i] = V(T(0));
         }
     }
 }
 
 // H = sum_{a=1..d} (x_a - x_0) (x) g_{a-1}
-template <int D, class T>
-__device__ __forceinline__ void grad_of(const Geo<D, T>& G, const T x[D + 1][D], T H[D][D]) {
-    T dx[D][D];
+template <int D, class T, class V>
+__device__ __forceinline__ void grad_of(const Geo<D, T>& G, const V x[D + 1][D], V H[D][D]) {
+    V dx[D][D];
 #pragma unroll
     for (int a = 0; a < D; ++a)
 #pragma unroll
@@ -116,205 +220,201 @@ __device__ __forceinline__ void grad_of(const Geo<D, T>& G, const T x[D + 1][D],
     for (int i = 0; i < D; ++i)
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-            T s = dx[0][i] * G.g[0][j];
+            V s = dx[0][i] * G.g[0][j];
 #pragma unroll
             for (int a = 1; a < D; ++a) s = fma(dx[a][i], G.g[a][j], s);
             H[i][j] = s;
         }
 }
 
-// g(x) = x - log1p(x) without cancellation: with z = x/(2+x), log1p(x) = 2 atanh z, so
-// g = x^2/(2+x) - 2 (z^3/3 + z^5/5 + ...)   (|x| < 1/2), direct form otherwise.
-template <class T>
-__device__ __forceinline__ T g_of(T x) {
-    if (fabs(x) < T(0.5)) {
-        T r = T(1) / (T(2) + x);
-        T z = x * r;
-        T z2 = z * z;
-        T s;
-        if (sizeof(T) == 4) {
-            s = T(1.0 / 11);
-            s = fma(s, z2, T(1.0 / 9));
-            s = fma(s, z2, T(1.0 / 7));
-            s = fma(s, z2, T(1.0 / 5));
-            s = fma(s, z2, T(1.0 / 3));
-        } else {
-            s = T(1.0 / 27);
+template <int D, class V>
+__device__ __forceinline__ void cofactor(const V F[D][D], V cof[D][D]) {
+    if constexpr (D == 2) {
+        cof[0][0] = F[1][1];
+        cof[0][1] = -F[1][0];
+        cof[1][0] = -F[0][1];
+        cof[1][1] = F[0][0];
+    } else {
 #pragma unroll
-            for (int k = 25; k >= 3; k -= 2) s = fma(s, z2, T(1.0) / T(k));
-        }
-        return x * x * r - T(2) * z * z2 * s;
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                const int i1 = (i + 1) % D, i2 = (i + 2) % D, j1 = (j + 1) % D, j2 = (j + 2) % D;
+                cof[i][j] = fma(F[i1][j1], F[i2][j2], -(F[i1][j2] * F[i2][j1]));
+            }
     }
-    return x - log1p(x);
 }
 
-// Neo-Hookean state from H: x = J-1, lnJ, 1/J, F^-T (A), and optionally psi
-template <int D, class T>
+// count of lanes with !(x > -1) (J <= 0 or NaN)
+template <class V>
+__device__ __forceinline__ int n_bad(V x) {
+    int n = 0;
+#pragma unroll
+    for (int k = 0; k < VTraits<V>::L; ++k) n += !(lane(x, k) > -1.0f) ? 1 : 0;
+    return n;
+}
+
+// Neo-Hookean linearisation state from H (tangent): ln J, A = F^-T = cof(F) / J
+template <int D, class V>
 struct NhState {
-    T x, lnJ, invJ, t, i2, detH;
-    T A[D][D];   // F^-T = cof(F) / J
+    V x, lnJ;
+    V A[D][D];
 };
 
-template <int D, class T>
-__device__ __forceinline__ void nh_state(const T H[D][D], NhState<D, T>& S, T H2[D][D]) {
-    if (D == 2) {
-        S.t = H[0][0] + H[1][1];
-        S.detH = H[0][0] * H[1][1] - H[0][1] * H[1][0];
-        S.i2 = T(0);
-        S.x = S.t + S.detH;
-    } else {
-        S.t = H[0][0] + H[1][1] + H[D - 1][D - 1];
-        // H2 = H H
+template <int D, class V>
+__device__ __forceinline__ void nh_state(const V H[D][D], NhState<D, V>& S) {
+    V F[D][D], cof[D][D];
 #pragma unroll
-        for (int i = 0; i < D; ++i)
+    for (int i = 0; i < D; ++i)
 #pragma unroll
-            for (int j = 0; j < D; ++j) {
-                T s = H[i][0] * H[0][j];
+        for (int j = 0; j < D; ++j) F[i][j] = (i == j) ? H[i][j] + 1.0f : H[i][j];
+    cofactor<D, V>(F, cof);
+    V J = F[0][0] * cof[0][0];
 #pragma unroll
-                for (int k = 1; k < D; ++k) s = fma(H[i][k], H[k][j], s);
-                H2[i][j] = s;
-            }
-        T trH2 = H2[0][0] + H2[1][1] + H2[D - 1][D - 1];
-        S.i2 = T(0.5) * (S.t * S.t - trH2);
-        // det H by cofactor expansion on row 0
-        S.detH = H[0][0] * (H[1][1] * H[D - 1][D - 1] - H[1][D - 1] * H[D - 1][1]) -
-                 H[0][1] * (H[1][0] * H[D - 1][D - 1] - H[1][D - 1] * H[D - 1][0]) +
-                 H[0][D - 1] * (H[1][0] * H[D - 1][1] - H[1][1] * H[D - 1][0]);
-        S.x = S.t + S.i2 + S.detH;
-    }
-    S.lnJ = log1p(S.x);
-    S.invJ = T(1) / (T(1) + S.x);
-    // cof(F) = adj(F)^T
-    if (D == 2) {
-        // adj = (1+t) I - H  ->  cof = (1+t) I - H^T
+    for (int j = 1; j < D; ++j) J = fma(F[0][j], cof[0][j], J);
+    S.x = J - 1.0f;
+    V g;
+    log1p_g(S.x, S.lnJ, g);
+    const V invJ = vrcp(J);
 #pragma unroll
-        for (int i = 0; i < D; ++i)
+    for (int i = 0; i < D; ++i)
 #pragma unroll
-            for (int j = 0; j < D; ++j)
-                S.A[i][j] = ((i == j ? T(1) + S.t : T(0)) - H[j][i]) * S.invJ;
-    } else {
-        // adj = (1+t+i2) I - (1+t) H + H^2  ->  cof = (1+t+i2) I - (1+t) H^T + (H^2)^T
-        const T c0 = T(1) + S.t + S.i2, c1 = T(1) + S.t;
-#pragma unroll
-        for (int i = 0; i < D; ++i)
-#pragma unroll
-            for (int j = 0; j < D; ++j)
-                S.A[i][j] = ((i == j ? c0 : T(0)) - c1 * H[j][i] + H2[j][i]) * S.invJ;
-    }
+        for (int j = 0; j < D; ++j) S.A[i][j] = cof[i][j] * invJ;
 }
 
-// first Piola stress and (optionally) the energy density
-template <int D, int MODEL, class T, bool WANT_PSI>
-__device__ __forceinline__ void stress(const Geo<D, T>& G, const T H[D][D], T P[D][D], T& psi,
-                                       bool& bad) {
-    if (MODEL == MODEL_LINEAR) {
-        T tr = H[0][0];
+// first Piola stress (times V_e) and, if WANT_PSI, the element energy W_e = V_e psi
+template <int D, int MODEL, class T, class V, bool WANT_PSI>
+__device__ __forceinline__ void stress(const Geo<D, T>& G, const V H[D][D], V P[D][D], V& psi, int& bad) {
+    if constexpr (MODEL == MODEL_LINEAR) {
+        V tr = H[0][0];
 #pragma unroll
-        for (int i = 1; i < D; ++i) tr += H[i][i];
-        T ee = T(0);
+        for (int i = 1; i < D; ++i) tr = tr + H[i][i];
+        const V lt = G.lam * tr;
+        V ee = V(T(0));
 #pragma unroll
         for (int i = 0; i < D; ++i)
 #pragma unroll
             for (int j = 0; j < D; ++j) {
-                T eps = T(0.5) * (H[i][j] + H[j][i]);
-                P[i][j] = T(2) * G.mu * eps + (i == j ? G.lam * tr : T(0));
-                if (WANT_PSI) ee = fma(eps, eps, ee);
+                if (i == j) {
+                    P[i][i] = fma(H[i][i], T(2) * G.mu, lt);
+                    if (WANT_PSI) ee = fma(H[i][i], H[i][i], ee);
+                } else if (j > i) {
+                    const V s = H[i][j] + H[j][i];          // 2 eps_ij
+                    P[i][j] = s * G.mu;
+                    P[j][i] = P[i][j];
+                    if (WANT_PSI) ee = fma(s, s * T(0.5), ee);   // eps_ij^2 + eps_ji^2
+                }
             }
-        if (WANT_PSI) psi = G.mu * ee + T(0.5) * G.lam * tr * tr;
-        bad = false;
+        if (WANT_PSI) psi = fma(ee, G.mu, (G.lam * T(0.5)) * (tr * tr));
+        bad = 0;
     } else {
-        NhState<D, T> S;
-        T H2[D][D];
-        nh_state<D, T>(H, S, H2);
-        bad = !(S.x > T(-1));
-        // F - F^-T
-        T Dm[D][D];
-        if (D == 2) {
+        V t = H[0][0];
 #pragma unroll
-            for (int i = 0; i < D; ++i)
-#pragma unroll
-                for (int j = 0; j < D; ++j)
-                    Dm[i][j] = ((i == j ? S.detH : T(0)) + (T(1) + S.x) * H[i][j] + H[j][i]) * S.invJ;
+        for (int i = 1; i < D; ++i) t = t + H[i][i];
+        V detH, i2 = V(T(0));
+        if constexpr (D == 2) {
+            detH = fma(H[0][0], H[1][1], -(H[0][1] * H[1][0]));
         } else {
-            const T c1 = T(1) + S.t;
+            V trH2 = H[0][0] * H[0][0];
 #pragma unroll
             for (int i = 0; i < D; ++i)
 #pragma unroll
                 for (int j = 0; j < D; ++j)
-                    Dm[i][j] = ((i == j ? S.detH : T(0)) + (T(1) + S.x) * H[i][j] + c1 * H[j][i] - H2[j][i]) *
-                               S.invJ;
+                    if (i || j) trH2 = fma(H[i][j], H[j][i], trH2);
+            i2 = fma(t, t, -trH2) * T(0.5);
+            const V m0 = fma(H[1][1], H[2][2], -(H[1][2] * H[2][1]));
+            const V m1 = fma(H[1][0], H[2][2], -(H[1][2] * H[2][0]));
+            const V m2 = fma(H[1][0], H[2][1], -(H[1][1] * H[2][0]));
+            detH = fma(H[0][0], m0, fma(-H[0][1], m1, H[0][2] * m2));
         }
-        const T ll = G.lam * S.lnJ;
+        const V x = t + i2 + detH;
+        bad = n_bad(x);
+        V lnJ, g;
+        log1p_g(x, lnJ, g);
+        const V invJ = vrcp(x + T(1));
+        V F[D][D], cof[D][D];
 #pragma unroll
         for (int i = 0; i < D; ++i)
 #pragma unroll
-            for (int j = 0; j < D; ++j) P[i][j] = G.mu * Dm[i][j] + ll * S.A[i][j];
+            for (int j = 0; j < D; ++j) F[i][j] = (i == j) ? H[i][j] + T(1) : H[i][j];
+        cofactor<D, V>(F, cof);
+        const V c = fma(lnJ, G.lam, V(-G.mu)) * invJ;
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = 0; j < D; ++j) P[i][j] = fma(c, cof[i][j], F[i][j] * G.mu);
         if (WANT_PSI) {
-            T hh = T(0);
+            V hh = H[0][0] * H[0][0];
 #pragma unroll
             for (int i = 0; i < D; ++i)
 #pragma unroll
-                for (int j = 0; j < D; ++j) hh = fma(H[i][j], H[i][j], hh);
-            psi = T(0.5) * G.lam * S.lnJ * S.lnJ + G.mu * (T(0.5) * hh - S.i2 - S.detH + g_of<T>(S.x));
+                for (int j = 0; j < D; ++j)
+                    if (i || j) hh = fma(H[i][j], H[i][j], hh);
+            const V inner = fma(hh, T(0.5), g - i2 - detH);
+            psi = fma((G.lam * T(0.5)) * lnJ, lnJ, inner * G.mu);
         }
     }
 }
 
-// tangent stress increment dP(dH) at state H (NH) or for the linear law
-template <int D, int MODEL, class T>
-__device__ __forceinline__ void dstress(const Geo<D, T>& G, const NhState<D, T>& S, const T dH[D][D],
-                                        T dP[D][D]) {
-    if (MODEL == MODEL_LINEAR) {
-        T tr = dH[0][0];
+// tangent stress increment dP(dH) at state S (NH) or for the linear law (times V_e)
+template <int D, int MODEL, class T, class V>
+__device__ __forceinline__ void dstress(const Geo<D, T>& G, const NhState<D, V>& S, const V dH[D][D], V dP[D][D]) {
+    if constexpr (MODEL == MODEL_LINEAR) {
+        V tr = dH[0][0];
 #pragma unroll
-        for (int i = 1; i < D; ++i) tr += dH[i][i];
+        for (int i = 1; i < D; ++i) tr = tr + dH[i][i];
+        const V lt = G.lam * tr;
 #pragma unroll
         for (int i = 0; i < D; ++i)
 #pragma unroll
-            for (int j = 0; j < D; ++j)
-                dP[i][j] = G.mu * (dH[i][j] + dH[j][i]) + (i == j ? G.lam * tr : T(0));
+            for (int j = 0; j < D; ++j) {
+                if (i == j) dP[i][i] = fma(dH[i][i], T(2) * G.mu, lt);
+                else if (j > i) {
+                    dP[i][j] = (dH[i][j] + dH[j][i]) * G.mu;
+                    dP[j][i] = dP[i][j];
+                }
+            }
     } else {
         // M1 = A dH^T ; M2 = M1 A ; tr(F^-1 dH) = A : dH
-        T M1[D][D];
-        T tr = T(0);
+        V M1[D][D];
+        V tr = S.A[0][0] * dH[0][0];
 #pragma unroll
         for (int i = 0; i < D; ++i)
 #pragma unroll
             for (int j = 0; j < D; ++j) {
-                T s = S.A[i][0] * dH[j][0];
+                V s = S.A[i][0] * dH[j][0];
 #pragma unroll
                 for (int k = 1; k < D; ++k) s = fma(S.A[i][k], dH[j][k], s);
                 M1[i][j] = s;
-                tr = fma(S.A[i][j], dH[i][j], tr);
+                if (i || j) tr = fma(S.A[i][j], dH[i][j], tr);
             }
-        const T c = G.mu - G.lam * S.lnJ;
-        const T lt = G.lam * tr;
+        const V cc = fma(S.lnJ, -G.lam, V(G.mu));
+        const V lt = tr * G.lam;
 #pragma unroll
         for (int i = 0; i < D; ++i)
 #pragma unroll
             for (int j = 0; j < D; ++j) {
-                T s = M1[i][0] * S.A[0][j];
+                V s = M1[i][0] * S.A[0][j];
 #pragma unroll
                 for (int k = 1; k < D; ++k) s = fma(M1[i][k], S.A[k][j], s);
-                dP[i][j] = G.mu * dH[i][j] + c * s + lt * S.A[i][j];
+                dP[i][j] = fma(cc, s, fma(lt, S.A[i][j], dH[i][j] * G.mu));
             }
     }
 }
 
-// nodal forces f[a][i], a = 0..d, from P (already including nothing of V)
-template <int D, class T>
-__device__ __forceinline__ void forces(const Geo<D, T>& G, const T P[D][D], T f[D + 1][D]) {
+// nodal forces f[a][i] = (V P) grad N_a, a = 0..d (V already folded into P via the moduli)
+template <int D, class T, class V>
+__device__ __forceinline__ void forces(const Geo<D, T>& G, const V P[D][D], V f[D + 1][D]) {
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-        T s0 = T(0);
+        V s0;
 #pragma unroll
         for (int a = 0; a < D; ++a) {
-            T s = P[i][0] * G.g[a][0];
+            V s = P[i][0] * G.g[a][0];
 #pragma unroll
             for (int j = 1; j < D; ++j) s = fma(P[i][j], G.g[a][j], s);
-            s *= G.V;
             f[a + 1][i] = s;
-            s0 -= s;
+            s0 = (a == 0) ? -s : s0 - s;
         }
         f[0][i] = s0;
     }

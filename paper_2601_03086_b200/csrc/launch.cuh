@@ -2,6 +2,9 @@
 // sizing, grid), instantiated per (dim, dtype) in asm_{2,3}{f,d}.cu.
 #pragma once
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "assemble.cuh"
 
 namespace pfem {
@@ -67,6 +70,13 @@ AsmParams<T> make_params(const Call& c) {
     p.loc_ent = P.loc_ent;
     p.node_occ_ptr = P.node_occ_ptr;
     p.node_occ = P.node_occ;
+    p.blk_fix = P.blk_fix;
+    p.fix_occ = P.fix_occ;
+    p.fix_node = P.fix_node;
+    p.fix_src_ptr = P.fix_src_ptr;
+    p.fix_src = P.fix_src;
+    p.rec = P.rec;
+    p.recs = P.recs;
     const WsLayout L = ws_layout(P, c.S, sizeof(T));
     char* w = (char*)c.ws;
     p.ctr = (Counters*)(w + L.counters);
@@ -76,36 +86,50 @@ AsmParams<T> make_params(const Call& c) {
     p.chunk_sum = (double*)(w + L.chunk_sum);
     p.partial = (T*)(w + L.partial);
     p.cg = c.cg;
+    p.dbg = 0;
+    p.lag = 0;
     return p;
 }
 
 template <int D, int MODEL, class T, int OP, int ST, bool MASKED>
-pfem_status launch_csr(const AsmParams<T>& p, cudaStream_t s) {
+pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
     constexpr bool HAS_FORCE = OP != OP_ENERGY;
-    const size_t smem = HAS_FORCE ? (size_t)ST * D * (D + 1) * p.eb_max * sizeof(T) : 0;
-    static size_t configured = 0;   // per instantiation
-    auto kern = k_assemble<D, MODEL, T, OP, ST, MASKED>;
-    if (smem > 40 * 1024 && smem > configured) {   // dynamic + static smem beyond the 48 KB default
-        PFEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = smem;
+    constexpr int EB = EbOf<D>::value;
+    constexpr int NT = ASM_NT;
+    constexpr int NFW = FIX_WARPS;
+    const size_t smem = 2 * (size_t)p.rec.bytes + 4 * EB * sizeof(T) +
+                        (HAS_FORCE ? (size_t)ST * D * (D + 1) * EB * sizeof(T) : 0);
+    auto kern = k_assemble<D, MODEL, T, OP, ST, MASKED, EB, NT, NFW>;
+    static int resident = 0;   // per instantiation: co-resident CTAs on the device (persistent grid)
+    static size_t resident_smem = 0;
+    if (resident == 0 || smem > resident_smem) {
+        resident_smem = smem;
+        if (smem > 40 * 1024)   // dynamic + static smem beyond the 48 KB default
+            PFEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int dev = 0, nsm = 0, per_sm = 0;
+        PFEM_CUDA_TRY(cudaGetDevice(&dev));
+        PFEM_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        PFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT + 32 * NFW, smem));
+        resident = std::max(1, per_sm) * nsm;
     }
-    kern<<<p.n_blocks, ASM_NT, smem, s>>>(p);
+    if (p.eb_max > EB) {
+        set_error("plan block larger than the kernel's block capacity");
+        return PFEM_ERR_CAPACITY;
+    }
+    p.lag = 0;
+    static const int dbg = getenv("PFEM_DEBUG") ? atoi(getenv("PFEM_DEBUG")) : 0;
+    p.dbg = dbg;
+    const int grid = std::min(resident, p.n_blocks);
+    kern<<<grid, NT + 32 * NFW, smem, s>>>(p);
     PFEM_LAUNCH_CHECK("k_assemble");
     return PFEM_OK;
 }
 
 template <int D, int MODEL, class T, int OP, bool MASKED>
 pfem_status dispatch_st(const AsmParams<T>& p, cudaStream_t s) {
-    constexpr bool HAS_FORCE = OP != OP_ENERGY;
-    int dev = 0, maxs = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&maxs, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    const size_t per = HAS_FORCE ? (size_t)D * (D + 1) * p.eb_max * sizeof(T) : 0;
     constexpr int STBIG = sizeof(T) == 4 ? 4 : 2;
-    if (p.S > 1 && per * STBIG + 1024 <= (size_t)maxs) return launch_csr<D, MODEL, T, OP, STBIG, MASKED>(p, s);
-    if (per + 1024 <= (size_t)maxs) return launch_csr<D, MODEL, T, OP, 1, MASKED>(p, s);
-    set_error("block_elems too large for shared memory");
-    return PFEM_ERR_CAPACITY;
+    if (p.S > 1) return launch_csr<D, MODEL, T, OP, STBIG, MASKED>(p, s);
+    return launch_csr<D, MODEL, T, OP, 1, MASKED>(p, s);
 }
 
 template <int D, int MODEL, class T, int OP, bool MASKED>

@@ -223,16 +223,19 @@ constexpr int CHUNK_BLOCKS = 32;   // == CHUNK of assemble.cuh
 // Per block: bitonic-sort the (node << 16 | local entry) keys of its elements in shared
 // memory; runs of equal node = occurrences, in ascending node order; inside a run the
 // local entries ascend = CSR order restricted to the block.
-// mode 0: count occurrences -> occ_cnt[b], min_dep[b]
-// mode 1: fill occ_node, occ_ent_ptr, loc_ent, node_occ
+// mode 0: count occurrences -> occ_cnt[b], fix-ups -> fix_cnt[b], min_dep[b]
+// mode 1: fill occ_node, occ_ent_ptr, loc_ent, node_occ, fix_occ (the block's owned nodes
+//         with partials in earlier blocks, ascending node order)
 __global__ void __launch_bounds__(PLAN_THREADS)
 k_block_build(int mode, int nv, int nb, const int32_t* __restrict__ blk_elem,
               const int32_t* __restrict__ conn, const int32_t* __restrict__ csr_ptr,
-              const int32_t* __restrict__ csr_ent, int32_t* occ_cnt, int32_t* min_dep,
+              const int32_t* __restrict__ csr_ent, int32_t* occ_cnt, int32_t* fix_cnt, int32_t* min_dep,
               const int32_t* __restrict__ blk_occ, int32_t* occ_node, int32_t* occ_ent_ptr,
-              uint16_t* loc_ent, const int32_t* __restrict__ node_occ_ptr, int32_t* node_occ) {
+              uint16_t* loc_ent, const int32_t* __restrict__ node_occ_ptr, int32_t* node_occ,
+              const int32_t* __restrict__ blk_fix, int32_t* fix_occ) {
     __shared__ unsigned long long key[PLAN_MAX_KEYS];
     __shared__ uint16_t runid[PLAN_MAX_KEYS];
+    __shared__ uint8_t sfix[PLAN_MAX_KEYS];
     __shared__ int32_t s_scan[PLAN_THREADS];
     __shared__ int32_t s_mindep;
     const int b = blockIdx.x;
@@ -297,6 +300,7 @@ k_block_build(int mode, int nv, int nb, const int32_t* __restrict__ blk_elem,
         int first = csr_ent[kb] / nv, last = csr_ent[ke - 1] / nv;
         bool earlier = first < e0;
         bool nonowner = last >= e1;
+        sfix[runid[i]] = (earlier && !nonowner) ? 1 : 0;
         if (mode == 0) {
             if (earlier && !nonowner) atomicMin(&s_mindep, block_of(first, blk_elem, nb));
         } else {
@@ -315,10 +319,73 @@ k_block_build(int mode, int nv, int nb, const int32_t* __restrict__ blk_elem,
         }
     }
     __syncthreads();
-    if (mode == 0 && threadIdx.x == 0) {
-        occ_cnt[b] = n_occ_b;
-        min_dep[b] = s_mindep;
+    if (threadIdx.x == 0) {
+        int nf = 0;
+        for (int r2 = 0; r2 < n_occ_b; ++r2) {
+            if (!sfix[r2]) continue;
+            if (mode == 1) fix_occ[blk_fix[b] + nf] = blk_occ[b] + r2;
+            ++nf;
+        }
+        if (mode == 0) {
+            occ_cnt[b] = n_occ_b;
+            fix_cnt[b] = nf;
+            min_dep[b] = s_mindep;
+        }
     }
+}
+
+// fix-up source lists: for each fix entry (owned node with earlier partials) all occurrences
+// of its node in ascending block order (the last one is the owner's own segment)
+__global__ void k_fix_count(int n_fix, const int32_t* __restrict__ fix_occ, const int32_t* __restrict__ occ_node,
+                            const int32_t* __restrict__ node_occ_ptr, int32_t* cnt, int32_t* fix_node) {
+    int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= n_fix) return;
+    const int node = occ_node[fix_occ[f]] & OCC_NODE_MASK;
+    fix_node[f] = node;
+    cnt[f] = node_occ_ptr[node + 1] - node_occ_ptr[node];
+}
+
+__global__ void k_fix_fill(int n_fix, const int32_t* __restrict__ fix_node, const int32_t* __restrict__ node_occ_ptr,
+                           const int32_t* __restrict__ node_occ, const int32_t* __restrict__ fix_src_ptr,
+                           int32_t* fix_src) {
+    int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= n_fix) return;
+    const int node = fix_node[f];
+    const int k0 = node_occ_ptr[node], k1 = node_occ_ptr[node + 1];
+    for (int k = k0; k < k1; ++k) fix_src[fix_src_ptr[f] + (k - k0)] = node_occ[k];
+}
+
+// packed block records (see RecLayout): grid = blocks
+template <int D, class T>
+__global__ void k_pack_records(int E, const int32_t* __restrict__ blk_elem, const int32_t* __restrict__ blk_occ,
+                               const int32_t* __restrict__ conn, const T* __restrict__ grad,
+                               const T* __restrict__ vol, const int32_t* __restrict__ occ_node,
+                               const int32_t* __restrict__ occ_ent_ptr, const uint16_t* __restrict__ loc_ent,
+                               unsigned char* recs, RecLayout L) {
+    constexpr int NV = D + 1;
+    const int b = blockIdx.x;
+    const int e0 = blk_elem[b], ne = blk_elem[b + 1] - e0;
+    const int o0 = blk_occ[b], no = blk_occ[b + 1] - o0;
+    unsigned char* r = recs + (size_t)b * L.bytes;
+    int32_t* rc = reinterpret_cast<int32_t*>(r + L.conn);
+    T* rg = reinterpret_cast<T*>(r + L.g);
+    T* rv = reinterpret_cast<T*>(r + L.vol);
+    int32_t* ron = reinterpret_cast<int32_t*>(r + L.occ_node);
+    uint16_t* roe = reinterpret_cast<uint16_t*>(r + L.occ_ent);
+    uint16_t* rle = reinterpret_cast<uint16_t*>(r + L.loc_ent);
+    for (int el = threadIdx.x; el < L.eb; el += blockDim.x) {
+        const bool in = el < ne;
+#pragma unroll
+        for (int a = 0; a < NV; ++a) rc[el * NV + a] = in ? conn[(int64_t)(e0 + el) * NV + a] : 0;
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) rg[k * L.eb + el] = in ? grad[(int64_t)k * E + e0 + el] : T(0);
+        rv[el] = in ? vol[e0 + el] : T(0);
+    }
+    for (int i = threadIdx.x; i < L.ocap; i += blockDim.x) ron[i] = i < no ? occ_node[o0 + i] : 0;
+    for (int i = threadIdx.x; i <= L.ocap; i += blockDim.x)
+        roe[i] = (uint16_t)(i <= no ? occ_ent_ptr[o0 + i] - NV * e0 : NV * ne);
+    for (int k = threadIdx.x; k < NV * L.eb; k += blockDim.x)
+        rle[k] = k < NV * ne ? loc_ent[(int64_t)NV * e0 + k] : (uint16_t)0;
 }
 
 // ------------------------------------------------------------------ host driver
@@ -467,7 +534,9 @@ pfem_status prepare_impl(pfem_mesh* m, cudaStream_t s) {
                 return PFEM_ERR_ARG;
             }
     }
-    int eb = m->block_elems > 0 ? m->block_elems : (D == 3 ? 512 : 1024);
+    // block capacity = the CSR kernel's compile-time EB (assemble.cuh EbOf): 256 T4 / 512 T3
+    const int eb_cap = D == 3 ? 256 : 512;
+    int eb = m->block_elems > 0 ? std::min(m->block_elems, eb_cap) : eb_cap;
     eb = std::min(eb, PLAN_MAX_KEYS / nv);
     std::vector<int32_t> blk_elem{0}, part_blk{0};
     for (int k = 0; k < K; ++k) {
@@ -503,7 +572,8 @@ pfem_status prepare_impl(pfem_mesh* m, cudaStream_t s) {
            o_pn = take(sizeof(int32_t) * (K + 1)), o_pe = take(sizeof(int32_t) * (K + 1)),
            o_bc = take(sizeof(int32_t) * (nb + 1)), o_cb = take(sizeof(int32_t) * (nch + 1)),
            o_pc = take(sizeof(int32_t) * (K + 1)), o_le = take(sizeof(uint16_t) * (size_t)nent),
-           o_np = take(sizeof(int32_t) * ((size_t)N + 1)), o_cnt = take(sizeof(int32_t) * (nb + 1));
+           o_np = take(sizeof(int32_t) * ((size_t)N + 1)), o_cnt = take(sizeof(int32_t) * (nb + 1)),
+           o_fc = take(sizeof(int32_t) * (nb + 1)), o_bf = take(sizeof(int32_t) * (nb + 1));
     size_t fixed = o;
     void* pool1 = nullptr;
     cudaError_t ce = cudaMallocAsync(&pool1, fixed, s);
@@ -520,9 +590,11 @@ pfem_status prepare_impl(pfem_mesh* m, cudaStream_t s) {
         P->part_chunk = (int32_t*)(pb + o_pc);
         P->loc_ent = (uint16_t*)(pb + o_le);
         P->node_occ_ptr = (int32_t*)(pb + o_np);
+        P->blk_fix = (int32_t*)(pb + o_bf);
     };
     bind((char*)pool1);
     int32_t* occ_cnt = (int32_t*)((char*)pool1 + o_cnt);
+    int32_t* fix_cnt = (int32_t*)((char*)pool1 + o_fc);
     P->pool = pool1;
     auto fail = [&](pfem_status st) { cudaFreeAsync(P->pool, s); delete P; return st; };
 #define PLAN_TRY(expr) do { cudaError_t _e = (expr); if (_e != cudaSuccess) return fail(cuda_status(_e, #expr)); } while (0)
@@ -545,24 +617,29 @@ pfem_status prepare_impl(pfem_mesh* m, cudaStream_t s) {
         if (st != PFEM_OK) return fail(st);
     }
     k_block_build<<<nb, PLAN_THREADS, 0, s>>>(0, nv, nb, P->blk_elem, m->conn, m->csr_ptr, m->csr_ent,
-                                              occ_cnt, P->blk_min_dep, nullptr, nullptr, nullptr,
-                                              nullptr, nullptr, nullptr);
+                                              occ_cnt, fix_cnt, P->blk_min_dep, nullptr, nullptr, nullptr,
+                                              nullptr, nullptr, nullptr, nullptr, nullptr);
     count_launch();
     PLAN_TRY(cudaGetLastError());
     PLAN_TRY(cudaMemsetAsync(occ_cnt + nb, 0, sizeof(int32_t), s));
+    PLAN_TRY(cudaMemsetAsync(fix_cnt + nb, 0, sizeof(int32_t), s));
     {
         pfem_status st = exclusive_scan_i32(occ_cnt, P->blk_occ, nb + 1, s);
         if (st != PFEM_OK) return fail(st);
+        st = exclusive_scan_i32(fix_cnt, P->blk_fix, nb + 1, s);
+        if (st != PFEM_OK) return fail(st);
     }
-    int32_t n_occ = 0;
+    int32_t n_occ = 0, n_fix = 0;
     PLAN_TRY(cudaMemcpyAsync(&n_occ, P->blk_occ + nb, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    PLAN_TRY(cudaMemcpyAsync(&n_fix, P->blk_fix + nb, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     PLAN_TRY(cudaStreamSynchronize(s));
     P->n_occ = n_occ;
+    P->n_fix = n_fix;
     // second allocation: occurrence arrays
     size_t o2 = 0;
     auto take2 = [&](size_t bytes) { size_t at = o2; o2 += align_up(bytes, 256); return at; };
     size_t q_on = take2(sizeof(int32_t) * (size_t)n_occ), q_oe = take2(sizeof(int32_t) * ((size_t)n_occ + 1)),
-           q_no = take2(sizeof(int32_t) * (size_t)n_occ);
+           q_no = take2(sizeof(int32_t) * (size_t)n_occ), q_fo = take2(sizeof(int32_t) * ((size_t)n_fix + 1));
     // grow the pool: allocate a new pool of fixed + o2 and copy the fixed part
     void* pool2 = nullptr;
     PLAN_TRY(cudaMallocAsync(&pool2, fixed + o2, s));
@@ -574,14 +651,82 @@ pfem_status prepare_impl(pfem_mesh* m, cudaStream_t s) {
     P->occ_node = (int32_t*)(pb + fixed + q_on);
     P->occ_ent_ptr = (int32_t*)(pb + fixed + q_oe);
     P->node_occ = (int32_t*)(pb + fixed + q_no);
+    P->fix_occ = (int32_t*)(pb + fixed + q_fo);
     occ_cnt = (int32_t*)(pb + o_cnt);
     k_block_build<<<nb, PLAN_THREADS, 0, s>>>(1, nv, nb, P->blk_elem, m->conn, m->csr_ptr, m->csr_ent,
-                                              nullptr, nullptr, P->blk_occ, P->occ_node, P->occ_ent_ptr,
-                                              P->loc_ent, P->node_occ_ptr, P->node_occ);
+                                              nullptr, nullptr, nullptr, P->blk_occ, P->occ_node, P->occ_ent_ptr,
+                                              P->loc_ent, P->node_occ_ptr, P->node_occ, P->blk_fix, P->fix_occ);
     count_launch();
     PLAN_TRY(cudaGetLastError());
     int32_t tail = (int32_t)nent;
     PLAN_TRY(cudaMemcpyAsync(P->occ_ent_ptr + n_occ, &tail, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    // fix-up source lists (third allocation)
+    {
+        const int nf = std::max(1, n_fix);
+        size_t o3 = 0;
+        auto take3 = [&](size_t bytes) { size_t at = o3; o3 += align_up(bytes, 256); return at; };
+        size_t r_ptr = take3(sizeof(int32_t) * ((size_t)nf + 1)), r_node = take3(sizeof(int32_t) * (size_t)nf),
+               r_cnt = take3(sizeof(int32_t) * ((size_t)nf + 1));
+        void* pool3 = nullptr;
+        PLAN_TRY(cudaMallocAsync(&pool3, o3, s));
+        P->pool_fix = pool3;
+        P->fix_src_ptr = (int32_t*)((char*)pool3 + r_ptr);
+        P->fix_node = (int32_t*)((char*)pool3 + r_node);
+        int32_t* fcnt = (int32_t*)((char*)pool3 + r_cnt);
+        PLAN_TRY(cudaMemsetAsync(fcnt, 0, sizeof(int32_t) * ((size_t)nf + 1), s));
+        if (n_fix > 0) {
+            k_fix_count<<<nblk(n_fix, 256), 256, 0, s>>>(n_fix, P->fix_occ, P->occ_node, P->node_occ_ptr, fcnt, P->fix_node);
+            count_launch();
+            PLAN_TRY(cudaGetLastError());
+        }
+        pfem_status st = exclusive_scan_i32(fcnt, P->fix_src_ptr, n_fix + 1, s);
+        if (st != PFEM_OK) return fail(st);
+        int32_t n_src = 0;
+        PLAN_TRY(cudaMemcpyAsync(&n_src, P->fix_src_ptr + n_fix, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        PLAN_TRY(cudaStreamSynchronize(s));
+        void* pool4 = nullptr;
+        PLAN_TRY(cudaMallocAsync(&pool4, sizeof(int32_t) * (size_t)std::max(1, n_src), s));
+        P->pool_src = pool4;
+        P->fix_src = (int32_t*)pool4;
+        if (n_fix > 0) {
+            k_fix_fill<<<nblk(n_fix, 256), 256, 0, s>>>(n_fix, P->fix_node, P->node_occ_ptr, P->node_occ,
+                                                         P->fix_src_ptr, P->fix_src);
+            count_launch();
+            PLAN_TRY(cudaGetLastError());
+        }
+    }
+    // packed block records (one TMA bulk copy per block in the CSR kernel)
+    {
+        std::vector<int32_t> bo(nb + 1);
+        PLAN_TRY(cudaMemcpyAsync(bo.data(), P->blk_occ, sizeof(int32_t) * (nb + 1), cudaMemcpyDeviceToHost, s));
+        PLAN_TRY(cudaStreamSynchronize(s));
+        int ocap = 8;
+        for (int b = 0; b < nb; ++b) ocap = std::max(ocap, bo[b + 1] - bo[b]);
+        ocap = (ocap + 7) / 8 * 8;
+        const size_t ts = m->dtype == PFEM_F64 ? 8 : 4;
+        P->rec = rec_layout(D, ts, eb_cap, ocap);
+        void* pr = nullptr;
+        PLAN_TRY(cudaMallocAsync(&pr, (size_t)P->rec.bytes * nb, s));
+        P->pool_rec = pr;
+        P->recs = (unsigned char*)pr;
+        if (D == 2) {
+            if (ts == 4)
+                k_pack_records<2, float><<<nb, 256, 0, s>>>(E, P->blk_elem, P->blk_occ, m->conn, (const float*)m->grad,
+                    (const float*)m->vol, P->occ_node, P->occ_ent_ptr, P->loc_ent, P->recs, P->rec);
+            else
+                k_pack_records<2, double><<<nb, 256, 0, s>>>(E, P->blk_elem, P->blk_occ, m->conn, (const double*)m->grad,
+                    (const double*)m->vol, P->occ_node, P->occ_ent_ptr, P->loc_ent, P->recs, P->rec);
+        } else {
+            if (ts == 4)
+                k_pack_records<3, float><<<nb, 256, 0, s>>>(E, P->blk_elem, P->blk_occ, m->conn, (const float*)m->grad,
+                    (const float*)m->vol, P->occ_node, P->occ_ent_ptr, P->loc_ent, P->recs, P->rec);
+            else
+                k_pack_records<3, double><<<nb, 256, 0, s>>>(E, P->blk_elem, P->blk_occ, m->conn, (const double*)m->grad,
+                    (const double*)m->vol, P->occ_node, P->occ_ent_ptr, P->loc_ent, P->recs, P->rec);
+        }
+        count_launch();
+        PLAN_TRY(cudaGetLastError());
+    }
     PLAN_TRY(cudaStreamSynchronize(s));
 #undef PLAN_TRY
     m->n_blocks = nb;
@@ -594,6 +739,9 @@ void release_impl(pfem_mesh* m) {
     if (!m || !m->plan) return;
     Plan* P = reinterpret_cast<Plan*>(m->plan);
     if (P->pool) cudaFree(P->pool);
+    if (P->pool_fix) cudaFree(P->pool_fix);
+    if (P->pool_src) cudaFree(P->pool_src);
+    if (P->pool_rec) cudaFree(P->pool_rec);
     delete P;
     m->plan = nullptr;
 }
