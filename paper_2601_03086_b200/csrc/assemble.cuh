@@ -35,7 +35,8 @@ namespace pfem {
 
 enum { OP_ENERGY = 0, OP_ENERGY_RESIDUAL = 1, OP_RESIDUAL = 2, OP_TANGENT = 3 };
 constexpr int ASM_NT = 256;   // main (element / occurrence) threads per CTA
-constexpr int FIX_WARPS = 2;  // fix-up warps per CTA
+constexpr int FIX_WARPS = 1;  // fix-up warps per CTA (+1 publisher warp)
+constexpr int FIX_UNROLL = 4; // segments loaded together by one fix-up lane
 constexpr int CHUNK = 32;     // blocks per reduction chunk (== CHUNK_BLOCKS of prep.cu)
 
 template <int D>
@@ -85,13 +86,15 @@ struct AsmParams {
     const int32_t* fix_node;
     const int32_t* fix_src_ptr;
     const int32_t* fix_src;
+    int n_fix;
     RecLayout rec;
     const unsigned char* recs;
     // workspace
     Counters* ctr;
     int32_t* flag;         // [n_blocks]
     double* blk_sum;       // [2S+2][n_blocks]: W_s, f.u_s, dot(main), dot(fix-up)
-    int32_t* chunk_done;   // [n_chunks]
+    int32_t* fix_flag;     // [n_blocks] fix-up of block done (CG dot)
+    int32_t* chunk_flag;   // [n_chunks] chunk reduced
     double* chunk_sum;     // [2S+1][n_chunks]
     T* partial;            // [n_occ][S][D]
     CgState* cg;           // non-null: fused p.q and alpha epilogue (S == 1)
@@ -226,6 +229,24 @@ __device__ __forceinline__ void ld_relaxed_vec(const T* p, T* v) {
     for (int k = 0; k < N; ++k) v[k] = ld_relaxed(p + k);
 }
 
+// L2 (coherent) loads of n <= N contiguous values; segments are published with release
+// and observed through a relaxed flag load before these loads are issued
+template <class T, int N>
+__device__ __forceinline__ void ld_cg_vec(const T* p, T* v, int n) {
+    if constexpr (N * sizeof(T) % 16 == 0) {
+        if (n == N && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+            for (int k = 0; k < N * (int)sizeof(T) / 16; ++k) {
+                const float4 q = __ldcg(reinterpret_cast<const float4*>(p) + k);
+                memcpy(reinterpret_cast<char*>(v) + 16 * k, &q, 16);
+            }
+            return;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k) v[k] = k < n ? __ldcg(p + k) : T(0);
+}
+
 // stage block b: one bulk copy of its packed record (thread 0) + per-element material
 // (cp.async, only for element-wise parameters); every thread commits one cp.async group
 template <int D, class T, int NT>
@@ -245,47 +266,453 @@ __device__ __forceinline__ void stage_block(unsigned char* st, T* mst, uint64_t*
     cp_commit();
 }
 
-// warp-group reduction of the chunk containing block `blk` once all its arrivals are in;
-// the completing group also finalises (totals / CG alpha) after the last chunk
-template <class T>
-__device__ __forceinline__ void chunk_reduce(const AsmParams<T>& p, int ch, int rb, int re, int w, int nw, int lane,
-                                             bool& last) {
-    const int c0 = __ldg(p.chunk_blk + ch), c1 = __ldg(p.chunk_blk + ch + 1);
-    const int S = p.S;
-    for (int r = rb + w; r < re; r += nw) {
-        double v = 0.0;
-        if (c0 + lane < c1) {
-            v = ld_relaxed(p.blk_sum + (int64_t)r * p.n_blocks + c0 + lane);
-            if (r == 2 * S) v += ld_relaxed(p.blk_sum + (int64_t)(2 * S + 1) * p.n_blocks + c0 + lane);
+// =====================================================================================
+// Kernel A (CSR mode): persistent element-block kernel.  CTA i processes blocks i, i+G,
+// i+2G, ... (no cross-CTA synchronisation at all).  Per block:
+//   stage   : ONE TMA bulk copy of the block's packed record (conn, grad N, V, block-local
+//             CSR, local vertex ids), prefetched one block ahead with mbarrier completion;
+//             element-wise material and the block's nodal fields (u, v for the NH tangent)
+//             prefetched into shared memory with cp.async (after the record has landed)
+//   phase 1 : thread per element: H, P / dP, psi from shared memory only -> nodal forces of
+//             all ST samples -> fbuf[slot][element][dim][sample] (fp32 pairs as FFMA2 lanes)
+//   phase 2 : thread per node occurrence: sum its block-local CSR entries (ascending element,
+//             slot).  Nodes touched only by this block: final value -> out.  Others: the
+//             block's segment -> seg[o][s][d] (finished by kernel B).
+// Kernel B: thread per multi-block node: out = sum of its segments in ascending block order
+// (i.e. its CSR row summed segment by segment), masked rows, the CG dot; per-part energy
+// totals and CG alpha by the last CTA.  Every sum has a fixed order: no float atomics.
+// =====================================================================================
+template <int D, class T, int NT, int ST, bool MASKED>
+__device__ __forceinline__ void stage_fields(T* ust, const unsigned char* rec, const T* src, const AsmParams<T>& p,
+                                             int s0, int nq, int no) {
+    // ust[occ][D][ST] <- src[s0 + q][node(occ)][i]; masked DOFs are zero-filled (src-size 0)
+    const int32_t* socc = reinterpret_cast<const int32_t*>(rec + p.rec.occ_node);
+    for (int o = threadIdx.x; o < no; o += NT) {
+        const int node = socc[o] & OCC_NODE_MASK;
+        T* dst = ust + (size_t)o * D * ST;
+        const T* g = src + (int64_t)s0 * p.sstride + (int64_t)node * D;
+        uint32_t keep[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) keep[i] = MASKED ? (__ldg(p.mask + (int64_t)node * D + i) ? 0u : (uint32_t)sizeof(T)) : (uint32_t)sizeof(T);
+        for (int q = 0; q < nq; ++q) {
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                if (MASKED)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(smem_addr(dst + i * ST + q)),
+                                 "l"(g + i), "n"(sizeof(T)), "r"(keep[i]));
+                else
+                    cpn<sizeof(T)>(dst + i * ST + q, g + i);
+            }
+            g += p.sstride;
         }
-        v = warp_sum(v);
-        if (lane == 0) p.chunk_sum[(int64_t)r * p.n_chunks + ch] = v;
     }
-    last = false;
-    (void)c1;
 }
 
-template <class T, bool HAS_PSI, bool TANGENT>
-__device__ __forceinline__ void finalize(const AsmParams<T>& p, int w, int nw, int lane) {
+template <int D, int MODEL, class T, int OP, int ST, bool MASKED, int EB, int NT>
+__global__ void __launch_bounds__(NT, 2)
+k_assemble(const AsmParams<T> p) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr bool HAS_FORCE = OP != OP_ENERGY;
+    constexpr bool HAS_PSI = OP == OP_ENERGY || OP == OP_ENERGY_RESIDUAL;
+    constexpr int NV = D + 1;
+    constexpr int SD = ST * D;
+    constexpr int NF = 1;    // staged field: u (energy / residual) or v (tangent; the NH state u is gathered)
+    using V = std::conditional_t<(sizeof(T) == 4 && ST % 2 == 0), F2, T>;
+    constexpr int L = VTraits<V>::L;
+    using A2 = std::conditional_t<(sizeof(T) == 4 && SD % 2 == 0), F2, T>;     // phase-2 accumulator
+    constexpr int LA = VTraits<A2>::L;
+    const T* staged_src = (OP == OP_TANGENT) ? p.v : p.u;
+    // shared layout: rec[2] | mat[2][2][EB] | ust[2][OCAP][D][ST] | fbuf[NV][EB][D][ST]
+    unsigned char* stage_ptr[2] = {smem_raw, smem_raw + p.rec.bytes};
+    T* mstage = reinterpret_cast<T*>(smem_raw + 2 * (size_t)p.rec.bytes);
+    T* ustage = mstage + 4 * EB;
+    const size_t ust_sz = (size_t)NF * p.rec.ocap * D * ST;
+    T* fbuf = ustage + 2 * ust_sz;
+    __shared__ __align__(8) uint64_t s_bar[2];
+    __shared__ double s_red[NT / 32][2 * ST + 1];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int S = p.S;
-    if (HAS_PSI && p.totals) {
-        for (int pair = w; pair < S * p.K; pair += nw) {
+    const bool pref = S <= ST;          // nodal fields staged in shared memory (else direct gathers)
+    const bool cgdot = OP == OP_TANGENT && p.cg != nullptr;
+    if (p.cg && ld_relaxed_i(&p.cg->done)) return;     // converged CG: the whole grid exits
+
+    if (tid == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    int n_inv = 0, first_inv = INT32_MAX, n_nonfin = 0;
+    const int G = gridDim.x;
+    int t = blockIdx.x;
+    uint32_t parity[2] = {0u, 0u};
+    // prologue: record of the first block, then its fields
+    if (t < p.n_blocks) {
+        stage_block<D, T, NT>(stage_ptr[0], mstage, &s_bar[0], p, t);
+        if (pref) {
+            mbar_wait(&s_bar[0], 0);
+            stage_fields<D, T, NT, ST, MASKED>(ustage, stage_ptr[0], staged_src, p, 0, S,
+                                               __ldg(p.blk_occ + t + 1) - __ldg(p.blk_occ + t));
+        }
+        cp_commit();
+    }
+    for (int it = 0; t < p.n_blocks; ++it, t += G) {
+        const int cur = it & 1;
+        const int tn = t + G;
+        const int b = t;
+        // prefetch the next block's record (its fields follow after phase 1)
+        if (tn < p.n_blocks) stage_block<D, T, NT>(stage_ptr[cur ^ 1], mstage + 2 * EB * (cur ^ 1), &s_bar[cur ^ 1], p, tn);
+        else cp_commit();
+        const int e0 = __ldg(p.blk_elem + b), ne = __ldg(p.blk_elem + b + 1) - e0;
+        const int o0 = __ldg(p.blk_occ + b), no = __ldg(p.blk_occ + b + 1) - o0;
+        const unsigned char* sg = stage_ptr[cur];
+        const int32_t* sconn = reinterpret_cast<const int32_t*>(sg + p.rec.conn);
+        const T* sgrad = reinterpret_cast<const T*>(sg + p.rec.g);
+        const T* svol = reinterpret_cast<const T*>(sg + p.rec.vol);
+        const int32_t* socc = reinterpret_cast<const int32_t*>(sg + p.rec.occ_node);
+        const uint16_t* soe = reinterpret_cast<const uint16_t*>(sg + p.rec.occ_ent);
+        const uint16_t* sle = reinterpret_cast<const uint16_t*>(sg + p.rec.loc_ent);
+        const uint16_t* slc = reinterpret_cast<const uint16_t*>(sg + p.rec.lconn);
+        const int32_t* sseg = reinterpret_cast<const int32_t*>(sg + p.rec.occ_seg);
+        const T* smat = mstage + 2 * EB * cur;
+        const T* ust = ustage + ust_sz * cur;
+        mbar_wait(&s_bar[cur], parity[cur]);   // this block's record
+        parity[cur] ^= 1u;
+        cp_wait<1>();                          // this thread's material + field copies of block b
+        bar_main(NT);                          // everyone's field copies have landed
+        double dot_acc = 0.0;
+        double wsum[ST], fsum[ST];
+#pragma unroll
+        for (int q = 0; q < ST; ++q) wsum[q] = fsum[q] = 0.0;
+        for (int s0 = 0; s0 < S; s0 += ST) {
+            const int nq = min(ST, S - s0);
+            // ---------------- phase 1: elements
+            T wacc[ST];
+#pragma unroll
+            for (int q = 0; q < ST; ++q) wacc[q] = T(0);
+            for (int el = tid; el < ne; el += NT) {
+                const int e = e0 + el;
+                Geo<D, T> G_;
+                if constexpr (D == 3) {
+                    const int4 cv = *reinterpret_cast<const int4*>(sconn + el * 4);
+                    G_.v[0] = cv.x; G_.v[1] = cv.y; G_.v[2] = cv.z; G_.v[3] = cv.w;
+                } else {
+#pragma unroll
+                    for (int a = 0; a <= D; ++a) G_.v[a] = sconn[el * NV + a];
+                }
+#pragma unroll
+                for (int a = 0; a < D; ++a)
+#pragma unroll
+                    for (int j = 0; j < D; ++j) G_.g[a][j] = sgrad[(a * D + j) * EB + el];
+                G_.V = svol[el];
+                {
+                    const T m0 = p.mat.s0 ? smat[el] : __ldg(p.mat.p0);
+                    const T m1 = p.mat.s1 ? smat[EB + el] : __ldg(p.mat.p1);
+                    lame_of<T>(p.mat.kind, m0, m1, G_.mu, G_.lam);
+                    G_.mu *= G_.V;
+                    G_.lam *= G_.V;
+                }
+                int lv[NV];
+#pragma unroll
+                for (int a = 0; a < NV; ++a) lv[a] = slc[el * NV + a];
+#pragma unroll
+                for (int qq = 0; qq < ST; qq += L) {
+                    if (qq >= nq || (p.dbg & 1)) break;
+                    const int s = s0 + qq;
+                    const int64_t lstride = (L > 1 && qq + 1 >= nq) ? 0 : p.sstride;
+                    V x[NV][D], H[D][D], P[D][D], psi = V(T(0));
+                    int bad = 0;
+                    // staged field (u, or v for the tangent) from shared memory when prefetched
+                    auto load_staged = [&](V xx[NV][D]) {
+                        if (pref) {
+#pragma unroll
+                            for (int a = 0; a < NV; ++a)
+#pragma unroll
+                                for (int i = 0; i < D; ++i)
+                                    xx[a][i] = *reinterpret_cast<const V*>(ust + ((size_t)lv[a] * D + i) * ST + qq);
+                        } else {
+                            gather<D, T, V, (OP == OP_TANGENT) && MASKED>(staged_src + (int64_t)s * p.sstride, lstride,
+                                                                           p.mask, G_, xx);
+                        }
+                    };
+                    if constexpr (OP == OP_TANGENT) {
+                        NhState<D, V> NS;
+                        if constexpr (MODEL == MODEL_NH) {
+                            V Hu[D][D];
+                            gather<D, T, V, false>(p.u + (int64_t)s * p.sstride, lstride, nullptr, G_, x);
+                            grad_of<D, T, V>(G_, x, Hu);
+                            nh_state<D, V>(Hu, NS);
+                            bad = n_bad(NS.x);
+                        }
+                        load_staged(x);
+                        grad_of<D, T, V>(G_, x, H);
+                        dstress<D, MODEL, T, V>(G_, NS, H, P);
+                    } else {
+                        load_staged(x);
+                        grad_of<D, T, V>(G_, x, H);
+                        stress<D, MODEL, T, V, HAS_PSI>(G_, H, P, psi, bad);
+                    }
+                    if (MODEL == MODEL_NH && bad) {
+                        n_inv += bad;
+                        first_inv = min(first_inv, e);
+                    }
+                    if (HAS_PSI) {
+#pragma unroll
+                        for (int k = 0; k < L; ++k) {
+                            if (qq + k >= nq) break;
+                            const T w = pfem::lane(psi, k);
+                            if (!isfinite(w)) ++n_nonfin;
+                            wacc[qq + k] += w;
+                            if (p.W_e) p.W_e[(int64_t)(s + k) * p.E + e] = w;
+                        }
+                    }
+                    if (HAS_FORCE) {
+                        V f[NV][D];
+                        forces<D, T, V>(G_, P, f);
+#pragma unroll
+                        for (int a = 0; a < NV; ++a)
+#pragma unroll
+                            for (int i = 0; i < D; ++i)
+                                *reinterpret_cast<V*>(fbuf + (((size_t)a * EB + el) * D + i) * ST + qq) = f[a][i];
+                        if (!HAS_PSI && !isfinite(pfem::lane(f[0][0], 0))) ++n_nonfin;
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < ST; ++q) wsum[q] += (double)wacc[q];   // per-thread, fixed order
+            // the next block's fields: its record has had phase 1 to land
+            if (s0 + ST >= S) {
+                if (pref && tn < p.n_blocks) {
+                    mbar_wait(&s_bar[cur ^ 1], parity[cur ^ 1]);
+                    stage_fields<D, T, NT, ST, MASKED>(ustage + ust_sz * (cur ^ 1), stage_ptr[cur ^ 1], staged_src, p, 0, S,
+                                                       __ldg(p.blk_occ + tn + 1) - __ldg(p.blk_occ + tn));
+                }
+                cp_commit();
+            }
+            if ((HAS_FORCE || p.f_ext) && !(p.dbg & 2)) {
+                bar_main(NT);
+                // ---------------- phase 2: block-local CSR gather, thread per occurrence
+                for (int oi = tid; oi < no; oi += NT) {
+                    const int o = o0 + oi;
+                    const int word = socc[oi];
+                    const int node = word & OCC_NODE_MASK;
+                    if (HAS_FORCE) {
+                        A2 acc[SD / LA];
+#pragma unroll
+                        for (int k = 0; k < SD / LA; ++k) acc[k] = A2(T(0));
+                        const int kb = soe[oi], k1 = soe[oi + 1];
+                        int k = kb;
+                        for (; k + 1 < k1; k += 2) {      // two independent entries per step
+                            const int j0 = sle[k], j1 = sle[k + 1];
+                            const int el0 = j0 / NV, a0 = j0 - el0 * NV, el1 = j1 / NV, a1 = j1 - el1 * NV;
+                            A2 f0[SD / LA], f1[SD / LA];
+                            sld<T, SD>(fbuf + ((size_t)a0 * EB + el0) * SD, reinterpret_cast<T*>(f0));
+                            sld<T, SD>(fbuf + ((size_t)a1 * EB + el1) * SD, reinterpret_cast<T*>(f1));
+#pragma unroll
+                            for (int c = 0; c < SD / LA; ++c) acc[c] += f0[c];
+#pragma unroll
+                            for (int c = 0; c < SD / LA; ++c) acc[c] += f1[c];
+                        }
+                        if (k < k1) {
+                            const int j = sle[k];
+                            const int el = j / NV, a = j - el * NV;
+                            A2 f[SD / LA];
+                            sld<T, SD>(fbuf + ((size_t)a * EB + el) * SD, reinterpret_cast<T*>(f));
+#pragma unroll
+                            for (int c = 0; c < SD / LA; ++c) acc[c] += f[c];
+                        }
+                        const T* accs = reinterpret_cast<const T*>(acc);
+                        if (word & (OCC_NONOWNER | OCC_EARLIER)) {
+                            // this block's segment of a multi-block node: seg[slot][s][d], slots
+                            // node-major (a node's segments contiguous, ascending block)
+                            const int slot = sseg[oi];
+#pragma unroll
+                            for (int q = 0; q < ST; ++q) {
+                                if (q >= nq) break;
+                                T* dst = p.partial + ((int64_t)slot * S + s0 + q) * D;
+#pragma unroll
+                                for (int i = 0; i < D; ++i) dst[i] = accs[i * ST + q];
+                            }
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < ST; ++q) {
+                                if (q >= nq) break;
+                                const int64_t nb = (int64_t)(s0 + q) * p.sstride + (int64_t)node * D;
+#pragma unroll
+                                for (int i = 0; i < D; ++i) {
+                                    T val = accs[i * ST + q];
+                                    if (OP == OP_TANGENT && MASKED && __ldg(p.mask + (int64_t)node * D + i))
+                                        val = __ldg(p.v + nb + i);
+                                    p.out[nb + i] = val;
+                                    if (cgdot) dot_acc += (double)__ldg(p.v + nb + i) * (double)val;
+                                }
+                            }
+                        }
+                    }
+                    if (HAS_PSI && p.f_ext && !(word & OCC_NONOWNER)) {
+#pragma unroll
+                        for (int q = 0; q < ST; ++q) {
+                            if (q >= nq) break;
+                            const int64_t nb = (int64_t)(s0 + q) * p.sstride + (int64_t)node * D;
+                            double w = 0.0;
+#pragma unroll
+                            for (int i = 0; i < D; ++i)
+                                w += (double)__ldg(p.f_ext + (int64_t)node * D + i) * (double)__ldg(p.u + nb + i);
+                            fsum[q] += w;
+                        }
+                    }
+                }
+            }
+            if (HAS_PSI && S > ST) {
+                // several sample chunks: flush this chunk's per-sample sums directly
+                bar_main(NT);
+#pragma unroll
+                for (int q = 0; q < ST; ++q) {
+                    double a = warp_sum(q < nq ? wsum[q] : 0.0), f2 = warp_sum(q < nq ? fsum[q] : 0.0);
+                    if (lane == 0) { s_red[warp][q] = a; s_red[warp][ST + q] = f2; }
+                    wsum[q] = fsum[q] = 0.0;
+                }
+                bar_main(NT);
+                if (tid < 2 * nq) {
+                    const int q = tid % nq, kind = tid / nq;
+                    double r = 0.0;
+                    for (int w = 0; w < NT / 32; ++w) r += s_red[w][kind * ST + q];
+                    p.blk_sum[(int64_t)(kind * S + s0 + q) * p.n_blocks + b] = r;
+                }
+                bar_main(NT);
+            } else if (HAS_FORCE && s0 + ST < S) {
+                bar_main(NT);   // fbuf is reused by the next chunk
+            }
+        }
+        // ---------------- per-block sums (single-chunk case) and CG dot
+        if (((HAS_PSI && S <= ST) || cgdot) && !(p.dbg & 8)) {
+            if (HAS_PSI && S <= ST) {
+#pragma unroll
+                for (int q = 0; q < ST; ++q) {
+                    if (q >= S) break;
+                    const double a = (double)warp_sum_t<T>((T)wsum[q]);
+                    const double f2 = p.f_ext ? warp_sum(fsum[q]) : 0.0;
+                    if (lane == 0) { s_red[warp][q] = a; s_red[warp][ST + q] = f2; }
+                }
+            }
+            if (cgdot) {
+                const double d2 = warp_sum(dot_acc);
+                if (lane == 0) s_red[warp][2 * ST] = d2;
+            }
+        }
+        bar_main(NT);   // phase 2 done (fbuf free), s_red complete
+        if (((HAS_PSI && S <= ST) || cgdot) && !(p.dbg & 8) && warp == 0) {
+            if (HAS_PSI && S <= ST && lane < 2 * S) {
+                const int q = lane % S, kind = lane / S;
+                double r = 0.0;
+                for (int w = 0; w < NT / 32; ++w) r += s_red[w][kind * ST + q];
+                p.blk_sum[(int64_t)(kind * S + q) * p.n_blocks + b] = r;
+            }
+            if (cgdot && lane == 31) {
+                double r = 0.0;
+                for (int w = 0; w < NT / 32; ++w) r += s_red[w][2 * ST];
+                p.blk_sum[(int64_t)(2 * S) * p.n_blocks + b] = r;
+            }
+        }
+        // s_red is rewritten only after the next block's first barrier: warp 0 is done by then
+    }
+    cp_wait<0>();
+    if (n_inv) {
+        atomicAdd(&p.ctr->n_inv, n_inv);
+        atomicMax(&p.ctr->first_inv, INT32_MAX - first_inv);
+    }
+    if (n_nonfin) atomicAdd(&p.ctr->n_nonfinite, n_nonfin);
+    // let kernel B's prologue start (programmatic dependent launch); its grid-dependency
+    // wait still covers every write of this grid
+    asm volatile("griddepcontrol.launch_dependents;");
+}
+
+// Kernel B: finish multi-block nodes, chunked energy / dot reductions, totals, CG alpha.
+template <int D, class T, int ST, bool MASKED, int NTB>
+__global__ void __launch_bounds__(NTB)
+k_node_finish(const AsmParams<T> p, int op_psi, int n_items) {
+    __shared__ double s_red[NTB / 32];
+    __shared__ int s_last;
+    constexpr int SD = ST * D;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int S = p.S;
+    const bool cgdot = p.cg != nullptr;
+    asm volatile("griddepcontrol.wait;" ::: "memory");    // kernel A complete and visible
+    if (p.cg && ld_relaxed_i(&p.cg->done)) return;
+    double dot_acc = 0.0;
+    // ---------------- multi-block nodes: item = (fix entry, sample chunk)
+    const int nsc = (S + ST - 1) / ST;
+    for (int item = blockIdx.x * NTB + tid; item < n_items; item += gridDim.x * NTB) {
+        const int f = item / nsc, s0 = (item - f * nsc) * ST;
+        const int nq = min(ST, S - s0);
+        const int node = __ldg(p.fix_node + f);
+        const int k0 = __ldg(p.fix_src_ptr + f), k1 = __ldg(p.fix_src_ptr + f + 1);
+        // the node's segments are contiguous: seg[k][s][d], k in [k0, k1) (ascending block)
+        T acc[SD];
+        ld_cg_vec<T, SD>(p.partial + ((int64_t)k0 * S + s0) * D, acc, nq * D);
+        for (int k = k0 + 1; k < k1; ++k) {
+            T v[SD];
+            ld_cg_vec<T, SD>(p.partial + ((int64_t)k * S + s0) * D, v, nq * D);
+#pragma unroll
+            for (int c = 0; c < SD; ++c) acc[c] += v[c];
+        }
+#pragma unroll
+        for (int q = 0; q < ST; ++q) {
+            if (q >= nq) break;
+            const int64_t nb = (int64_t)(s0 + q) * p.sstride + (int64_t)node * D;
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                T val = acc[q * D + i];
+                if (MASKED && __ldg(p.mask + (int64_t)node * D + i)) val = __ldg(p.v + nb + i);
+                p.out[nb + i] = val;
+                if (cgdot) dot_acc += (double)__ldg(p.v + nb + i) * (double)val;
+            }
+        }
+    }
+    // ---------------- chunk reductions of the per-block sums (one chunk per CTA)
+    const int rb = op_psi ? 0 : 2 * S;
+    const int re = cgdot ? 2 * S + 1 : (op_psi ? 2 * S : 2 * S);
+    for (int ch = blockIdx.x; ch < p.n_chunks; ch += gridDim.x) {
+        const int c0 = __ldg(p.chunk_blk + ch), c1 = __ldg(p.chunk_blk + ch + 1);
+        for (int r = rb + warp; r < re; r += NTB / 32) {
+            double v = (c0 + lane < c1) ? __ldcg(p.blk_sum + (int64_t)r * p.n_blocks + c0 + lane) : 0.0;
+            v = warp_sum(v);
+            if (lane == 0) p.chunk_sum[(int64_t)r * p.n_chunks + ch] = v;
+        }
+    }
+    if (cgdot) {
+        const double t = cta_sum<NTB>(dot_acc, s_red);
+        if (tid == 0) p.blk_sum[(int64_t)(2 * S + 1) * p.n_blocks + blockIdx.x] = t;   // per-CTA dot
+    }
+    // ---------------- last CTA: totals per (sample, part), CG alpha, flags, reset
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        s_last = atomicAdd(&p.ctr->exit_count, 1) == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (op_psi && p.totals) {
+        for (int pair = warp; pair < S * p.K; pair += NTB / 32) {
             const int s = pair / p.K, k = pair - s * p.K;
             const int cb = __ldg(p.part_chunk + k), ce = __ldg(p.part_chunk + k + 1);
             double wv = 0.0, fv = 0.0;
             for (int cc = cb + lane; cc < ce; cc += 32) {
-                wv += ld_relaxed(p.chunk_sum + (int64_t)s * p.n_chunks + cc);
-                fv += ld_relaxed(p.chunk_sum + (int64_t)(S + s) * p.n_chunks + cc);
+                wv += __ldcg(p.chunk_sum + (int64_t)s * p.n_chunks + cc);
+                fv += __ldcg(p.chunk_sum + (int64_t)(S + s) * p.n_chunks + cc);
             }
             wv = warp_sum(wv);
             fv = warp_sum(fv);
             if (lane == 0) p.totals[(int64_t)s * p.K + k] = (T)(wv - fv);
         }
     }
-    if (TANGENT && p.cg && w == 0) {
+    if (cgdot && warp == 0) {
         double pq = 0.0;
-        for (int cc = lane; cc < p.n_chunks; cc += 32) pq += ld_relaxed(p.chunk_sum + (int64_t)(2 * S) * p.n_chunks + cc);
-        pq = warp_sum(pq);
+        for (int cc = lane; cc < p.n_chunks; cc += 32) pq += __ldcg(p.chunk_sum + (int64_t)(2 * S) * p.n_chunks + cc);
+        double pb = 0.0;
+        for (int cc = lane; cc < (int)gridDim.x; cc += 32) pb += __ldcg(p.blk_sum + (int64_t)(2 * S + 1) * p.n_blocks + cc);
+        pq = warp_sum(pq) + warp_sum(pb);
         if (lane == 0) {
             CgState* cg = p.cg;
             cg->pq = pq;
@@ -298,399 +725,7 @@ __device__ __forceinline__ void finalize(const AsmParams<T>& p, int w, int nw, i
             }
         }
     }
-}
-
-// Persistent, software-pipelined CSR-mode kernel.
-//   main warps (NT threads): ticket stream over blocks.  Per block: the packed record is
-//     staged by ONE TMA bulk copy (prefetched one block ahead, mbarrier completion) and the
-//     ticket after next is requested; phase 1 -> fbuf -> phase 2 -> outputs / partials;
-//     warp 0 then publishes the block (flag, release) and does the reductions while the
-//     other warps start the next block.  Main warps never wait on other CTAs.
-//   fix-up warps (NFW x 32 threads): an independent ticket stream over blocks c; wait
-//     until the blocks holding c's segments have published, then write the final value of
-//     every node c owns that has earlier segments (ascending block order).
-template <int D, int MODEL, class T, int OP, int ST, bool MASKED, int EB, int NT, int NFW>
-__global__ void __launch_bounds__(NT + 32 * NFW, 2)
-k_assemble(const AsmParams<T> p) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    unsigned char* stage_ptr[2] = {smem_raw, smem_raw + p.rec.bytes};
-    T* mstage = reinterpret_cast<T*>(smem_raw + 2 * (size_t)p.rec.bytes);               // [2][2][EB]
-    T* fbuf = mstage + 4 * EB;                                                           // [NV][EB][D][ST]
-    __shared__ __align__(8) uint64_t s_bar[2];
-    __shared__ int s_tk[2], s_epoch;
-    __shared__ double s_red[NT / 32][2 * ST + 1];
-    constexpr bool HAS_FORCE = OP != OP_ENERGY;
-    constexpr bool HAS_PSI = OP == OP_ENERGY || OP == OP_ENERGY_RESIDUAL;
-    constexpr int NV = D + 1;
-    constexpr int SD = ST * D;
-    using V = std::conditional_t<(sizeof(T) == 4 && ST % 2 == 0), F2, T>;
-    constexpr int L = VTraits<V>::L;
-    using A2 = std::conditional_t<(sizeof(T) == 4 && SD % 2 == 0), F2, T>;     // phase-2 accumulator
-    constexpr int LA = VTraits<A2>::L;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int S = p.S;
-    const bool cgdot = OP == OP_TANGENT && p.cg != nullptr;
-    const int arrivals = cgdot ? 2 : 1;   // main (+ fix-up for the CG dot)
-    if (p.cg && ld_relaxed_i(&p.cg->done)) return;     // converged CG: the whole grid exits
-
     if (tid == 0) {
-        s_epoch = ld_relaxed_i(&p.ctr->epoch);
-        mbar_init(&s_bar[0], 1);
-        mbar_init(&s_bar[1], 1);
-        mbar_fence_init();
-    }
-    __syncthreads();
-    const int epoch = s_epoch;
-    int n_inv = 0, first_inv = INT32_MAX, n_nonfin = 0;
-
-    if (warp >= NT / 32) {
-        // =================================================================  fix-up warps
-        if (!HAS_FORCE || (p.dbg & 4)) goto done;
-        while (true) {
-            int c = 0;
-            if (lane == 0) c = atomicAdd(&p.ctr->fix_ticket, 1);
-            c = __shfl_sync(0xffffffffu, c, 0);
-            if (c >= p.n_blocks) break;
-            double dot_acc = 0.0;
-            const int f0 = __ldg(p.blk_fix + c), nfix = __ldg(p.blk_fix + c + 1) - f0;
-            if (nfix > 0) {
-                const int md = __ldg(p.blk_min_dep + c);
-                for (int q = md + lane; q <= c; q += 32) {
-                    unsigned ns = 256;
-                    while (ld_relaxed_i(p.flag + q) != epoch + 1) {
-                        __nanosleep(ns);
-                        ns = min(ns * 2, 4096u);
-                    }
-                }
-                __syncwarp();
-                for (int fi = lane; fi < nfix; fi += 32) {
-                    const int f = f0 + fi;
-                    const int node = __ldg(p.fix_node + f);
-                    const int k0 = __ldg(p.fix_src_ptr + f), k1 = __ldg(p.fix_src_ptr + f + 1);
-                    for (int s = 0; s < S; ++s) {
-                        T acc[D];
-                        ld_relaxed_vec<T, D>(p.partial + ((int64_t)__ldg(p.fix_src + k0) * S + s) * D, acc);
-                        for (int k = k0 + 1; k < k1; ++k) {
-                            T v[D];
-                            ld_relaxed_vec<T, D>(p.partial + ((int64_t)__ldg(p.fix_src + k) * S + s) * D, v);
-#pragma unroll
-                            for (int i = 0; i < D; ++i) acc[i] += v[i];
-                        }
-                        const int64_t nb = (int64_t)s * p.sstride + (int64_t)node * D;
-#pragma unroll
-                        for (int i = 0; i < D; ++i) {
-                            T val = acc[i];
-                            if (OP == OP_TANGENT && MASKED && __ldg(p.mask + (int64_t)node * D + i)) val = __ldg(p.v + nb + i);
-                            p.out[nb + i] = val;
-                            if (cgdot) dot_acc += (double)__ldg(p.v + nb + i) * (double)val;
-                        }
-                    }
-                }
-            }
-            if (cgdot) {
-                dot_acc = warp_sum(dot_acc);
-                int last = 0;
-                const int ch = __ldg(p.blk_chunk + c);
-                if (lane == 0) {
-                    p.blk_sum[(int64_t)(2 * S + 1) * p.n_blocks + c] = dot_acc;
-                    const int need = arrivals * (__ldg(p.chunk_blk + ch + 1) - __ldg(p.chunk_blk + ch));
-                    last = atom_add_acq_rel(p.chunk_done + ch, 1) == need - 1;
-                }
-                last = __shfl_sync(0xffffffffu, last, 0);
-                if (last) {
-                    bool dummy;
-                    chunk_reduce<T>(p, ch, 2 * S, 2 * S + 1, 0, 1, lane, dummy);
-                    int fin = 0;
-                    if (lane == 0) {
-                        p.chunk_done[ch] = 0;
-                        fin = atom_add_acq_rel(&p.ctr->done, 1) == p.n_chunks - 1;
-                    }
-                    fin = __shfl_sync(0xffffffffu, fin, 0);
-                    if (fin) finalize<T, HAS_PSI, OP == OP_TANGENT>(p, 0, 1, lane);
-                }
-            }
-        }
-        goto done;
-    }
-
-    {
-        // =================================================================  main warps
-        if (tid == 0) {
-            s_tk[0] = atomicAdd(&p.ctr->ticket, 1);
-            s_tk[1] = atomicAdd(&p.ctr->ticket, 1);
-        }
-        bar_main(NT);
-        int t = s_tk[0], t_next = s_tk[1];
-        uint32_t parity[2] = {0u, 0u};
-        if (t < p.n_blocks && !(p.dbg & 16)) stage_block<D, T, NT>(stage_ptr[0], mstage, &s_bar[0], p, t);
-        else cp_commit();
-        int it = 0;
-        int req = 0;   // ticket requested by thread 0 this iteration (consumed after phase 2)
-        while (t < p.n_blocks) {
-            const int cur = it & 1;
-            if (tid == 0) req = (t_next < p.n_blocks) ? atomicAdd(&p.ctr->ticket, 1) : p.n_blocks;
-            if (t_next < p.n_blocks && !(p.dbg & 16))
-                stage_block<D, T, NT>(stage_ptr[cur ^ 1], mstage + 2 * EB * (cur ^ 1), &s_bar[cur ^ 1], p, t_next);
-            else
-                cp_commit();
-            const int b = t;
-            const int e0 = __ldg(p.blk_elem + b), ne = __ldg(p.blk_elem + b + 1) - e0;
-            const int o0 = __ldg(p.blk_occ + b), no = __ldg(p.blk_occ + b + 1) - o0;
-            const unsigned char* sg = stage_ptr[cur];
-            const int32_t* sconn = reinterpret_cast<const int32_t*>(sg + p.rec.conn);
-            const T* sgrad = reinterpret_cast<const T*>(sg + p.rec.g);
-            const T* svol = reinterpret_cast<const T*>(sg + p.rec.vol);
-            const int32_t* socc = reinterpret_cast<const int32_t*>(sg + p.rec.occ_node);
-            const uint16_t* soe = reinterpret_cast<const uint16_t*>(sg + p.rec.occ_ent);
-            const uint16_t* sle = reinterpret_cast<const uint16_t*>(sg + p.rec.loc_ent);
-            const T* smat = mstage + 2 * EB * cur;
-            cp_wait<1>();                                   // this thread's material copies
-            if (!(p.dbg & 16)) mbar_wait(&s_bar[cur], parity[cur]);   // the block record
-            parity[cur] ^= 1u;
-            double dot_acc = 0.0;
-            double wsum[ST], fsum[ST];
-#pragma unroll
-            for (int q = 0; q < ST; ++q) wsum[q] = fsum[q] = 0.0;
-            for (int s0 = 0; s0 < S; s0 += ST) {
-                const int nq = min(ST, S - s0);
-                // ---------------- phase 1: elements
-                T wacc[ST];
-#pragma unroll
-                for (int q = 0; q < ST; ++q) wacc[q] = T(0);
-                for (int el = tid; el < ne; el += NT) {
-                    const int e = e0 + el;
-                    Geo<D, T> G;
-                    if constexpr (D == 3) {
-                        const int4 cv = *reinterpret_cast<const int4*>(sconn + el * 4);
-                        G.v[0] = cv.x; G.v[1] = cv.y; G.v[2] = cv.z; G.v[3] = cv.w;
-                    } else {
-#pragma unroll
-                        for (int a = 0; a <= D; ++a) G.v[a] = sconn[el * NV + a];
-                    }
-#pragma unroll
-                    for (int a = 0; a < D; ++a)
-#pragma unroll
-                        for (int j = 0; j < D; ++j) G.g[a][j] = sgrad[(a * D + j) * EB + el];
-                    G.V = svol[el];
-                    {
-                        const T m0 = p.mat.s0 ? smat[el] : __ldg(p.mat.p0);
-                        const T m1 = p.mat.s1 ? smat[EB + el] : __ldg(p.mat.p1);
-                        lame_of<T>(p.mat.kind, m0, m1, G.mu, G.lam);
-                        G.mu *= G.V;
-                        G.lam *= G.V;
-                    }
-#pragma unroll
-                    for (int qq = 0; qq < ST; qq += L) {
-                        if (qq >= nq || (p.dbg & 1)) break;
-                        const int s = s0 + qq;
-                        // lanes beyond the last sample re-read sample s (results discarded)
-                        const int64_t lstride = (L > 1 && qq + 1 >= nq) ? 0 : p.sstride;
-                        V x[NV][D], H[D][D], P[D][D], psi = V(T(0));
-                        int bad = 0;
-                        if constexpr (OP == OP_TANGENT) {
-                            NhState<D, V> NS;
-                            if constexpr (MODEL == MODEL_NH) {
-                                V Hu[D][D];
-                                gather<D, T, V, false>(p.u + (int64_t)s * p.sstride, lstride, nullptr, G, x);
-                                grad_of<D, T, V>(G, x, Hu);
-                                nh_state<D, V>(Hu, NS);
-                                bad = n_bad(NS.x);
-                            }
-                            gather<D, T, V, MASKED>(p.v + (int64_t)s * p.sstride, lstride, p.mask, G, x);
-                            grad_of<D, T, V>(G, x, H);
-                            dstress<D, MODEL, T, V>(G, NS, H, P);
-                        } else {
-                            gather<D, T, V, false>(p.u + (int64_t)s * p.sstride, lstride, nullptr, G, x);
-                            grad_of<D, T, V>(G, x, H);
-                            stress<D, MODEL, T, V, HAS_PSI>(G, H, P, psi, bad);
-                        }
-                        if (MODEL == MODEL_NH && bad) {
-                            n_inv += bad;
-                            first_inv = min(first_inv, e);
-                        }
-                        if (HAS_PSI) {
-#pragma unroll
-                            for (int k = 0; k < L; ++k) {
-                                if (qq + k >= nq) break;
-                                const T w = pfem::lane(psi, k);
-                                if (!isfinite(w)) ++n_nonfin;
-                                wacc[qq + k] += w;
-                                if (p.W_e) p.W_e[(int64_t)(s + k) * p.E + e] = w;
-                            }
-                        }
-                        if (HAS_FORCE) {
-                            V f[NV][D];
-                            forces<D, T, V>(G, P, f);
-#pragma unroll
-                            for (int a = 0; a < NV; ++a)
-#pragma unroll
-                                for (int i = 0; i < D; ++i)
-                                    *reinterpret_cast<V*>(fbuf + (((size_t)a * EB + el) * D + i) * ST + qq) = f[a][i];
-                            if (!HAS_PSI && !isfinite(pfem::lane(f[0][0], 0))) ++n_nonfin;
-                        }
-                    }
-                }
-#pragma unroll
-                for (int q = 0; q < ST; ++q) wsum[q] += (double)wacc[q];   // per-thread, fixed order
-                if ((HAS_FORCE || p.f_ext) && !(p.dbg & 2)) {
-                    bar_main(NT);
-                    // ---------------- phase 2: block-local CSR gather, thread per occurrence
-                    for (int oi = tid; oi < no; oi += NT) {
-                        const int o = o0 + oi;
-                        const int word = socc[oi];
-                        const int node = word & OCC_NODE_MASK;
-                        if (HAS_FORCE) {
-                            A2 acc[SD / LA];
-#pragma unroll
-                            for (int k = 0; k < SD / LA; ++k) acc[k] = A2(T(0));
-                            const int k1 = soe[oi + 1];
-                            for (int k = soe[oi]; k < k1; ++k) {
-                                const int j = sle[k];
-                                const int el = j / NV, a = j - el * NV;
-                                A2 f[SD / LA];
-                                sld<T, SD>(fbuf + ((size_t)a * EB + el) * SD, reinterpret_cast<T*>(f));
-#pragma unroll
-                                for (int c = 0; c < SD / LA; ++c) acc[c] += f[c];
-                            }
-                            const T* accs = reinterpret_cast<const T*>(acc);
-                            if (word & (OCC_NONOWNER | OCC_EARLIER)) {
-                                // segment of a node finished elsewhere: partial[o][s][i]
-#pragma unroll
-                                for (int q = 0; q < ST; ++q) {
-                                    if (q >= nq) break;
-                                    T* dst = p.partial + ((int64_t)o * S + s0 + q) * D;
-#pragma unroll
-                                    for (int i = 0; i < D; ++i) dst[i] = accs[i * ST + q];
-                                }
-                            } else {
-#pragma unroll
-                                for (int q = 0; q < ST; ++q) {
-                                    if (q >= nq) break;
-                                    const int64_t nb = (int64_t)(s0 + q) * p.sstride + (int64_t)node * D;
-#pragma unroll
-                                    for (int i = 0; i < D; ++i) {
-                                        T val = accs[i * ST + q];
-                                        if (OP == OP_TANGENT && MASKED && __ldg(p.mask + (int64_t)node * D + i))
-                                            val = __ldg(p.v + nb + i);
-                                        p.out[nb + i] = val;
-                                        if (cgdot) dot_acc += (double)__ldg(p.v + nb + i) * (double)val;
-                                    }
-                                }
-                            }
-                        }
-                        if (HAS_PSI && p.f_ext && !(word & OCC_NONOWNER)) {
-#pragma unroll
-                            for (int q = 0; q < ST; ++q) {
-                                if (q >= nq) break;
-                                const int64_t nb = (int64_t)(s0 + q) * p.sstride + (int64_t)node * D;
-                                double w = 0.0;
-#pragma unroll
-                                for (int i = 0; i < D; ++i)
-                                    w += (double)__ldg(p.f_ext + (int64_t)node * D + i) * (double)__ldg(p.u + nb + i);
-                                fsum[q] += w;
-                            }
-                        }
-                    }
-                }
-                if (HAS_PSI && S > ST) {
-                    // several chunks: flush this chunk's sums (per-sample channels)
-                    bar_main(NT);
-#pragma unroll
-                    for (int q = 0; q < ST; ++q) {
-                        double a = warp_sum(q < nq ? wsum[q] : 0.0), f2 = warp_sum(q < nq ? fsum[q] : 0.0);
-                        if (lane == 0) { s_red[warp][q] = a; s_red[warp][ST + q] = f2; }
-                        wsum[q] = fsum[q] = 0.0;
-                    }
-                    bar_main(NT);
-                    if (tid < 2 * nq) {
-                        const int q = tid % nq, kind = tid / nq;
-                        double r = 0.0;
-                        for (int w = 0; w < NT / 32; ++w) r += s_red[w][kind * ST + q];
-                        p.blk_sum[(int64_t)(kind * S + s0 + q) * p.n_blocks + b] = r;
-                    }
-                } else if (HAS_FORCE && s0 + ST < S) {
-                    bar_main(NT);   // fbuf is reused by the next chunk
-                }
-            }
-            // ---------------- per-warp sums into shared memory (single-chunk case), CG dot
-            const bool sums = ((HAS_PSI && S <= ST) || cgdot) && !(p.dbg & 8);
-            if (sums) {
-                if (HAS_PSI && S <= ST) {
-#pragma unroll
-                    for (int q = 0; q < ST; ++q) {
-                        if (q >= S) break;
-                        const double a = (double)warp_sum_t<T>((T)wsum[q]);
-                        const double f2 = p.f_ext ? warp_sum(fsum[q]) : 0.0;
-                        if (lane == 0) { s_red[warp][q] = a; s_red[warp][ST + q] = f2; }
-                    }
-                }
-                if (cgdot) {
-                    const double d2 = warp_sum(dot_acc);
-                    if (lane == 0) s_red[warp][2 * ST] = d2;
-                }
-            }
-            if (tid == 0) s_tk[it & 1] = req;    // the ticket after next (requested long ago)
-            bar_main(NT);                        // phase-2 writes, s_red and s_tk complete
-            // ---------------- warp 0: block sums, publish, chunk arrival; others go on
-            if (warp == 0) {
-                if (sums) {
-                    if (HAS_PSI && S <= ST && lane < 2 * S) {
-                        const int q = lane % S, kind = lane / S;
-                        double r = 0.0;
-                        for (int w = 0; w < NT / 32; ++w) r += s_red[w][kind * ST + q];
-                        p.blk_sum[(int64_t)(kind * S + q) * p.n_blocks + b] = r;
-                    }
-                    if (cgdot && lane == 31) {
-                        double r = 0.0;
-                        for (int w = 0; w < NT / 32; ++w) r += s_red[w][2 * ST];
-                        p.blk_sum[(int64_t)(2 * S) * p.n_blocks + b] = r;
-                    }
-                    __syncwarp();
-                }
-                int last = 0;
-                if (lane == 0) {
-                    // release is cumulative over the CTA's writes observed through the barrier
-                    if (HAS_FORCE) st_release_gpu(p.flag + b, epoch + 1);
-                    if ((HAS_PSI || cgdot) && !(p.dbg & 8)) {
-                        const int ch = __ldg(p.blk_chunk + b);
-                        const int need = arrivals * (__ldg(p.chunk_blk + ch + 1) - __ldg(p.chunk_blk + ch));
-                        last = atom_add_acq_rel(p.chunk_done + ch, 1) == need - 1;
-                    }
-                }
-                last = __shfl_sync(0xffffffffu, last, 0);
-                if (last) {
-                    const int ch = __ldg(p.blk_chunk + b);
-                    bool dummy;
-                    chunk_reduce<T>(p, ch, HAS_PSI ? 0 : 2 * S, cgdot ? 2 * S + 1 : 2 * S, 0, 1, lane, dummy);
-                    int fin = 0;
-                    if (lane == 0) {
-                        p.chunk_done[ch] = 0;
-                        fin = atom_add_acq_rel(&p.ctr->done, 1) == p.n_chunks - 1;
-                    }
-                    fin = __shfl_sync(0xffffffffu, fin, 0);
-                    if (fin) finalize<T, HAS_PSI, OP == OP_TANGENT>(p, 0, 1, lane);
-                }
-            }
-            t = t_next;
-            t_next = s_tk[it & 1];
-            ++it;
-        }
-        cp_wait<0>();
-        if (t_next < p.n_blocks) { /* unreachable: t_next >= t */ }
-    }
-
-done:
-    // every CTA reports its (rare) flag counts; the last CTA to leave publishes them and
-    // resets the workspace counters for the next launch
-    if (n_inv) {
-        atomicAdd(&p.ctr->n_inv, n_inv);
-        atomicMax(&p.ctr->first_inv, INT32_MAX - first_inv);
-    }
-    if (n_nonfin) atomicAdd(&p.ctr->n_nonfinite, n_nonfin);
-    __threadfence();
-    __syncthreads();
-    if (tid == 0 && atomicAdd(&p.ctr->exit_count, 1) == (int)gridDim.x - 1) {
-        __threadfence();
         const int ni = ld_relaxed_i(&p.ctr->n_inv);
         const int fi = ld_relaxed_i(&p.ctr->first_inv);
         if (p.uflags) {
@@ -702,12 +737,7 @@ done:
         p.ctr->n_inv = 0;
         p.ctr->first_inv = 0;
         p.ctr->n_nonfinite = 0;
-        p.ctr->done = 0;
-        p.ctr->ticket = 0;
-        p.ctr->fix_ticket = 0;
         p.ctr->exit_count = 0;
-        __threadfence();
-        p.ctr->epoch = epoch + 1;
     }
 }
 

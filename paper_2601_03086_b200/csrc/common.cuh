@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include "../../include/pfem.h"
@@ -41,10 +42,13 @@ constexpr int32_t OCC_EARLIER = 0x20000000;    // owner, and earlier blocks hold
 // everything phase 1 and phase 2 read from HBM about the block, so a single TMA bulk copy
 // (cp.async.bulk) stages it into shared memory:
 //   conn [EB][d+1] int32 | grad [d*d][EB] T | vol [EB] T | occ_node [OCAP] int32 |
-//   occ_ent [OCAP+1] uint16 (block-relative entry offsets) | loc_ent [(d+1) EB] uint16
+//   occ_ent [OCAP+1] uint16 (block-relative entry offsets) | loc_ent [(d+1) EB] uint16 |
+//   lconn [EB][d+1] uint16 (block-local occurrence index of each element vertex) |
+//   occ_seg [OCAP] int32 (node-major segment slot of a multi-block node's occurrence, -1 if
+//   the node is finished inside the block)
 struct RecLayout {
     int eb = 0, ocap = 0;
-    uint32_t conn = 0, g = 0, vol = 0, occ_node = 0, occ_ent = 0, loc_ent = 0, bytes = 0;
+    uint32_t conn = 0, g = 0, vol = 0, occ_node = 0, occ_ent = 0, loc_ent = 0, lconn = 0, occ_seg = 0, bytes = 0;
 };
 
 inline RecLayout rec_layout(int D, size_t tsize, int eb, int ocap) {
@@ -59,6 +63,8 @@ inline RecLayout rec_layout(int D, size_t tsize, int eb, int ocap) {
     L.occ_node = take(4 * (size_t)ocap);
     L.occ_ent = take(2 * (size_t)(ocap + 1));
     L.loc_ent = take(2 * (size_t)(D + 1) * eb);
+    L.lconn = take(2 * (size_t)(D + 1) * eb);
+    L.occ_seg = take(4 * (size_t)ocap);
     L.bytes = (uint32_t)o;
     return L;
 }
@@ -89,6 +95,8 @@ struct Plan {
     int32_t* fix_node = nullptr;      // [n_fix] node id of each fix entry
     int32_t* fix_src_ptr = nullptr;   // [n_fix+1] offsets into fix_src
     int32_t* fix_src = nullptr;       // all occurrences of the node, ascending block (own last)
+    int32_t* occ_seg = nullptr;       // [n_occ] node-major segment slot (fix_src position), -1 single
+    int32_t n_seg = 0;                // segments of multi-block nodes (= fix_src_ptr[n_fix])
     void* pool_fix = nullptr;
     void* pool_src = nullptr;
     RecLayout rec;                    // packed block records (one bulk copy per block)
@@ -98,7 +106,7 @@ struct Plan {
 };
 
 // ------------------------------------------------------------------ workspace layout
-// [ Counters | blk_flag[n_blocks] | blk_sum[2S+2][n_blocks] (double) | chunk_done[n_chunks] |
+// [ Counters | blk_flag[n_blocks] | fix_flag[n_blocks] | blk_sum[2S+2][n_blocks] (double) | chunk_flag[n_chunks] |
 //   chunk_sum[2S+1][n_chunks] (double) | partial[n_occ][S][d] (T) | colour-mode W [S][E] (T) ]
 struct Counters {
     int32_t ticket;
@@ -113,7 +121,7 @@ struct Counters {
 };
 
 struct WsLayout {
-    size_t counters, flags, blk_sum, chunk_done, chunk_sum, partial, wtmp, total;
+    size_t counters, flags, fix_flags, blk_sum, chunk_flags, chunk_sum, partial, wtmp, total;
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -123,10 +131,11 @@ inline WsLayout ws_layout(const Plan& p, int S, size_t tsize) {
     size_t o = 0;
     L.counters = o; o += align_up(sizeof(Counters), 256);
     L.flags = o;    o += align_up(sizeof(int32_t) * (size_t)(p.n_blocks + 1), 256);
+    L.fix_flags = o; o += align_up(sizeof(int32_t) * (size_t)(p.n_blocks + 1), 256);
     L.blk_sum = o;  o += align_up(sizeof(double) * (2 * (size_t)S + 2) * (p.n_blocks + 1), 256);
-    L.chunk_done = o; o += align_up(sizeof(int32_t) * (size_t)(p.n_chunks + 1), 256);
+    L.chunk_flags = o; o += align_up(sizeof(int32_t) * (size_t)(p.n_chunks + 1), 256);
     L.chunk_sum = o;  o += align_up(sizeof(double) * (2 * (size_t)S + 1) * (p.n_chunks + 1), 256);
-    L.partial = o;  o += align_up(tsize * (size_t)S * p.n_occ * p.dim, 256);
+    L.partial = o;  o += align_up(tsize * (size_t)S * std::max(p.n_seg, 1) * p.dim, 256);
     L.wtmp = o;     o += align_up(tsize * (size_t)S * p.n_elems, 256);
     L.total = o;
     return L;

@@ -8,6 +8,11 @@
 #include "assemble.cuh"
 
 namespace pfem {
+template <class T>
+inline int P_nfix(const AsmParams<T>& p) { return p.n_fix; }
+}  // namespace pfem
+
+namespace pfem {
 
 struct Call {
     const pfem_mesh* m;
@@ -75,6 +80,7 @@ AsmParams<T> make_params(const Call& c) {
     p.fix_node = P.fix_node;
     p.fix_src_ptr = P.fix_src_ptr;
     p.fix_src = P.fix_src;
+    p.n_fix = P.n_fix;
     p.rec = P.rec;
     p.recs = P.recs;
     const WsLayout L = ws_layout(P, c.S, sizeof(T));
@@ -82,7 +88,8 @@ AsmParams<T> make_params(const Call& c) {
     p.ctr = (Counters*)(w + L.counters);
     p.flag = (int32_t*)(w + L.flags);
     p.blk_sum = (double*)(w + L.blk_sum);
-    p.chunk_done = (int32_t*)(w + L.chunk_done);
+    p.fix_flag = (int32_t*)(w + L.fix_flags);
+    p.chunk_flag = (int32_t*)(w + L.chunk_flags);
     p.chunk_sum = (double*)(w + L.chunk_sum);
     p.partial = (T*)(w + L.partial);
     p.cg = c.cg;
@@ -94,34 +101,56 @@ AsmParams<T> make_params(const Call& c) {
 template <int D, int MODEL, class T, int OP, int ST, bool MASKED>
 pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
     constexpr bool HAS_FORCE = OP != OP_ENERGY;
+    constexpr bool HAS_PSI = OP == OP_ENERGY || OP == OP_ENERGY_RESIDUAL;
     constexpr int EB = EbOf<D>::value;
     constexpr int NT = ASM_NT;
-    constexpr int NFW = FIX_WARPS;
+    constexpr int NF = 1;
     const size_t smem = 2 * (size_t)p.rec.bytes + 4 * EB * sizeof(T) +
+                        2 * (size_t)NF * p.rec.ocap * D * ST * sizeof(T) +
                         (HAS_FORCE ? (size_t)ST * D * (D + 1) * EB * sizeof(T) : 0);
-    auto kern = k_assemble<D, MODEL, T, OP, ST, MASKED, EB, NT, NFW>;
-    static int resident = 0;   // per instantiation: co-resident CTAs on the device (persistent grid)
-    static size_t resident_smem = 0;
-    if (resident == 0 || smem > resident_smem) {
-        resident_smem = smem;
-        if (smem > 40 * 1024)   // dynamic + static smem beyond the 48 KB default
-            PFEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    auto kern = k_assemble<D, MODEL, T, OP, ST, MASKED, EB, NT>;
+    static int resident = 0;   // per instantiation: co-resident CTAs (persistent grid)
+    static size_t configured = 0;
+    if (resident == 0 || smem > configured) {
+        PFEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = smem;
         int dev = 0, nsm = 0, per_sm = 0;
         PFEM_CUDA_TRY(cudaGetDevice(&dev));
         PFEM_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        PFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT + 32 * NFW, smem));
-        resident = std::max(1, per_sm) * nsm;
+        PFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+        if (per_sm < 1) {
+            set_error("CSR kernel does not fit on an SM (block record too large)");
+            return PFEM_ERR_CAPACITY;
+        }
+        resident = per_sm * nsm;
     }
     if (p.eb_max > EB) {
         set_error("plan block larger than the kernel's block capacity");
         return PFEM_ERR_CAPACITY;
     }
-    p.lag = 0;
     static const int dbg = getenv("PFEM_DEBUG") ? atoi(getenv("PFEM_DEBUG")) : 0;
     p.dbg = dbg;
-    const int grid = std::min(resident, p.n_blocks);
-    kern<<<grid, NT + 32 * NFW, smem, s>>>(p);
+    const int grid = std::max(1, std::min(resident, p.n_blocks));
+    kern<<<grid, NT, smem, s>>>(p);
     PFEM_LAUNCH_CHECK("k_assemble");
+    // kernel B: finish multi-block nodes + reductions (programmatic dependent launch)
+    constexpr int NTB = 256;
+    const int nsc = (p.S + ST - 1) / ST;
+    const int n_items = HAS_FORCE ? P_nfix(p) * nsc : 0;
+    int gridb = std::max({1, (n_items + NTB - 1) / NTB, 0});
+    gridb = std::max(1, std::min(gridb, std::min(p.n_blocks, 4096)));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(gridb);
+    cfg.blockDim = dim3(NTB);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    PFEM_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_node_finish<D, T, ST, MASKED, NTB>, p, HAS_PSI ? 1 : 0, n_items));
+    count_launch();
     return PFEM_OK;
 }
 

@@ -347,12 +347,15 @@ __global__ void k_fix_count(int n_fix, const int32_t* __restrict__ fix_occ, cons
 
 __global__ void k_fix_fill(int n_fix, const int32_t* __restrict__ fix_node, const int32_t* __restrict__ node_occ_ptr,
                            const int32_t* __restrict__ node_occ, const int32_t* __restrict__ fix_src_ptr,
-                           int32_t* fix_src) {
+                           int32_t* fix_src, int32_t* occ_seg) {
     int f = blockIdx.x * blockDim.x + threadIdx.x;
     if (f >= n_fix) return;
     const int node = fix_node[f];
     const int k0 = node_occ_ptr[node], k1 = node_occ_ptr[node + 1];
-    for (int k = k0; k < k1; ++k) fix_src[fix_src_ptr[f] + (k - k0)] = node_occ[k];
+    for (int k = k0; k < k1; ++k) {
+        fix_src[fix_src_ptr[f] + (k - k0)] = node_occ[k];
+        occ_seg[node_occ[k]] = fix_src_ptr[f] + (k - k0);
+    }
 }
 
 // packed block records (see RecLayout): grid = blocks
@@ -361,7 +364,7 @@ __global__ void k_pack_records(int E, const int32_t* __restrict__ blk_elem, cons
                                const int32_t* __restrict__ conn, const T* __restrict__ grad,
                                const T* __restrict__ vol, const int32_t* __restrict__ occ_node,
                                const int32_t* __restrict__ occ_ent_ptr, const uint16_t* __restrict__ loc_ent,
-                               unsigned char* recs, RecLayout L) {
+                               const int32_t* __restrict__ occ_seg, unsigned char* recs, RecLayout L) {
     constexpr int NV = D + 1;
     const int b = blockIdx.x;
     const int e0 = blk_elem[b], ne = blk_elem[b + 1] - e0;
@@ -382,10 +385,28 @@ __global__ void k_pack_records(int E, const int32_t* __restrict__ blk_elem, cons
         rv[el] = in ? vol[e0 + el] : T(0);
     }
     for (int i = threadIdx.x; i < L.ocap; i += blockDim.x) ron[i] = i < no ? occ_node[o0 + i] : 0;
+    int32_t* ros = reinterpret_cast<int32_t*>(r + L.occ_seg);
+    for (int i = threadIdx.x; i < L.ocap; i += blockDim.x) ros[i] = i < no ? occ_seg[o0 + i] : -1;
     for (int i = threadIdx.x; i <= L.ocap; i += blockDim.x)
         roe[i] = (uint16_t)(i <= no ? occ_ent_ptr[o0 + i] - NV * e0 : NV * ne);
     for (int k = threadIdx.x; k < NV * L.eb; k += blockDim.x)
         rle[k] = k < NV * ne ? loc_ent[(int64_t)NV * e0 + k] : (uint16_t)0;
+    // local occurrence index of each element vertex: binary search in the block's sorted nodes
+    uint16_t* rlc = reinterpret_cast<uint16_t*>(r + L.lconn);
+    for (int k = threadIdx.x; k < NV * L.eb; k += blockDim.x) {
+        uint16_t idx = 0;
+        if (k < NV * ne) {
+            const int node = conn[(int64_t)NV * e0 + k];
+            int lo = 0, hi = no - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if ((occ_node[o0 + mid] & OCC_NODE_MASK) < node) lo = mid + 1;
+                else hi = mid;
+            }
+            idx = (uint16_t)lo;
+        }
+        rlc[k] = idx;
+    }
 }
 
 // ------------------------------------------------------------------ host driver
@@ -685,12 +706,16 @@ pfem_status prepare_impl(pfem_mesh* m, cudaStream_t s) {
         PLAN_TRY(cudaMemcpyAsync(&n_src, P->fix_src_ptr + n_fix, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         PLAN_TRY(cudaStreamSynchronize(s));
         void* pool4 = nullptr;
-        PLAN_TRY(cudaMallocAsync(&pool4, sizeof(int32_t) * (size_t)std::max(1, n_src), s));
+        const size_t src_bytes = align_up(sizeof(int32_t) * (size_t)std::max(1, n_src), 256);
+        PLAN_TRY(cudaMallocAsync(&pool4, src_bytes + sizeof(int32_t) * (size_t)std::max(1, n_occ), s));
         P->pool_src = pool4;
         P->fix_src = (int32_t*)pool4;
+        P->occ_seg = (int32_t*)((char*)pool4 + src_bytes);
+        P->n_seg = n_src;
+        PLAN_TRY(cudaMemsetAsync(P->occ_seg, 0xff, sizeof(int32_t) * (size_t)std::max(1, n_occ), s));
         if (n_fix > 0) {
             k_fix_fill<<<nblk(n_fix, 256), 256, 0, s>>>(n_fix, P->fix_node, P->node_occ_ptr, P->node_occ,
-                                                         P->fix_src_ptr, P->fix_src);
+                                                         P->fix_src_ptr, P->fix_src, P->occ_seg);
             count_launch();
             PLAN_TRY(cudaGetLastError());
         }
@@ -712,17 +737,17 @@ pfem_status prepare_impl(pfem_mesh* m, cudaStream_t s) {
         if (D == 2) {
             if (ts == 4)
                 k_pack_records<2, float><<<nb, 256, 0, s>>>(E, P->blk_elem, P->blk_occ, m->conn, (const float*)m->grad,
-                    (const float*)m->vol, P->occ_node, P->occ_ent_ptr, P->loc_ent, P->recs, P->rec);
+                    (const float*)m->vol, P->occ_node, P->occ_ent_ptr, P->loc_ent, P->occ_seg, P->recs, P->rec);
             else
                 k_pack_records<2, double><<<nb, 256, 0, s>>>(E, P->blk_elem, P->blk_occ, m->conn, (const double*)m->grad,
-                    (const double*)m->vol, P->occ_node, P->occ_ent_ptr, P->loc_ent, P->recs, P->rec);
+                    (const double*)m->vol, P->occ_node, P->occ_ent_ptr, P->loc_ent, P->occ_seg, P->recs, P->rec);
         } else {
             if (ts == 4)
                 k_pack_records<3, float><<<nb, 256, 0, s>>>(E, P->blk_elem, P->blk_occ, m->conn, (const float*)m->grad,
-                    (const float*)m->vol, P->occ_node, P->occ_ent_ptr, P->loc_ent, P->recs, P->rec);
+                    (const float*)m->vol, P->occ_node, P->occ_ent_ptr, P->loc_ent, P->occ_seg, P->recs, P->rec);
             else
                 k_pack_records<3, double><<<nb, 256, 0, s>>>(E, P->blk_elem, P->blk_occ, m->conn, (const double*)m->grad,
-                    (const double*)m->vol, P->occ_node, P->occ_ent_ptr, P->loc_ent, P->recs, P->rec);
+                    (const double*)m->vol, P->occ_node, P->occ_ent_ptr, P->loc_ent, P->occ_seg, P->recs, P->rec);
         }
         count_launch();
         PLAN_TRY(cudaGetLastError());
