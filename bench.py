@@ -175,7 +175,8 @@ def run_gpu(args):
     if world > 1:
         tdist.init_process_group("nccl", device_id=dev)
     pf.load()
-    prob = config3()
+    # weak scaling: every rank owns its own batch of 4 fields on the (replicated) mesh
+    prob = config3(seed_base=3000 + 1000 * rank) if rank else config3()
     E, N, d, S = prob.n_elems, prob.n_nodes, prob.dim, prob.n_samples
     t_prep0 = time.perf_counter()
     sets = build_workload(torch, pf, dev, prob, N_COPIES)
