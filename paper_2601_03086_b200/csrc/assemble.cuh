@@ -232,13 +232,13 @@ __device__ __forceinline__ void ld_relaxed_vec(const T* p, T* v) {
 // L2 (coherent) loads of n <= N contiguous values; segments are published with release
 // and observed through a relaxed flag load before these loads are issued
 template <class T, int N>
-__device__ __forceinline__ void ld_cg_vec(const T* p, T* v, int n) {
-    if constexpr (N * sizeof(T) % 16 == 0) {
+__device__ __forceinline__ void ld_cg_vec(const T* p, T (&v)[N], int n) {
+    if constexpr (sizeof(T) == 4 && N % 4 == 0) {
         if (n == N && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
 #pragma unroll
-            for (int k = 0; k < N * (int)sizeof(T) / 16; ++k) {
+            for (int k = 0; k < N / 4; ++k) {
                 const float4 q = __ldcg(reinterpret_cast<const float4*>(p) + k);
-                memcpy(reinterpret_cast<char*>(v) + 16 * k, &q, 16);
+                v[4 * k] = q.x; v[4 * k + 1] = q.y; v[4 * k + 2] = q.z; v[4 * k + 3] = q.w;
             }
             return;
         }
@@ -282,6 +282,59 @@ __device__ __forceinline__ void stage_block(unsigned char* st, T* mst, uint64_t*
 // (i.e. its CSR row summed segment by segment), masked rows, the CG dot; per-part energy
 // totals and CG alpha by the last CTA.  Every sum has a fixed order: no float atomics.
 // =====================================================================================
+// staged nodal values of the element's vertices (ust[occ][D][ST]); pairs of fp32 samples
+// are adjacent, so an F2 lane pair is one 8-byte shared load
+template <int D, class T, class V, int ST>
+__device__ __forceinline__ void load_staged_field(const T* __restrict__ ust, const int (&lv)[D + 1], int qq,
+                                                  V (&x)[D + 1][D]) {
+#pragma unroll
+    for (int a = 0; a <= D; ++a)
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            const T* src = ust + ((size_t)lv[a] * D + i) * ST + qq;
+            if constexpr (sizeof(V) == 8 && sizeof(T) == 4) {
+                const float2 q = *reinterpret_cast<const float2*>(src);
+                x[a][i] = V(q.x, q.y);
+            } else {
+                x[a][i] = *src;
+            }
+        }
+}
+
+// accumulate SD contiguous shared-memory values into acc without taking the address of a
+// register array (keeps acc in registers)
+template <class T, int SD>
+__device__ __forceinline__ void sacc(const T* __restrict__ src, T (&acc)[SD]) {
+    if constexpr (sizeof(T) == 4 && SD % 4 == 0) {
+#pragma unroll
+        for (int c = 0; c < SD / 4; ++c) {
+            const float4 q = reinterpret_cast<const float4*>(src)[c];
+            F2 a0(acc[4 * c], acc[4 * c + 1]), a1(acc[4 * c + 2], acc[4 * c + 3]);
+            a0 = a0 + F2(q.x, q.y);
+            a1 = a1 + F2(q.z, q.w);
+            acc[4 * c] = a0.v.x; acc[4 * c + 1] = a0.v.y; acc[4 * c + 2] = a1.v.x; acc[4 * c + 3] = a1.v.y;
+        }
+    } else if constexpr (sizeof(T) == 4 && SD % 2 == 0) {
+#pragma unroll
+        for (int c = 0; c < SD / 2; ++c) {
+            const float2 q = reinterpret_cast<const float2*>(src)[c];
+            F2 a0(acc[2 * c], acc[2 * c + 1]);
+            a0 = a0 + F2(q.x, q.y);
+            acc[2 * c] = a0.v.x; acc[2 * c + 1] = a0.v.y;
+        }
+    } else if constexpr (sizeof(T) == 8 && SD % 2 == 0) {
+#pragma unroll
+        for (int c = 0; c < SD / 2; ++c) {
+            const double2 q = reinterpret_cast<const double2*>(src)[c];
+            acc[2 * c] += q.x;
+            acc[2 * c + 1] += q.y;
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < SD; ++c) acc[c] += src[c];
+    }
+}
+
 template <int D, class T, int NT, int ST, bool MASKED>
 __device__ __forceinline__ void stage_fields(T* ust, const unsigned char* rec, const T* src, const AsmParams<T>& p,
                                              int s0, int nq, int no) {
@@ -323,7 +376,8 @@ k_assemble(const AsmParams<T> p) {
     constexpr int LA = VTraits<A2>::L;
     const T* staged_src = (OP == OP_TANGENT) ? p.v : p.u;
     // shared layout: rec[2] | mat[2][2][EB] | ust[2][OCAP][D][ST] | fbuf[NV][EB][D][ST]
-    unsigned char* stage_ptr[2] = {smem_raw, smem_raw + p.rec.bytes};
+    unsigned char* const stage0 = smem_raw;
+    unsigned char* const stage1 = smem_raw + p.rec.bytes;
     T* mstage = reinterpret_cast<T*>(smem_raw + 2 * (size_t)p.rec.bytes);
     T* ustage = mstage + 4 * EB;
     const size_t ust_sz = (size_t)NF * p.rec.ocap * D * ST;
@@ -345,13 +399,13 @@ k_assemble(const AsmParams<T> p) {
     int n_inv = 0, first_inv = INT32_MAX, n_nonfin = 0;
     const int G = gridDim.x;
     int t = blockIdx.x;
-    uint32_t parity[2] = {0u, 0u};
+    uint32_t par0 = 0u, par1 = 0u;   // mbarrier phase of each record buffer (registers, no arrays)
     // prologue: record of the first block, then its fields
     if (t < p.n_blocks) {
-        stage_block<D, T, NT>(stage_ptr[0], mstage, &s_bar[0], p, t);
+        stage_block<D, T, NT>(stage0, mstage, &s_bar[0], p, t);
         if (pref) {
             mbar_wait(&s_bar[0], 0);
-            stage_fields<D, T, NT, ST, MASKED>(ustage, stage_ptr[0], staged_src, p, 0, S,
+            stage_fields<D, T, NT, ST, MASKED>(ustage, stage0, staged_src, p, 0, S,
                                                __ldg(p.blk_occ + t + 1) - __ldg(p.blk_occ + t));
         }
         cp_commit();
@@ -361,11 +415,13 @@ k_assemble(const AsmParams<T> p) {
         const int tn = t + G;
         const int b = t;
         // prefetch the next block's record (its fields follow after phase 1)
-        if (tn < p.n_blocks) stage_block<D, T, NT>(stage_ptr[cur ^ 1], mstage + 2 * EB * (cur ^ 1), &s_bar[cur ^ 1], p, tn);
+        unsigned char* const sg_cur = cur ? stage1 : stage0;
+        unsigned char* const sg_nxt = cur ? stage0 : stage1;
+        if (tn < p.n_blocks) stage_block<D, T, NT>(sg_nxt, mstage + 2 * EB * (cur ^ 1), &s_bar[cur ^ 1], p, tn);
         else cp_commit();
         const int e0 = __ldg(p.blk_elem + b), ne = __ldg(p.blk_elem + b + 1) - e0;
         const int o0 = __ldg(p.blk_occ + b), no = __ldg(p.blk_occ + b + 1) - o0;
-        const unsigned char* sg = stage_ptr[cur];
+        const unsigned char* sg = sg_cur;
         const int32_t* sconn = reinterpret_cast<const int32_t*>(sg + p.rec.conn);
         const T* sgrad = reinterpret_cast<const T*>(sg + p.rec.g);
         const T* svol = reinterpret_cast<const T*>(sg + p.rec.vol);
@@ -376,8 +432,8 @@ k_assemble(const AsmParams<T> p) {
         const int32_t* sseg = reinterpret_cast<const int32_t*>(sg + p.rec.occ_seg);
         const T* smat = mstage + 2 * EB * cur;
         const T* ust = ustage + ust_sz * cur;
-        mbar_wait(&s_bar[cur], parity[cur]);   // this block's record
-        parity[cur] ^= 1u;
+        mbar_wait(&s_bar[cur], cur ? par1 : par0);   // this block's record
+        if (cur) par1 ^= 1u; else par0 ^= 1u;
         cp_wait<1>();                          // this thread's material + field copies of block b
         bar_main(NT);                          // everyone's field copies have landed
         double dot_acc = 0.0;
@@ -422,19 +478,6 @@ k_assemble(const AsmParams<T> p) {
                     const int64_t lstride = (L > 1 && qq + 1 >= nq) ? 0 : p.sstride;
                     V x[NV][D], H[D][D], P[D][D], psi = V(T(0));
                     int bad = 0;
-                    // staged field (u, or v for the tangent) from shared memory when prefetched
-                    auto load_staged = [&](V xx[NV][D]) {
-                        if (pref) {
-#pragma unroll
-                            for (int a = 0; a < NV; ++a)
-#pragma unroll
-                                for (int i = 0; i < D; ++i)
-                                    xx[a][i] = *reinterpret_cast<const V*>(ust + ((size_t)lv[a] * D + i) * ST + qq);
-                        } else {
-                            gather<D, T, V, (OP == OP_TANGENT) && MASKED>(staged_src + (int64_t)s * p.sstride, lstride,
-                                                                           p.mask, G_, xx);
-                        }
-                    };
                     if constexpr (OP == OP_TANGENT) {
                         NhState<D, V> NS;
                         if constexpr (MODEL == MODEL_NH) {
@@ -444,11 +487,13 @@ k_assemble(const AsmParams<T> p) {
                             nh_state<D, V>(Hu, NS);
                             bad = n_bad(NS.x);
                         }
-                        load_staged(x);
+                        if (pref) load_staged_field<D, T, V, ST>(ust, lv, qq, x);
+                        else gather<D, T, V, MASKED>(staged_src + (int64_t)s * p.sstride, lstride, p.mask, G_, x);
                         grad_of<D, T, V>(G_, x, H);
                         dstress<D, MODEL, T, V>(G_, NS, H, P);
                     } else {
-                        load_staged(x);
+                        if (pref) load_staged_field<D, T, V, ST>(ust, lv, qq, x);
+                        else gather<D, T, V, false>(staged_src + (int64_t)s * p.sstride, lstride, nullptr, G_, x);
                         grad_of<D, T, V>(G_, x, H);
                         stress<D, MODEL, T, V, HAS_PSI>(G_, H, P, psi, bad);
                     }
@@ -483,8 +528,8 @@ k_assemble(const AsmParams<T> p) {
             // the next block's fields: its record has had phase 1 to land
             if (s0 + ST >= S) {
                 if (pref && tn < p.n_blocks) {
-                    mbar_wait(&s_bar[cur ^ 1], parity[cur ^ 1]);
-                    stage_fields<D, T, NT, ST, MASKED>(ustage + ust_sz * (cur ^ 1), stage_ptr[cur ^ 1], staged_src, p, 0, S,
+                    mbar_wait(&s_bar[cur ^ 1], cur ? par0 : par1);
+                    stage_fields<D, T, NT, ST, MASKED>(ustage + ust_sz * (cur ^ 1), sg_nxt, staged_src, p, 0, S,
                                                        __ldg(p.blk_occ + tn + 1) - __ldg(p.blk_occ + tn));
                 }
                 cp_commit();
@@ -497,31 +542,15 @@ k_assemble(const AsmParams<T> p) {
                     const int word = socc[oi];
                     const int node = word & OCC_NODE_MASK;
                     if (HAS_FORCE) {
-                        A2 acc[SD / LA];
+                        T accs[SD];
 #pragma unroll
-                        for (int k = 0; k < SD / LA; ++k) acc[k] = A2(T(0));
+                        for (int k = 0; k < SD; ++k) accs[k] = T(0);
                         const int kb = soe[oi], k1 = soe[oi + 1];
-                        int k = kb;
-                        for (; k + 1 < k1; k += 2) {      // two independent entries per step
-                            const int j0 = sle[k], j1 = sle[k + 1];
-                            const int el0 = j0 / NV, a0 = j0 - el0 * NV, el1 = j1 / NV, a1 = j1 - el1 * NV;
-                            A2 f0[SD / LA], f1[SD / LA];
-                            sld<T, SD>(fbuf + ((size_t)a0 * EB + el0) * SD, reinterpret_cast<T*>(f0));
-                            sld<T, SD>(fbuf + ((size_t)a1 * EB + el1) * SD, reinterpret_cast<T*>(f1));
-#pragma unroll
-                            for (int c = 0; c < SD / LA; ++c) acc[c] += f0[c];
-#pragma unroll
-                            for (int c = 0; c < SD / LA; ++c) acc[c] += f1[c];
-                        }
-                        if (k < k1) {
+                        for (int k = kb; k < k1; ++k) {
                             const int j = sle[k];
                             const int el = j / NV, a = j - el * NV;
-                            A2 f[SD / LA];
-                            sld<T, SD>(fbuf + ((size_t)a * EB + el) * SD, reinterpret_cast<T*>(f));
-#pragma unroll
-                            for (int c = 0; c < SD / LA; ++c) acc[c] += f[c];
+                            sacc<T, SD>(fbuf + ((size_t)a * EB + el) * SD, accs);
                         }
-                        const T* accs = reinterpret_cast<const T*>(acc);
                         if (word & (OCC_NONOWNER | OCC_EARLIER)) {
                             // this block's segment of a multi-block node: seg[slot][s][d], slots
                             // node-major (a node's segments contiguous, ascending block)
