@@ -86,6 +86,7 @@ struct AsmParams {
     const int32_t* fix_node;
     const int32_t* fix_src_ptr;
     const int32_t* fix_src;
+    const int32_t* occ_seg;   // [n_occ] segment slot of a multi-block occurrence
     int n_fix;
     RecLayout rec;
     const unsigned char* recs;
@@ -397,6 +398,7 @@ k_assemble(const AsmParams<T> p) {
     }
     __syncthreads();
     int n_inv = 0, first_inv = INT32_MAX, n_nonfin = 0;
+    const LameScale<T> lsc = lame_scale<T>(p.mat);
     const int G = gridDim.x;
     int t = blockIdx.x;
     uint32_t par0 = 0u, par1 = 0u;   // mbarrier phase of each record buffer (registers, no arrays)
@@ -464,7 +466,7 @@ k_assemble(const AsmParams<T> p) {
                 {
                     const T m0 = p.mat.s0 ? smat[el] : __ldg(p.mat.p0);
                     const T m1 = p.mat.s1 ? smat[EB + el] : __ldg(p.mat.p1);
-                    lame_of<T>(p.mat.kind, m0, m1, G_.mu, G_.lam);
+                    lame_elem<T>(p.mat, lsc, m0, m1, G_.mu, G_.lam);
                     G_.mu *= G_.V;
                     G_.lam *= G_.V;
                 }

@@ -152,6 +152,34 @@ __device__ __forceinline__ void lame_of(int kind, T p0, T p1, T& mu, T& lam) {
     }
 }
 
+// (E, nu) with a uniform nu: both moduli are E times a constant, (mu, lambda) = E (mu_1, lambda_1)
+// with (mu_1, lambda_1) = lame(1, nu) formed once per thread, so the per-element work is two
+// multiplies instead of two divisions (1 ulp from the quotient form)
+template <class T>
+struct LameScale {
+    T mu1, lam1;
+    bool on;
+};
+
+template <class T>
+__device__ __forceinline__ LameScale<T> lame_scale(const MatArgs<T>& m) {
+    LameScale<T> L;
+    L.on = m.kind != KIND_LAME && m.s1 == 0;
+    L.mu1 = L.lam1 = T(0);
+    if (L.on) lame_of<T>(m.kind, T(1), __ldg(m.p1), L.mu1, L.lam1);
+    return L;
+}
+
+template <class T>
+__device__ __forceinline__ void lame_elem(const MatArgs<T>& m, const LameScale<T>& L, T p0, T p1, T& mu, T& lam) {
+    if (L.on) {
+        mu = p0 * L.mu1;
+        lam = p0 * L.lam1;
+    } else {
+        lame_of<T>(m.kind, p0, p1, mu, lam);
+    }
+}
+
 template <int D, class T>
 __device__ __forceinline__ void load_geo(int e, int E, const int32_t* __restrict__ conn,
                                          const T* __restrict__ grad, const T* __restrict__ vol,

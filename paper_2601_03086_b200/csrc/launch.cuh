@@ -6,6 +6,7 @@
 #include <cstdlib>
 
 #include "assemble.cuh"
+#include "assemble_direct.cuh"
 
 namespace pfem {
 template <class T>
@@ -80,6 +81,7 @@ AsmParams<T> make_params(const Call& c) {
     p.fix_node = P.fix_node;
     p.fix_src_ptr = P.fix_src_ptr;
     p.fix_src = P.fix_src;
+    p.occ_seg = P.occ_seg;
     p.n_fix = P.n_fix;
     p.rec = P.rec;
     p.recs = P.recs;
@@ -96,6 +98,32 @@ AsmParams<T> make_params(const Call& c) {
     p.dbg = 0;
     p.lag = 0;
     return p;
+}
+
+template <int D, int MODEL, class T, int OP, int ST, bool MASKED, int NT>
+pfem_status launch_direct(AsmParams<T> p, cudaStream_t s) {
+    constexpr bool HAS_FORCE = OP != OP_ENERGY;
+    constexpr int NFd = (OP == OP_TANGENT && MODEL == MODEL_NH) ? 2 : 1;
+    const size_t smem = ((NFd * (size_t)p.rec.ocap * D * ST * sizeof(T) + 2 * (size_t)(D + 1) * p.rec.eb + 15) &
+                         ~size_t(15)) +
+                        (HAS_FORCE ? (size_t)ST * D * (D + 1) * p.rec.eb * sizeof(T) : 0);
+    auto kd = k_assemble_direct<D, MODEL, T, OP, ST, MASKED, NT>;
+    static size_t configured = 0;
+    static int pf_auto = 0;
+    if (smem > configured || pf_auto == 0) {
+        PFEM_CUDA_TRY(cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
+        configured = std::max(configured, smem);
+        int dev = 0, nsm = 0, per_sm = 0;
+        PFEM_CUDA_TRY(cudaGetDevice(&dev));
+        PFEM_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        PFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kd, NT, smem));
+        pf_auto = std::max(1, per_sm * nsm);
+    }
+    static const int pf = getenv("PFEM_PF") ? atoi(getenv("PFEM_PF")) : -1;
+    p.lag = pf >= 0 ? pf : pf_auto;   // L2 prefetch distance in blocks (~ one wave ahead)
+    kd<<<std::max(1, p.n_blocks), NT, smem, s>>>(p);
+    PFEM_LAUNCH_CHECK("k_assemble_direct");
+    return PFEM_OK;
 }
 
 template <int D, int MODEL, class T, int OP, int ST, bool MASKED>
@@ -129,10 +157,21 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
         return PFEM_ERR_CAPACITY;
     }
     static const int dbg = getenv("PFEM_DEBUG") ? atoi(getenv("PFEM_DEBUG")) : 0;
+    static const int variant = getenv("PFEM_VARIANT") ? atoi(getenv("PFEM_VARIANT")) : -1;
     p.dbg = dbg;
-    const int grid = std::max(1, std::min(resident, p.n_blocks));
-    kern<<<grid, NT, smem, s>>>(p);
-    PFEM_LAUNCH_CHECK("k_assemble");
+    // kernel A form: direct (one CTA per block, small shared memory) for single-sample calls,
+    // where the kernel is bound by memory latency and occupancy pays; staged persistent
+    // otherwise (several samples per element: arithmetic-heavy, staging amortised).
+    // PFEM_VARIANT=0/1 forces staged/direct (measurement switch).
+    const bool direct = variant >= 0 ? variant == 1 : p.S == 1;
+    if (direct) {
+        const pfem_status st = launch_direct<D, MODEL, T, OP, ST, MASKED, NT>(p, s);
+        if (st != PFEM_OK) return st;
+    } else {
+        const int grid = std::max(1, std::min(resident, p.n_blocks));
+        kern<<<grid, NT, smem, s>>>(p);
+        PFEM_LAUNCH_CHECK("k_assemble");
+    }
     // kernel B: finish multi-block nodes + reductions (programmatic dependent launch)
     constexpr int NTB = 256;
     const int nsc = (p.S + ST - 1) / ST;
