@@ -40,7 +40,14 @@ __device__ __forceinline__ void l2_prefetch(const void* base, size_t total, size
 template <class T>
 __device__ __forceinline__ void prefetch_record(const AsmParams<T>& p, int b) {
     const size_t rb = (size_t)p.rec.bytes, total = rb * p.n_blocks;
-    l2_prefetch(p.recs, total, (size_t)b * rb + p.rec.g, rb - p.rec.g);
+    // the fields the direct kernel reads: gradients .. occ_seg, without conn; fp32 (ent_pos
+    // layout) skips loc_ent, fp64 skips ent_pos
+    if (sizeof(T) == 4) {
+        l2_prefetch(p.recs, total, (size_t)b * rb + p.rec.g, p.rec.loc_ent - p.rec.g);
+        l2_prefetch(p.recs, total, (size_t)b * rb + p.rec.lconn, rb - p.rec.lconn);
+    } else {
+        l2_prefetch(p.recs, total, (size_t)b * rb + p.rec.g, p.rec.ent_pos - p.rec.g);
+    }
     const int e0 = __ldg(p.blk_elem + b), e1 = __ldg(p.blk_elem + b + 1);
     const size_t E = (size_t)p.E, ne = (size_t)(e1 - e0);
     if (p.mat.s0) l2_prefetch(p.mat.p0, E * sizeof(T), e0 * sizeof(T), ne * sizeof(T));
@@ -50,7 +57,12 @@ __device__ __forceinline__ void prefetch_record(const AsmParams<T>& p, int b) {
 template <int D, int MODEL, class T, int OP, int ST, bool MASKED, int NT>
 __global__ void __launch_bounds__(NT)
 k_assemble_direct(const AsmParams<T> p) {
-    // shared: ust[NF][OCAP][D][ST] (staged nodal fields) | le[(d+1) EB] u16 | fbuf[NV][EB][D][ST]
+    // shared: ust[NF][OCAP][D][ST] (staged nodal fields) | [le[(d+1) EB] u16] | fbuf
+    // EPOS (fp32): fbuf[(d+1) EB entries][D][ST], element vertex forces scattered to their
+    //   block-CSR entry (ent_pos), so phase 2 reads an occurrence's entries contiguously
+    // !EPOS (fp64): fbuf[NV][EB][D][ST] written conflict-free by consecutive elements, phase 2
+    //   gathers through loc_ent (le, copied to shared memory); fp64 vertex vectors are 24-byte
+    //   and scattered 8-byte stores saturate the shared-memory pipe
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ double s_red[NT / 32][2 * ST + 1];
     constexpr bool HAS_FORCE = OP != OP_ENERGY;
@@ -65,8 +77,10 @@ k_assemble_direct(const AsmParams<T> p) {
     const int EB = p.rec.eb;                                    // record / fbuf stride
     const size_t ust_sz = (size_t)p.rec.ocap * D * ST;
     T* ust = reinterpret_cast<T*>(smem_raw);
+    constexpr bool EPOS = sizeof(T) == 4;
     uint16_t* le = reinterpret_cast<uint16_t*>(ust + NF * ust_sz);
-    T* fbuf = reinterpret_cast<T*>(smem_raw + ((NF * ust_sz * sizeof(T) + 2 * (size_t)NV * EB + 15) & ~size_t(15)));
+    T* fbuf = reinterpret_cast<T*>(smem_raw + ((NF * ust_sz * sizeof(T) + (EPOS ? 0 : 2 * (size_t)NV * EB) + 15) &
+                                               ~size_t(15)));
     const bool cgdot = OP == OP_TANGENT && p.cg != nullptr;
     if (p.cg && ld_relaxed_i(&p.cg->done)) return;
     const int b = blockIdx.x;
@@ -77,8 +91,7 @@ k_assemble_direct(const AsmParams<T> p) {
     const int32_t* socc = reinterpret_cast<const int32_t*>(rg + p.rec.occ_node);
     const uint16_t* soe = reinterpret_cast<const uint16_t*>(rg + p.rec.occ_ent);
     const int32_t* sseg = reinterpret_cast<const int32_t*>(rg + p.rec.occ_seg);
-    // block-local CSR entries -> shared (async, lands by the first barrier)
-    if (HAS_FORCE) {
+    if (!EPOS && HAS_FORCE) {   // block-local CSR entries -> shared (async, lands by the first barrier)
         const int nchunk = (2 * NV * ne + 15) / 16;
         for (int c = tid; c < nchunk; c += NT) cpn<16>(le + 8 * c, rg + p.rec.loc_ent + 16 * c);
     }
@@ -95,7 +108,11 @@ k_assemble_direct(const AsmParams<T> p) {
     double wsum[ST], fsum[ST];
 #pragma unroll
     for (int q = 0; q < ST; ++q) wsum[q] = fsum[q] = 0.0;
-    const LameScale<T> lsc = lame_scale<T>(p.mat);
+    // uniform-nu Lame constants: one thread forms them (two divisions), read after the barrier
+    __shared__ T s_lame[2];
+    LameScale<T> lsc;
+    lsc.on = p.mat.kind != KIND_LAME && p.mat.s1 == 0;
+    if (lsc.on && tid == 0) lame_of<T>(p.mat.kind, T(1), __ldg(p.mat.p1), s_lame[0], s_lame[1]);
     for (int s0 = 0; s0 < S; s0 += ST) {
         const int nq = min(ST, S - s0);
         if (OP == OP_TANGENT) {
@@ -109,19 +126,29 @@ k_assemble_direct(const AsmParams<T> p) {
 #pragma unroll
         for (int q = 0; q < ST; ++q) wacc[q] = T(0);
         cp_wait<0>();
-        __syncthreads();     // staged fields (and loc_ent) visible
+        __syncthreads();     // staged fields, loc_ent and Lame constants visible
+        lsc.mu1 = s_lame[0];
+        lsc.lam1 = s_lame[1];
         // ---------------- phase 1: elements (one per thread and pass)
         for (int el = tid; el < ne; el += NT) {
             const int e = e0 + el;
             Geo<D, T> G;
-            int lv[NV];
+            int lv[NV], ep[NV];   // vertex -> staged occurrence, vertex -> block-CSR entry
             if constexpr (D == 3) {
                 const uint2 c = __ldg(reinterpret_cast<const uint2*>(rg + p.rec.lconn) + el);
                 lv[0] = c.x & 0xffff; lv[1] = c.x >> 16; lv[2] = c.y & 0xffff; lv[3] = c.y >> 16;
+                if (EPOS) {
+                    const uint2 q = __ldg(reinterpret_cast<const uint2*>(rg + p.rec.ent_pos) + el);
+                    ep[0] = q.x & 0xffff; ep[1] = q.x >> 16; ep[2] = q.y & 0xffff; ep[3] = q.y >> 16;
+                }
             } else {
                 const uint16_t* lc = reinterpret_cast<const uint16_t*>(rg + p.rec.lconn) + el * NV;
+                const uint16_t* lp = reinterpret_cast<const uint16_t*>(rg + p.rec.ent_pos) + el * NV;
 #pragma unroll
-                for (int a = 0; a < NV; ++a) lv[a] = __ldg(lc + a);
+                for (int a = 0; a < NV; ++a) {
+                    lv[a] = __ldg(lc + a);
+                    if (EPOS) ep[a] = __ldg(lp + a);
+                }
             }
             {
                 const T* sg = reinterpret_cast<const T*>(rg + p.rec.g);
@@ -180,7 +207,7 @@ k_assemble_direct(const AsmParams<T> p) {
                     for (int a = 0; a < NV; ++a)
 #pragma unroll
                         for (int i = 0; i < D; ++i)
-                            *reinterpret_cast<V*>(fbuf + (((size_t)a * EB + el) * D + i) * ST + qq) = f[a][i];
+                            *reinterpret_cast<V*>(fbuf + ((size_t)(EPOS ? ep[a] : a * EB + el) * D + i) * ST + qq) = f[a][i];
                     if (!HAS_PSI && !isfinite(pfem::lane(f[0][0], 0))) ++n_nonfin;
                 }
             }
@@ -200,9 +227,13 @@ k_assemble_direct(const AsmParams<T> p) {
                     for (int k = 0; k < SD; ++k) accs[k] = T(0);
                     const int k1 = first ? k1_0 : __ldg(soe + oi + 1);
                     for (int k = first ? kb_0 : __ldg(soe + oi); k < k1; ++k) {
-                        const int j = le[k];
-                        const int el = j / NV, a = j - el * NV;
-                        sacc<T, SD>(fbuf + ((size_t)a * EB + el) * SD, accs);
+                        int slot = k;
+                        if (!EPOS) {
+                            const int j = le[k];
+                            const int el = j / NV, a = j - el * NV;
+                            slot = a * EB + el;
+                        }
+                        sacc<T, SD>(fbuf + (size_t)slot * SD, accs);
                     }
                     if (word & (OCC_NONOWNER | OCC_EARLIER)) {
                         const int slot = first ? sl_0 : __ldg(sseg + oi);

@@ -45,10 +45,11 @@ constexpr int32_t OCC_EARLIER = 0x20000000;    // owner, and earlier blocks hold
 //   occ_ent [OCAP+1] uint16 (block-relative entry offsets) | loc_ent [(d+1) EB] uint16 |
 //   lconn [EB][d+1] uint16 (block-local occurrence index of each element vertex) |
 //   occ_seg [OCAP] int32 (node-major segment slot of a multi-block node's occurrence, -1 if
-//   the node is finished inside the block)
+//   the node is finished inside the block) | ent_pos [EB][d+1] uint16 (inverse of loc_ent:
+//   the block-CSR entry of each element vertex)
 struct RecLayout {
     int eb = 0, ocap = 0;
-    uint32_t conn = 0, g = 0, vol = 0, occ_node = 0, occ_ent = 0, loc_ent = 0, lconn = 0, occ_seg = 0, bytes = 0;
+    uint32_t conn = 0, g = 0, vol = 0, occ_node = 0, occ_ent = 0, loc_ent = 0, lconn = 0, occ_seg = 0, ent_pos = 0, bytes = 0;
 };
 
 inline RecLayout rec_layout(int D, size_t tsize, int eb, int ocap) {
@@ -65,6 +66,7 @@ inline RecLayout rec_layout(int D, size_t tsize, int eb, int ocap) {
     L.loc_ent = take(2 * (size_t)(D + 1) * eb);
     L.lconn = take(2 * (size_t)(D + 1) * eb);
     L.occ_seg = take(4 * (size_t)ocap);
+    L.ent_pos = take(2 * (size_t)(D + 1) * eb);
     L.bytes = (uint32_t)o;
     return L;
 }

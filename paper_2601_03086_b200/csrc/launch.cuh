@@ -100,12 +100,15 @@ AsmParams<T> make_params(const Call& c) {
     return p;
 }
 
+template <class T>
+constexpr int direct_nt() { return sizeof(T) == 4 ? 128 : 256; }   // direct kernel threads per CTA (measured)
+
 template <int D, int MODEL, class T, int OP, int ST, bool MASKED, int NT>
 pfem_status launch_direct(AsmParams<T> p, cudaStream_t s) {
     constexpr bool HAS_FORCE = OP != OP_ENERGY;
     constexpr int NFd = (OP == OP_TANGENT && MODEL == MODEL_NH) ? 2 : 1;
-    const size_t smem = ((NFd * (size_t)p.rec.ocap * D * ST * sizeof(T) + 2 * (size_t)(D + 1) * p.rec.eb + 15) &
-                         ~size_t(15)) +
+    const size_t smem = ((NFd * (size_t)p.rec.ocap * D * ST * sizeof(T) + (sizeof(T) == 4 ? 0 : 2 * (size_t)(D + 1) * p.rec.eb) +
+                          15) & ~size_t(15)) +
                         (HAS_FORCE ? (size_t)ST * D * (D + 1) * p.rec.eb * sizeof(T) : 0);
     auto kd = k_assemble_direct<D, MODEL, T, OP, ST, MASKED, NT>;
     static size_t configured = 0;
@@ -165,7 +168,7 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
     // PFEM_VARIANT=0/1 forces staged/direct (measurement switch).
     const bool direct = variant >= 0 ? variant == 1 : p.S == 1;
     if (direct) {
-        const pfem_status st = launch_direct<D, MODEL, T, OP, ST, MASKED, NT>(p, s);
+        const pfem_status st = launch_direct<D, MODEL, T, OP, ST, MASKED, direct_nt<T>()>(p, s);
         if (st != PFEM_OK) return st;
     } else {
         const int grid = std::max(1, std::min(resident, p.n_blocks));

@@ -389,8 +389,12 @@ __global__ void k_pack_records(int E, const int32_t* __restrict__ blk_elem, cons
     for (int i = threadIdx.x; i < L.ocap; i += blockDim.x) ros[i] = i < no ? occ_seg[o0 + i] : -1;
     for (int i = threadIdx.x; i <= L.ocap; i += blockDim.x)
         roe[i] = (uint16_t)(i <= no ? occ_ent_ptr[o0 + i] - NV * e0 : NV * ne);
-    for (int k = threadIdx.x; k < NV * L.eb; k += blockDim.x)
+    uint16_t* rep = reinterpret_cast<uint16_t*>(r + L.ent_pos);
+    for (int k = threadIdx.x; k < NV * L.eb; k += blockDim.x) {
         rle[k] = k < NV * ne ? loc_ent[(int64_t)NV * e0 + k] : (uint16_t)0;
+        if (k < NV * ne) rep[loc_ent[(int64_t)NV * e0 + k]] = (uint16_t)k;   // a permutation of [0, NV ne)
+        else rep[k] = (uint16_t)k;
+    }
     // local occurrence index of each element vertex: binary search in the block's sorted nodes
     uint16_t* rlc = reinterpret_cast<uint16_t*>(r + L.lconn);
     for (int k = threadIdx.x; k < NV * L.eb; k += blockDim.x) {
