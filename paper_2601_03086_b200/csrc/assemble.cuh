@@ -97,6 +97,7 @@ struct AsmParams {
     int32_t* fix_flag;     // [n_blocks] fix-up of block done (CG dot)
     int32_t* chunk_flag;   // [n_chunks] chunk reduced
     double* chunk_sum;     // [2S+1][n_chunks]
+    int32_t* part_cnt;     // [K] reduced chunks per part (0 at rest)
     T* partial;            // [n_occ][S][D]
     CgState* cg;           // non-null: fused p.q and alpha epilogue (S == 1)
 };
@@ -133,6 +134,20 @@ __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
+}
+
+// fixed-order lane-strided sum of a[lo, hi): lane l adds a[lo+l], a[lo+l+32], ... in ascending
+// order, the loads issued 8 at a time (a plain strided loop waits one latency per element)
+__device__ __forceinline__ double lane_sum(const double* a, int lo, int hi, int lane) {
+    double acc = 0.0;
+    for (int c0 = lo + lane; c0 < hi; c0 += 32 * 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = c0 + 32 * u < hi ? __ldcg(a + c0 + 32 * u) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += v[u];
+    }
+    return acc;
 }
 
 // vector load / store of N contiguous T in shared memory (N*sizeof(T) in {4..48} bytes)
@@ -703,6 +718,9 @@ k_node_finish(const AsmParams<T> p, int op_psi, int n_items) {
     // ---------------- chunk reductions of the per-block sums (one chunk per CTA)
     const int rb = op_psi ? 0 : 2 * S;
     const int re = cgdot ? 2 * S + 1 : (op_psi ? 2 * S : 2 * S);
+    // The CTA completing the last chunk of a part forms that part's totals (parts finish in
+    // parallel; fixed order: blocks within a chunk, chunks within the part)
+    const bool part_totals = op_psi && p.totals;
     for (int ch = blockIdx.x; ch < p.n_chunks; ch += gridDim.x) {
         const int c0 = __ldg(p.chunk_blk + ch), c1 = __ldg(p.chunk_blk + ch + 1);
         for (int r = rb + warp; r < re; r += NTB / 32) {
@@ -710,6 +728,32 @@ k_node_finish(const AsmParams<T> p, int op_psi, int n_items) {
             v = warp_sum(v);
             if (lane == 0) p.chunk_sum[(int64_t)r * p.n_chunks + ch] = v;
         }
+        if (!part_totals) continue;
+        __syncthreads();
+        if (tid == 0) {
+            int lo = 0, hi = p.K - 1;   // part of chunk ch: last k with part_chunk[k] <= ch
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (__ldg(p.part_chunk + mid) <= ch) lo = mid;
+                else hi = mid - 1;
+            }
+            const int cb = __ldg(p.part_chunk + lo), ce = __ldg(p.part_chunk + lo + 1);
+            __threadfence();
+            s_last = atomicAdd(p.part_cnt + lo, 1) == ce - cb - 1 ? lo : -1;
+        }
+        __syncthreads();
+        const int k = s_last;
+        if (k >= 0) {
+            __threadfence();
+            const int cb = __ldg(p.part_chunk + k), ce = __ldg(p.part_chunk + k + 1);
+            for (int s = warp; s < S; s += NTB / 32) {
+                const double wv = warp_sum(lane_sum(p.chunk_sum + (int64_t)s * p.n_chunks, cb, ce, lane));
+                const double fv = warp_sum(lane_sum(p.chunk_sum + (int64_t)(S + s) * p.n_chunks, cb, ce, lane));
+                if (lane == 0) p.totals[(int64_t)s * p.K + k] = (T)(wv - fv);
+            }
+            if (tid == 0) p.part_cnt[k] = 0;
+        }
+        __syncthreads();   // s_last reused
     }
     if (cgdot) {
         const double t = cta_sum<NTB>(dot_acc, s_red);
@@ -724,26 +768,9 @@ k_node_finish(const AsmParams<T> p, int op_psi, int n_items) {
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    if (op_psi && p.totals) {
-        for (int pair = warp; pair < S * p.K; pair += NTB / 32) {
-            const int s = pair / p.K, k = pair - s * p.K;
-            const int cb = __ldg(p.part_chunk + k), ce = __ldg(p.part_chunk + k + 1);
-            double wv = 0.0, fv = 0.0;
-            for (int cc = cb + lane; cc < ce; cc += 32) {
-                wv += __ldcg(p.chunk_sum + (int64_t)s * p.n_chunks + cc);
-                fv += __ldcg(p.chunk_sum + (int64_t)(S + s) * p.n_chunks + cc);
-            }
-            wv = warp_sum(wv);
-            fv = warp_sum(fv);
-            if (lane == 0) p.totals[(int64_t)s * p.K + k] = (T)(wv - fv);
-        }
-    }
     if (cgdot && warp == 0) {
-        double pq = 0.0;
-        for (int cc = lane; cc < p.n_chunks; cc += 32) pq += __ldcg(p.chunk_sum + (int64_t)(2 * S) * p.n_chunks + cc);
-        double pb = 0.0;
-        for (int cc = lane; cc < (int)gridDim.x; cc += 32) pb += __ldcg(p.blk_sum + (int64_t)(2 * S + 1) * p.n_blocks + cc);
-        pq = warp_sum(pq) + warp_sum(pb);
+        const double pq = warp_sum(lane_sum(p.chunk_sum + (int64_t)(2 * S) * p.n_chunks, 0, p.n_chunks, lane)) +
+                          warp_sum(lane_sum(p.blk_sum + (int64_t)(2 * S + 1) * p.n_blocks, 0, (int)gridDim.x, lane));
         if (lane == 0) {
             CgState* cg = p.cg;
             cg->pq = pq;

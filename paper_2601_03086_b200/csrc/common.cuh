@@ -123,7 +123,7 @@ struct Counters {
 };
 
 struct WsLayout {
-    size_t counters, flags, fix_flags, blk_sum, chunk_flags, chunk_sum, partial, wtmp, total;
+    size_t counters, flags, fix_flags, blk_sum, chunk_flags, chunk_sum, partial, wtmp, part_cnt, total;
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -139,6 +139,7 @@ inline WsLayout ws_layout(const Plan& p, int S, size_t tsize) {
     L.chunk_sum = o;  o += align_up(sizeof(double) * (2 * (size_t)S + 1) * (p.n_chunks + 1), 256);
     L.partial = o;  o += align_up(tsize * (size_t)S * std::max(p.n_seg, 1) * p.dim, 256);
     L.wtmp = o;     o += align_up(tsize * (size_t)S * p.n_elems, 256);
+    L.part_cnt = o; o += align_up(sizeof(int32_t) * (size_t)(p.n_parts + 1), 256);   // reduced chunks per part
     L.total = o;
     return L;
 }

@@ -94,6 +94,7 @@ AsmParams<T> make_params(const Call& c) {
     p.chunk_flag = (int32_t*)(w + L.chunk_flags);
     p.chunk_sum = (double*)(w + L.chunk_sum);
     p.partial = (T*)(w + L.partial);
+    p.part_cnt = (int32_t*)(w + L.part_cnt);
     p.cg = c.cg;
     p.dbg = 0;
     p.lag = 0;
@@ -180,7 +181,18 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
     const int nsc = (p.S + ST - 1) / ST;
     const int n_items = HAS_FORCE ? P_nfix(p) * nsc : 0;
     int gridb = std::max({1, (n_items + NTB - 1) / NTB, 0});
-    gridb = std::max(1, std::min(gridb, std::min(p.n_blocks, 4096)));
+    // few CTAs, grid-stride: every CTA ends with one atomic on the shared exit counter, and
+    // thousands of same-address atomics serialise into a tail that idles the GPU
+    static int cap_b = 0;
+    if (cap_b == 0) {
+        int dev = 0, nsm = 0;
+        PFEM_CUDA_TRY(cudaGetDevice(&dev));
+        PFEM_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        const char* env = getenv("PFEM_GRIDB");
+        cap_b = env ? std::max(1, atoi(env)) : 8 * nsm;
+    }
+    gridb = std::max(1, std::min(gridb, std::min(p.n_blocks, cap_b)));
+    if (dbg & 32) return PFEM_OK;   // measurement switch: kernel A alone (results incomplete)
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(gridb);
     cfg.blockDim = dim3(NTB);
@@ -190,8 +202,9 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    PFEM_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_node_finish<D, T, ST, MASKED, NTB>, p, HAS_PSI ? 1 : 0, n_items));
+    cfg.numAttrs = (dbg & 128) ? 0 : 1;   // measurement switch: plain stream order instead of PDL
+    PFEM_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_node_finish<D, T, ST, MASKED, NTB>, p, HAS_PSI ? 1 : 0,
+                                     (dbg & 64) ? 0 : n_items));
     count_launch();
     return PFEM_OK;
 }
