@@ -245,22 +245,23 @@ __device__ __forceinline__ void ld_relaxed_vec(const T* p, T* v) {
     for (int k = 0; k < N; ++k) v[k] = ld_relaxed(p + k);
 }
 
-// L2 (coherent) loads of n <= N contiguous values; segments are published with release
-// and observed through a relaxed flag load before these loads are issued
+// loads of n <= N contiguous values of the segment buffer (written by the previous grid,
+// read-only here: the non-coherent path may cache them in L1, where the d components of
+// neighbouring segments share sectors)
 template <class T, int N>
-__device__ __forceinline__ void ld_cg_vec(const T* p, T (&v)[N], int n) {
+__device__ __forceinline__ void ld_seg_vec(const T* p, T (&v)[N], int n) {
     if constexpr (sizeof(T) == 4 && N % 4 == 0) {
         if (n == N && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
 #pragma unroll
             for (int k = 0; k < N / 4; ++k) {
-                const float4 q = __ldcg(reinterpret_cast<const float4*>(p) + k);
+                const float4 q = __ldg(reinterpret_cast<const float4*>(p) + k);
                 v[4 * k] = q.x; v[4 * k + 1] = q.y; v[4 * k + 2] = q.z; v[4 * k + 3] = q.w;
             }
             return;
         }
     }
 #pragma unroll
-    for (int k = 0; k < N; ++k) v[k] = k < n ? __ldcg(p + k) : T(0);
+    for (int k = 0; k < N; ++k) v[k] = k < n ? __ldg(p + k) : T(0);
 }
 
 // stage block b: one bulk copy of its packed record (thread 0) + per-element material
@@ -695,10 +696,10 @@ k_node_finish(const AsmParams<T> p, int op_psi, int n_items) {
         const int k0 = __ldg(p.fix_src_ptr + f), k1 = __ldg(p.fix_src_ptr + f + 1);
         // the node's segments are contiguous: seg[k][s][d], k in [k0, k1) (ascending block)
         T acc[SD];
-        ld_cg_vec<T, SD>(p.partial + ((int64_t)k0 * S + s0) * D, acc, nq * D);
+        ld_seg_vec<T, SD>(p.partial + ((int64_t)k0 * S + s0) * D, acc, nq * D);
         for (int k = k0 + 1; k < k1; ++k) {
             T v[SD];
-            ld_cg_vec<T, SD>(p.partial + ((int64_t)k * S + s0) * D, v, nq * D);
+            ld_seg_vec<T, SD>(p.partial + ((int64_t)k * S + s0) * D, v, nq * D);
 #pragma unroll
             for (int c = 0; c < SD; ++c) acc[c] += v[c];
         }
