@@ -54,8 +54,16 @@ __device__ __forceinline__ void prefetch_record(const AsmParams<T>& p, int b) {
     if (p.mat.s1) l2_prefetch(p.mat.p1, E * sizeof(T), e0 * sizeof(T), ne * sizeof(T));
 }
 
+#ifndef PFEM_DIRECT_MINB1
+#define PFEM_DIRECT_MINB1 (65536 / (NT * 64))
+#endif
+#ifndef PFEM_DIRECT_MINBS
+#define PFEM_DIRECT_MINBS 6
+#endif
+// register budget (minimum resident CTAs): single-sample calls 64 registers, several-sample
+// fp32 calls 80 (measured; the compiler's default allocation is larger and costs occupancy)
 template <int D, int MODEL, class T, int OP, int ST, bool MASKED, int NT>
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NT, ST > 1 ? PFEM_DIRECT_MINBS : PFEM_DIRECT_MINB1)
 k_assemble_direct(const AsmParams<T> p) {
     // shared: ust[NF][OCAP][D][ST] (staged nodal fields) | [le[(d+1) EB] u16] | fbuf
     // EPOS (fp32): fbuf[(d+1) EB entries][D][ST], element vertex forces scattered to their

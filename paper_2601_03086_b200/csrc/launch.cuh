@@ -212,6 +212,8 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
 template <int D, int MODEL, class T, int OP, bool MASKED>
 pfem_status dispatch_st(const AsmParams<T>& p, cudaStream_t s) {
     constexpr int STBIG = sizeof(T) == 4 ? 4 : 2;
+    static const int st_env = getenv("PFEM_ST") ? atoi(getenv("PFEM_ST")) : 0;   // measurement switch
+    if (p.S > 1 && st_env == 2 && sizeof(T) == 4) return launch_csr<D, MODEL, T, OP, 2, MASKED>(p, s);
     if (p.S > 1) return launch_csr<D, MODEL, T, OP, STBIG, MASKED>(p, s);
     return launch_csr<D, MODEL, T, OP, 1, MASKED>(p, s);
 }
