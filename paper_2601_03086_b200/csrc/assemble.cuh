@@ -31,6 +31,13 @@
 #include "common.cuh"
 #include "element.cuh"
 
+#ifndef PFEM_STAGED_MINB
+#define PFEM_STAGED_MINB 2
+#endif
+#ifndef PFEM_STAGED_SCALAR
+#define PFEM_STAGED_SCALAR 0
+#endif
+
 namespace pfem {
 
 enum { OP_ENERGY = 0, OP_ENERGY_RESIDUAL = 1, OP_RESIDUAL = 2, OP_TANGENT = 3 };
@@ -379,7 +386,7 @@ __device__ __forceinline__ void stage_fields(T* ust, const unsigned char* rec, c
 }
 
 template <int D, int MODEL, class T, int OP, int ST, bool MASKED, int EB, int NT>
-__global__ void __launch_bounds__(NT, 2)
+__global__ void __launch_bounds__(NT, PFEM_STAGED_MINB)
 k_assemble(const AsmParams<T> p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr bool HAS_FORCE = OP != OP_ENERGY;
@@ -387,7 +394,7 @@ k_assemble(const AsmParams<T> p) {
     constexpr int NV = D + 1;
     constexpr int SD = ST * D;
     constexpr int NF = 1;    // staged field: u (energy / residual) or v (tangent; the NH state u is gathered)
-    using V = std::conditional_t<(sizeof(T) == 4 && ST % 2 == 0), F2, T>;
+    using V = std::conditional_t<(sizeof(T) == 4 && ST % 2 == 0 && !PFEM_STAGED_SCALAR), F2, T>;
     constexpr int L = VTraits<V>::L;
     using A2 = std::conditional_t<(sizeof(T) == 4 && SD % 2 == 0), F2, T>;     // phase-2 accumulator
     constexpr int LA = VTraits<A2>::L;

@@ -57,6 +57,9 @@ __device__ __forceinline__ void prefetch_record(const AsmParams<T>& p, int b) {
 #ifndef PFEM_DIRECT_MINB1
 #define PFEM_DIRECT_MINB1 (65536 / (NT * 64))
 #endif
+#ifndef PFEM_DIRECT_SCALAR
+#define PFEM_DIRECT_SCALAR 0
+#endif
 #ifndef PFEM_DIRECT_MINBS
 #define PFEM_DIRECT_MINBS 6
 #endif
@@ -78,7 +81,7 @@ k_assemble_direct(const AsmParams<T> p) {
     constexpr int NV = D + 1;
     constexpr int SD = ST * D;
     constexpr int NF = (OP == OP_TANGENT && MODEL == MODEL_NH) ? 2 : 1;   // NH tangent stages u and v
-    using V = std::conditional_t<(sizeof(T) == 4 && ST % 2 == 0), F2, T>;
+    using V = std::conditional_t<(sizeof(T) == 4 && ST % 2 == 0 && !PFEM_DIRECT_SCALAR), F2, T>;
     constexpr int L = VTraits<V>::L;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int S = p.S;
