@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define PFEM_ABI_VERSION 1
+#define PFEM_ABI_VERSION 2
 
 typedef enum {
     PFEM_OK = 0,
@@ -79,6 +79,13 @@ typedef enum {
                                  (element, slot)                                              */
 } pfem_assembly;
 
+typedef enum {
+    PFEM_ORDER_INPUT = 0,          /* blocks of consecutive input elements                      */
+    PFEM_ORDER_LOCALITY = 1,       /* blocks of consecutive elements in Morton order of their
+                                      centroids, inside each part (fewer nodes shared by blocks) */
+    PFEM_ORDER_AUTO = 2            /* whichever of the two gives fewer (block, node) occurrences  */
+} pfem_elem_order;
+
 typedef struct pfem_plan pfem_plan;   /* opaque, library-owned device data */
 
 /* Mesh descriptor.  Inputs are set by the caller; pfem_mesh_prepare fills the outputs. */
@@ -89,6 +96,9 @@ typedef struct {
     int32_t n_parts;               /* >= 1: independent meshes concatenated (config 5)          */
     int32_t dtype;                 /* pfem_dtype of grad / vol and of every field call          */
     int32_t block_elems;           /* assembly block size (elements); 0 = library default       */
+    int32_t elem_order;            /* assembly element order (pfem_elem_order): the plan may visit
+                                      elements in a locality order; results are unchanged up to
+                                      rounding and are reported in input element order           */
     const double* coords;          /* [n_nodes][dim], float64 always                             */
     const int32_t* conn;           /* [n_elems][dim+1], node ids in [0, n_nodes)                 */
     const int32_t* part_elem;      /* [n_parts+1] element offsets (device), NULL if n_parts == 1 */
@@ -145,10 +155,12 @@ pfem_status pfem_mesh_prepare(pfem_mesh* m, void* stream);
 void pfem_mesh_release(pfem_mesh* m);
 
 /* Device copies of the plan arrays, for tests (host pointers to fill, each may be NULL).
- * Sizes: blk_elem [n_blocks+1], blk_occ [n_blocks+1], occ_node [n_occ] (node id | kind
- * bits 30..31), occ_ent_ptr [n_occ+1], loc_ent [(dim+1)*n_elems] (uint16). */
+ * Sizes: blk_elem [n_blocks+1] (plan positions), blk_occ [n_blocks+1], occ_node [n_occ]
+ * (node id | kind bits 29..30), occ_ent_ptr [n_occ+1], loc_ent [(dim+1)*n_elems] (uint16),
+ * elem_perm [n_elems] (position -> input element id). */
 pfem_status pfem_plan_export(const pfem_mesh* m, int32_t* blk_elem, int32_t* blk_occ,
-                             int32_t* occ_node, int32_t* occ_ent_ptr, uint16_t* loc_ent);
+                             int32_t* occ_node, int32_t* occ_ent_ptr, uint16_t* loc_ent,
+                             int32_t* elem_perm);
 
 /* Bytes of the per-call workspace of pfem_energy / pfem_residual / pfem_tangent_apply
  * for `n_samples` fields.  The workspace must be ZERO-FILLED before its first use; the

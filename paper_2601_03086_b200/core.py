@@ -38,7 +38,8 @@ class Mesh:
     """A prepared mesh (pfem_mesh_prepare): geometry, CSR, colouring and assembly plan."""
 
     def __init__(self, coords: torch.Tensor, conn: torch.Tensor, dtype=torch.float64, part_elem=None,
-                 part_node=None, block_elems: int = 0, max_colours: int = 128, stream=None):
+                 part_node=None, block_elems: int = 0, max_colours: int = 128, stream=None,
+                 elem_order: str = "auto"):
         lib = L.load()
         _require_cuda(coords, conn)
         dev = coords.device
@@ -68,6 +69,7 @@ class Mesh:
         m.dim, m.n_nodes, m.n_elems, m.n_parts = d, N, E, K
         m.dtype = _DT[dtype]
         m.block_elems = block_elems
+        m.elem_order = {"input": 0, "locality": 1, "auto": 2}[elem_order]
         m.coords, m.conn = self.coords.data_ptr(), self.conn.data_ptr()
         m.part_elem = self.part_elem.data_ptr() if self.part_elem is not None else None
         m.part_node = self.part_node.data_ptr() if self.part_node is not None else None
@@ -126,10 +128,11 @@ class Mesh:
         on = np.zeros(no, np.int32)
         oe = np.zeros(no + 1, np.int32)
         le = np.zeros(self.n_elems * (self.dim + 1), np.uint16)
+        pm = np.zeros(self.n_elems, np.int32)
         torch.cuda.synchronize()
         L.check(L.load().pfem_plan_export(self.ref(), be.ctypes.data, bo.ctypes.data, on.ctypes.data,
-                                          oe.ctypes.data, le.ctypes.data))
-        return {"blk_elem": be, "blk_occ": bo, "occ_node": on, "occ_ent_ptr": oe, "loc_ent": le}
+                                          oe.ctypes.data, le.ctypes.data, pm.ctypes.data))
+        return {"blk_elem": be, "blk_occ": bo, "occ_node": on, "occ_ent_ptr": oe, "loc_ent": le, "elem_perm": pm}
 
     def release(self):
         if getattr(self, "_m", None) is not None and self._m.plan:

@@ -118,6 +118,7 @@ pfem_status pfem_mesh_prepare(pfem_mesh* m, void* stream) {
     if ((int64_t)m->n_elems * (m->dim + 1) >= INT32_MAX) { set_error("too many elements"); return PFEM_ERR_ARG; }
     if (m->max_colours < 1 || m->max_colours > 128) { set_error("max_colours must be in [1, 128]"); return PFEM_ERR_ARG; }
     if (m->block_elems < 0) { set_error("block_elems must be >= 0"); return PFEM_ERR_ARG; }
+    if (m->elem_order < 0 || m->elem_order > 2) { set_error("elem_order must be 0, 1 or 2"); return PFEM_ERR_ARG; }
     if (m->dim == 3 && ((uintptr_t)m->conn & 15)) { set_error("conn must be 16-byte aligned for dim 3"); return PFEM_ERR_ARG; }
     if (m->plan) release_impl(m);
     return prepare_impl(m, (cudaStream_t)stream);
@@ -126,7 +127,7 @@ pfem_status pfem_mesh_prepare(pfem_mesh* m, void* stream) {
 void pfem_mesh_release(pfem_mesh* m) { release_impl(m); }
 
 pfem_status pfem_plan_export(const pfem_mesh* m, int32_t* blk_elem, int32_t* blk_occ, int32_t* occ_node,
-                             int32_t* occ_ent_ptr, uint16_t* loc_ent) {
+                             int32_t* occ_ent_ptr, uint16_t* loc_ent, int32_t* elem_perm) {
     pfem_status st = check_mesh(m, true);
     if (st) return st;
     const Plan* P = reinterpret_cast<const Plan*>(m->plan);
@@ -137,6 +138,13 @@ pfem_status pfem_plan_export(const pfem_mesh* m, int32_t* blk_elem, int32_t* blk
     if (occ_ent_ptr && e == cudaSuccess) e = cudaMemcpy(occ_ent_ptr, P->occ_ent_ptr, sizeof(int32_t) * (P->n_occ + 1), cudaMemcpyDeviceToHost);
     if (loc_ent && e == cudaSuccess)
         e = cudaMemcpy(loc_ent, P->loc_ent, sizeof(uint16_t) * (size_t)P->n_elems * (P->dim + 1), cudaMemcpyDeviceToHost);
+    if (elem_perm && e == cudaSuccess) {
+        if (P->elem_perm) {
+            e = cudaMemcpy(elem_perm, P->elem_perm, sizeof(int32_t) * (size_t)P->n_elems, cudaMemcpyDeviceToHost);
+        } else {
+            for (int32_t i = 0; i < P->n_elems; ++i) elem_perm[i] = i;
+        }
+    }
     if (e != cudaSuccess) return cuda_status(e, "pfem_plan_export");
     return PFEM_OK;
 }

@@ -95,6 +95,7 @@ struct AsmParams {
     const int32_t* fix_src;
     const int32_t* occ_seg;   // [n_occ] segment slot of a multi-block occurrence
     int n_fix;
+    int perm;              // plan positions are a permutation of the input elements
     RecLayout rec;
     const unsigned char* recs;
     // workspace
@@ -280,14 +281,19 @@ __device__ __forceinline__ void stage_block(unsigned char* st, T* mst, uint64_t*
         mbar_expect_tx(bar, p.rec.bytes);
         tma_bulk_g2s(st, p.recs + (size_t)b * p.rec.bytes, p.rec.bytes, bar);
     }
-    if (p.mat.s0 | p.mat.s1) {
-        const int e0 = __ldg(p.blk_elem + b), ne = __ldg(p.blk_elem + b + 1) - e0;
-        for (int el = threadIdx.x; el < ne; el += NT) {
-            if (p.mat.s0) cpn<sizeof(T)>(mst + el, p.mat.p0 + (int64_t)(e0 + el) * p.mat.s0);
-            if (p.mat.s1) cpn<sizeof(T)>(mst + p.rec.eb + el, p.mat.p1 + (int64_t)(e0 + el) * p.mat.s1);
-        }
+    cp_commit();   // (empty group: keeps the one-group-per-stage accounting of cp_wait)
+}
+
+// element-wise material of a block whose record has landed in shared memory: cp.async by
+// input element id (the plan may visit elements in a locality order)
+template <class T, int NT>
+__device__ __forceinline__ void stage_material(T* mst, const unsigned char* rec, const AsmParams<T>& p, int ne) {
+    const int32_t* eid = reinterpret_cast<const int32_t*>(rec + p.rec.eid);
+    for (int el = threadIdx.x; el < ne; el += NT) {
+        const int64_t e = eid[el];
+        if (p.mat.s0) cpn<sizeof(T)>(mst + el, p.mat.p0 + e * p.mat.s0);
+        if (p.mat.s1) cpn<sizeof(T)>(mst + p.rec.eb + el, p.mat.p1 + e * p.mat.s1);
     }
-    cp_commit();
 }
 
 // =====================================================================================
@@ -426,12 +432,15 @@ k_assemble(const AsmParams<T> p) {
     int t = blockIdx.x;
     uint32_t par0 = 0u, par1 = 0u;   // mbarrier phase of each record buffer (registers, no arrays)
     // prologue: record of the first block, then its fields
+    const bool has_mat = (p.mat.s0 | p.mat.s1) != 0;
     if (t < p.n_blocks) {
         stage_block<D, T, NT>(stage0, mstage, &s_bar[0], p, t);
-        if (pref) {
+        if (pref || has_mat) {
             mbar_wait(&s_bar[0], 0);
-            stage_fields<D, T, NT, ST, MASKED>(ustage, stage0, staged_src, p, 0, S,
-                                               __ldg(p.blk_occ + t + 1) - __ldg(p.blk_occ + t));
+            if (pref)
+                stage_fields<D, T, NT, ST, MASKED>(ustage, stage0, staged_src, p, 0, S,
+                                                   __ldg(p.blk_occ + t + 1) - __ldg(p.blk_occ + t));
+            if (has_mat) stage_material<T, NT>(mstage, stage0, p, __ldg(p.blk_elem + t + 1) - __ldg(p.blk_elem + t));
         }
         cp_commit();
     }
@@ -455,6 +464,7 @@ k_assemble(const AsmParams<T> p) {
         const uint16_t* sle = reinterpret_cast<const uint16_t*>(sg + p.rec.loc_ent);
         const uint16_t* slc = reinterpret_cast<const uint16_t*>(sg + p.rec.lconn);
         const int32_t* sseg = reinterpret_cast<const int32_t*>(sg + p.rec.occ_seg);
+        const int32_t* seid = reinterpret_cast<const int32_t*>(sg + p.rec.eid);
         const T* smat = mstage + 2 * EB * cur;
         const T* ust = ustage + ust_sz * cur;
         mbar_wait(&s_bar[cur], cur ? par1 : par0);   // this block's record
@@ -472,7 +482,7 @@ k_assemble(const AsmParams<T> p) {
 #pragma unroll
             for (int q = 0; q < ST; ++q) wacc[q] = T(0);
             for (int el = tid; el < ne; el += NT) {
-                const int e = e0 + el;
+                const int e = seid[el];   // input element id (W_e, flags)
                 Geo<D, T> G_;
                 if constexpr (D == 3) {
                     const int4 cv = *reinterpret_cast<const int4*>(sconn + el * 4);
@@ -552,10 +562,14 @@ k_assemble(const AsmParams<T> p) {
             for (int q = 0; q < ST; ++q) wsum[q] += (double)wacc[q];   // per-thread, fixed order
             // the next block's fields: its record has had phase 1 to land
             if (s0 + ST >= S) {
-                if (pref && tn < p.n_blocks) {
+                if ((pref || has_mat) && tn < p.n_blocks) {
                     mbar_wait(&s_bar[cur ^ 1], cur ? par0 : par1);
-                    stage_fields<D, T, NT, ST, MASKED>(ustage + ust_sz * (cur ^ 1), sg_nxt, staged_src, p, 0, S,
-                                                       __ldg(p.blk_occ + tn + 1) - __ldg(p.blk_occ + tn));
+                    if (pref)
+                        stage_fields<D, T, NT, ST, MASKED>(ustage + ust_sz * (cur ^ 1), sg_nxt, staged_src, p, 0, S,
+                                                           __ldg(p.blk_occ + tn + 1) - __ldg(p.blk_occ + tn));
+                    if (has_mat)
+                        stage_material<T, NT>(mstage + 2 * EB * (cur ^ 1), sg_nxt, p,
+                                              __ldg(p.blk_elem + tn + 1) - __ldg(p.blk_elem + tn));
                 }
                 cp_commit();
             }

@@ -50,6 +50,7 @@ __device__ __forceinline__ void prefetch_record(const AsmParams<T>& p, int b) {
     }
     const int e0 = __ldg(p.blk_elem + b), e1 = __ldg(p.blk_elem + b + 1);
     const size_t E = (size_t)p.E, ne = (size_t)(e1 - e0);
+    if (p.perm) return;   // element-wise materials are gathered through the permutation
     if (p.mat.s0) l2_prefetch(p.mat.p0, E * sizeof(T), e0 * sizeof(T), ne * sizeof(T));
     if (p.mat.s1) l2_prefetch(p.mat.p1, E * sizeof(T), e0 * sizeof(T), ne * sizeof(T));
 }
@@ -142,7 +143,7 @@ k_assemble_direct(const AsmParams<T> p) {
         lsc.lam1 = s_lame[1];
         // ---------------- phase 1: elements (one per thread and pass)
         for (int el = tid; el < ne; el += NT) {
-            const int e = e0 + el;
+            const int e = __ldg(reinterpret_cast<const int32_t*>(rg + p.rec.eid) + el);   // input element id
             Geo<D, T> G;
             int lv[NV], ep[NV];   // vertex -> staged occurrence, vertex -> block-CSR entry
             if constexpr (D == 3) {

@@ -41,7 +41,8 @@ constexpr int32_t OCC_EARLIER = 0x20000000;    // owner, and earlier blocks hold
 // The plan keeps, per element block, one contiguous 16-byte-aligned record holding
 // everything phase 1 and phase 2 read from HBM about the block, so a single TMA bulk copy
 // (cp.async.bulk) stages it into shared memory:
-//   conn [EB][d+1] int32 | grad [d*d][EB] T | vol [EB] T | occ_node [OCAP] int32 |
+//   conn [EB][d+1] int32 | grad [d*d][EB] T | vol [EB] T | eid [EB] int32 (input element id
+//   of each position: the plan may order elements for locality) | occ_node [OCAP] int32 |
 //   occ_ent [OCAP+1] uint16 (block-relative entry offsets) | loc_ent [(d+1) EB] uint16 |
 //   lconn [EB][d+1] uint16 (block-local occurrence index of each element vertex) |
 //   occ_seg [OCAP] int32 (node-major segment slot of a multi-block node's occurrence, -1 if
@@ -49,7 +50,7 @@ constexpr int32_t OCC_EARLIER = 0x20000000;    // owner, and earlier blocks hold
 //   the block-CSR entry of each element vertex)
 struct RecLayout {
     int eb = 0, ocap = 0;
-    uint32_t conn = 0, g = 0, vol = 0, occ_node = 0, occ_ent = 0, loc_ent = 0, lconn = 0, occ_seg = 0, ent_pos = 0, bytes = 0;
+    uint32_t conn = 0, g = 0, vol = 0, eid = 0, occ_node = 0, occ_ent = 0, loc_ent = 0, lconn = 0, occ_seg = 0, ent_pos = 0, bytes = 0;
 };
 
 inline RecLayout rec_layout(int D, size_t tsize, int eb, int ocap) {
@@ -61,6 +62,7 @@ inline RecLayout rec_layout(int D, size_t tsize, int eb, int ocap) {
     L.conn = take(4 * (size_t)(D + 1) * eb);
     L.g = take(tsize * D * D * (size_t)eb);
     L.vol = take(tsize * (size_t)eb);
+    L.eid = take(4 * (size_t)eb);
     L.occ_node = take(4 * (size_t)ocap);
     L.occ_ent = take(2 * (size_t)(ocap + 1));
     L.loc_ent = take(2 * (size_t)(D + 1) * eb);
@@ -74,7 +76,13 @@ inline RecLayout rec_layout(int D, size_t tsize, int eb, int ocap) {
 struct Plan {
     int32_t dim = 0, n_nodes = 0, n_elems = 0, n_parts = 0;
     int32_t n_blocks = 0, n_occ = 0, eb_max = 0;
-    int32_t* blk_elem = nullptr;      // [n_blocks+1]
+    int32_t* blk_elem = nullptr;      // [n_blocks+1] in plan positions (see elem_perm)
+    int32_t elem_order = 0;           // 0 input order, 1 locality (Morton) order of the positions
+    int32_t* elem_perm = nullptr;     // [n_elems] position -> input element id (null: identity)
+    int32_t* conn_p = nullptr;        // [n_elems][d+1] connectivity in position order (null: conn)
+    int32_t* csr_ptr_p = nullptr;     // node -> (position, slot) CSR (null: the mesh's CSR)
+    int32_t* csr_ent_p = nullptr;
+    void* pool_perm = nullptr;
     int32_t* blk_occ = nullptr;       // [n_blocks+1]
     int32_t* blk_min_dep = nullptr;   // [n_blocks] lowest block holding a partial this block
                                       // needs (== b if none); the block waits for [min_dep, b)

@@ -83,6 +83,7 @@ AsmParams<T> make_params(const Call& c) {
     p.fix_src = P.fix_src;
     p.occ_seg = P.occ_seg;
     p.n_fix = P.n_fix;
+    p.perm = P.elem_perm != nullptr;
     p.rec = P.rec;
     p.recs = P.recs;
     const WsLayout L = ws_layout(P, c.S, sizeof(T));

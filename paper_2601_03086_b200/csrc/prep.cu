@@ -191,6 +191,88 @@ __global__ void k_iota(int n, int32_t* out) {
     if (i < n) out[i] = i;
 }
 
+// ------------------------------------------------------------------ locality order
+// order-preserving map of a double onto uint64 (for integer atomics min / max)
+__device__ __forceinline__ unsigned long long dkey(double x) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dkey_inv(unsigned long long k) {
+    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+
+// bounding box of the nodes: bb[0..D) = min keys, bb[D..2D) = max keys
+__global__ void k_bbox(int N, int D, const double* __restrict__ coords, unsigned long long* bb) {
+    unsigned long long lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0ull, 0ull, 0ull};
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x)
+        for (int j = 0; j < D; ++j) {
+            const unsigned long long k = dkey(coords[(int64_t)n * D + j]);
+            lo[j] = min(lo[j], k);
+            hi[j] = max(hi[j], k);
+        }
+    for (int j = 0; j < D; ++j) {
+        atomicMin(bb + j, lo[j]);
+        atomicMax(bb + D + j, hi[j]);
+    }
+}
+
+__device__ __forceinline__ uint32_t spread2(uint32_t x) {   // 15 bits -> every 2nd bit
+    x &= 0x7fff;
+    x = (x | (x << 8)) & 0x00ff00ffu;
+    x = (x | (x << 4)) & 0x0f0f0f0fu;
+    x = (x | (x << 2)) & 0x33333333u;
+    x = (x | (x << 1)) & 0x55555555u;
+    return x;
+}
+__device__ __forceinline__ uint32_t spread3(uint32_t x) {   // 10 bits -> every 3rd bit
+    x &= 0x3ff;
+    x = (x | (x << 16)) & 0x030000ffu;
+    x = (x | (x << 8)) & 0x0300f00fu;
+    x = (x | (x << 4)) & 0x030c30c3u;
+    x = (x | (x << 2)) & 0x09249249u;
+    return x;
+}
+
+// key = part << 32 | Morton code of the element centroid (30 bits, bounding box of the mesh)
+__global__ void k_morton_keys(int E, int D, int K, const double* __restrict__ coords,
+                              const int32_t* __restrict__ conn, const int32_t* __restrict__ part_elem,
+                              const unsigned long long* __restrict__ bb, unsigned long long* key, int32_t* val) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    const int nv = D + 1;
+    const int bits = D == 3 ? 10 : 15;
+    uint32_t code = 0;
+    for (int j = 0; j < D; ++j) {
+        double c = 0.0;
+        for (int a = 0; a < nv; ++a) c += coords[(int64_t)conn[(int64_t)e * nv + a] * D + j];
+        c /= nv;
+        const double lo = dkey_inv(bb[j]), hi = dkey_inv(bb[D + j]);
+        const double t = hi > lo ? (c - lo) / (hi - lo) : 0.0;
+        const uint32_t q = (uint32_t)min((double)((1 << bits) - 1), max(0.0, t * (double)(1 << bits)));
+        code |= (D == 3 ? spread3(q) : spread2(q)) << j;
+    }
+    int part = 0;
+    if (K > 1) {
+        int lo = 0, hi = K - 1;   // last k with part_elem[k] <= e
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (part_elem[mid] <= e) lo = mid;
+            else hi = mid - 1;
+        }
+        part = lo;
+    }
+    key[e] = ((unsigned long long)part << 32) | code;
+    val[e] = e;
+}
+
+__global__ void k_gather_conn(int E, int nv, const int32_t* __restrict__ perm, const int32_t* __restrict__ conn,
+                              int32_t* conn_p) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= (int64_t)E * nv) return;
+    const int64_t i = k / nv, a = k - i * nv;
+    conn_p[k] = conn[(int64_t)perm[i] * nv + a];
+}
+
 // ------------------------------------------------------------------ plan
 __device__ __forceinline__ int block_of(int e, const int32_t* __restrict__ blk_elem, int nb) {
     int lo = 0, hi = nb;     // blk_elem[lo] <= e < blk_elem[hi]
@@ -364,7 +446,10 @@ __global__ void k_pack_records(int E, const int32_t* __restrict__ blk_elem, cons
                                const int32_t* __restrict__ conn, const T* __restrict__ grad,
                                const T* __restrict__ vol, const int32_t* __restrict__ occ_node,
                                const int32_t* __restrict__ occ_ent_ptr, const uint16_t* __restrict__ loc_ent,
-                               const int32_t* __restrict__ occ_seg, unsigned char* recs, RecLayout L) {
+                               const int32_t* __restrict__ occ_seg, const int32_t* __restrict__ perm,
+                               unsigned char* recs, RecLayout L) {
+    // conn (and every index here) is in plan positions; grad / vol are read at the input
+    // element perm[position] (identity when perm is null), whose id the record keeps (eid)
     constexpr int NV = D + 1;
     const int b = blockIdx.x;
     const int e0 = blk_elem[b], ne = blk_elem[b + 1] - e0;
@@ -376,13 +461,16 @@ __global__ void k_pack_records(int E, const int32_t* __restrict__ blk_elem, cons
     int32_t* ron = reinterpret_cast<int32_t*>(r + L.occ_node);
     uint16_t* roe = reinterpret_cast<uint16_t*>(r + L.occ_ent);
     uint16_t* rle = reinterpret_cast<uint16_t*>(r + L.loc_ent);
+    int32_t* rid = reinterpret_cast<int32_t*>(r + L.eid);
     for (int el = threadIdx.x; el < L.eb; el += blockDim.x) {
         const bool in = el < ne;
+        const int src = !in ? 0 : (perm ? perm[e0 + el] : e0 + el);
 #pragma unroll
         for (int a = 0; a < NV; ++a) rc[el * NV + a] = in ? conn[(int64_t)(e0 + el) * NV + a] : 0;
 #pragma unroll
-        for (int k = 0; k < D * D; ++k) rg[k * L.eb + el] = in ? grad[(int64_t)k * E + e0 + el] : T(0);
-        rv[el] = in ? vol[e0 + el] : T(0);
+        for (int k = 0; k < D * D; ++k) rg[k * L.eb + el] = in ? grad[(int64_t)k * E + src] : T(0);
+        rv[el] = in ? vol[src] : T(0);
+        rid[el] = in ? src : 0;
     }
     for (int i = threadIdx.x; i < L.ocap; i += blockDim.x) ron[i] = i < no ? occ_node[o0 + i] : 0;
     int32_t* ros = reinterpret_cast<int32_t*>(r + L.occ_seg);
@@ -621,7 +709,12 @@ pfem_status prepare_impl(pfem_mesh* m, cudaStream_t s) {
     int32_t* occ_cnt = (int32_t*)((char*)pool1 + o_cnt);
     int32_t* fix_cnt = (int32_t*)((char*)pool1 + o_fc);
     P->pool = pool1;
-    auto fail = [&](pfem_status st) { cudaFreeAsync(P->pool, s); delete P; return st; };
+    auto fail = [&](pfem_status st) {
+        cudaFreeAsync(P->pool, s);
+        if (P->pool_perm) cudaFreeAsync(P->pool_perm, s);
+        delete P;
+        return st;
+    };
 #define PLAN_TRY(expr) do { cudaError_t _e = (expr); if (_e != cudaSuccess) return fail(cuda_status(_e, #expr)); } while (0)
     PLAN_TRY(cudaMemcpyAsync(P->blk_elem, blk_elem.data(), sizeof(int32_t) * (nb + 1), cudaMemcpyHostToDevice, s));
     PLAN_TRY(cudaMemcpyAsync(P->part_blk, part_blk.data(), sizeof(int32_t) * (K + 1), cudaMemcpyHostToDevice, s));
@@ -633,15 +726,108 @@ pfem_status prepare_impl(pfem_mesh* m, cudaStream_t s) {
     P->colour_ptr_host.resize(m->n_colours + 1);
     PLAN_TRY(cudaMemcpyAsync(P->colour_ptr_host.data(), m->colour_ptr, sizeof(int32_t) * (m->n_colours + 1),
                              cudaMemcpyDeviceToHost, s));
+    // ---------------- element order of the plan (positions)
+    const int32_t* pconn = m->conn;
+    const int32_t* pptr = m->csr_ptr;
+    const int32_t* pent = m->csr_ent;
+    if (m->elem_order != PFEM_ORDER_INPUT && E > 0) {
+        {
+            const size_t a_perm = align_up(sizeof(int32_t) * (size_t)E, 256);
+            const size_t a_conn = align_up(sizeof(int32_t) * (size_t)E * nv, 256);
+            const size_t a_ptr = align_up(sizeof(int32_t) * ((size_t)N + 1), 256);
+            void* pp = nullptr;
+            PLAN_TRY(cudaMallocAsync(&pp, a_perm + 2 * a_conn + a_ptr, s));
+            P->pool_perm = pp;
+            P->elem_perm = (int32_t*)pp;
+            P->conn_p = (int32_t*)((char*)pp + a_perm);
+            P->csr_ent_p = (int32_t*)((char*)pp + a_perm + a_conn);
+            P->csr_ptr_p = (int32_t*)((char*)pp + a_perm + 2 * a_conn);
+        }
+        {
+            // Morton keys of the centroids (part id in the high word), stable radix sort
+            DevBuf tmp;
+            tmp.s = s;
+            const size_t a_key = align_up(sizeof(unsigned long long) * (size_t)E, 256);
+            const size_t a_val = align_up(sizeof(int32_t) * (size_t)E, 256);
+            int end_bit = 32;
+            while ((1ll << (end_bit - 32)) < K) ++end_bit;
+            size_t tb = 0;
+            PLAN_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, (unsigned long long*)nullptr,
+                                                     (unsigned long long*)nullptr, (int32_t*)nullptr,
+                                                     P->elem_perm, E, 0, end_bit, s));
+            PLAN_TRY(cudaMallocAsync(&tmp.p, 2 * a_key + a_val + 256 + tb, s));
+            unsigned long long* kin = (unsigned long long*)tmp.p;
+            unsigned long long* kout = (unsigned long long*)((char*)tmp.p + a_key);
+            int32_t* vin = (int32_t*)((char*)tmp.p + 2 * a_key);
+            unsigned long long* bb = (unsigned long long*)((char*)tmp.p + 2 * a_key + a_val);
+            void* t2 = (char*)tmp.p + 2 * a_key + a_val + 256;
+            unsigned long long bb0[6] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull};
+            unsigned long long bbi[6];
+            for (int j = 0; j < D; ++j) { bbi[j] = bb0[0]; bbi[D + j] = 0ull; }
+            PLAN_TRY(cudaMemcpyAsync(bb, bbi, sizeof(unsigned long long) * 2 * D, cudaMemcpyHostToDevice, s));
+            k_bbox<<<std::max(1u, std::min(nblk(N, 256), 1184u)), 256, 0, s>>>(N, D, m->coords, bb);
+            count_launch();
+            k_morton_keys<<<nblk(E, 256), 256, 0, s>>>(E, D, K, m->coords, m->conn, P->part_elem, bb, kin, vin);
+            count_launch();
+            PLAN_TRY(cudaGetLastError());
+            PLAN_TRY(cub::DeviceRadixSort::SortPairs(t2, tb, kin, kout, vin, P->elem_perm, E, 0, end_bit, s));
+            count_launch();
+            PLAN_TRY(cudaStreamSynchronize(s));   // tmp is released at scope end
+        }
+        k_gather_conn<<<nblk((int64_t)E * nv, 256), 256, 0, s>>>(E, nv, P->elem_perm, m->conn, P->conn_p);
+        count_launch();
+        // node -> (position, slot) CSR of the ordered connectivity
+        PLAN_TRY(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (N + 1), s));
+        k_count<<<nblk(nent, 256), 256, 0, s>>>(nent, P->conn_p, cnt);
+        count_launch();
+        {
+            pfem_status st = exclusive_scan_i32(cnt, P->csr_ptr_p, N + 1, s);
+            if (st != PFEM_OK) return fail(st);
+        }
+        PLAN_TRY(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (N + 1), s));
+        k_csr_fill<<<nblk(nent, 256), 256, 0, s>>>(nent, P->conn_p, P->csr_ptr_p, cnt, P->csr_ent_p);
+        count_launch();
+        k_csr_sort_rows<<<nblk(N, 128), 128, 0, s>>>(N, P->csr_ptr_p, P->csr_ent_p);
+        count_launch();
+        PLAN_TRY(cudaGetLastError());
+        if (m->elem_order == PFEM_ORDER_AUTO) {
+            // keep the order with fewer (block, node) occurrences (block-local sort counts)
+            int32_t tot[2] = {0, 0};
+            for (int v = 0; v < 2; ++v) {
+                k_block_build<<<nb, PLAN_THREADS, 0, s>>>(0, nv, nb, P->blk_elem, v ? P->conn_p : m->conn,
+                                                          v ? P->csr_ptr_p : m->csr_ptr, v ? P->csr_ent_p : m->csr_ent,
+                                                          occ_cnt, fix_cnt, P->blk_min_dep, nullptr, nullptr, nullptr,
+                                                          nullptr, nullptr, nullptr, nullptr, nullptr);
+                count_launch();
+                PLAN_TRY(cudaGetLastError());
+                PLAN_TRY(cudaMemsetAsync(occ_cnt + nb, 0, sizeof(int32_t), s));
+                pfem_status st = exclusive_scan_i32(occ_cnt, P->blk_occ, nb + 1, s);
+                if (st != PFEM_OK) return fail(st);
+                PLAN_TRY(cudaMemcpyAsync(&tot[v], P->blk_occ + nb, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+                PLAN_TRY(cudaStreamSynchronize(s));
+            }
+            if (tot[1] >= tot[0]) {
+                PLAN_TRY(cudaFreeAsync(P->pool_perm, s));
+                P->pool_perm = nullptr;
+                P->elem_perm = P->conn_p = P->csr_ptr_p = P->csr_ent_p = nullptr;
+            }
+        }
+    }
+    if (P->elem_perm) {
+        pconn = P->conn_p;
+        pptr = P->csr_ptr_p;
+        pent = P->csr_ent_p;
+    }
+    P->elem_order = P->elem_perm ? 1 : 0;
     // node-major occurrence counts -> node_occ_ptr
-    k_node_occ_count<<<nblk(N, 256), 256, 0, s>>>(N, nv, m->csr_ptr, m->csr_ent, P->blk_elem, nb, cnt);
+    k_node_occ_count<<<nblk(N, 256), 256, 0, s>>>(N, nv, pptr, pent, P->blk_elem, nb, cnt);
     count_launch();
     PLAN_TRY(cudaGetLastError());
     {
         pfem_status st = exclusive_scan_i32(cnt, P->node_occ_ptr, N + 1, s);
         if (st != PFEM_OK) return fail(st);
     }
-    k_block_build<<<nb, PLAN_THREADS, 0, s>>>(0, nv, nb, P->blk_elem, m->conn, m->csr_ptr, m->csr_ent,
+    k_block_build<<<nb, PLAN_THREADS, 0, s>>>(0, nv, nb, P->blk_elem, pconn, pptr, pent,
                                               occ_cnt, fix_cnt, P->blk_min_dep, nullptr, nullptr, nullptr,
                                               nullptr, nullptr, nullptr, nullptr, nullptr);
     count_launch();
@@ -678,7 +864,7 @@ pfem_status prepare_impl(pfem_mesh* m, cudaStream_t s) {
     P->node_occ = (int32_t*)(pb + fixed + q_no);
     P->fix_occ = (int32_t*)(pb + fixed + q_fo);
     occ_cnt = (int32_t*)(pb + o_cnt);
-    k_block_build<<<nb, PLAN_THREADS, 0, s>>>(1, nv, nb, P->blk_elem, m->conn, m->csr_ptr, m->csr_ent,
+    k_block_build<<<nb, PLAN_THREADS, 0, s>>>(1, nv, nb, P->blk_elem, pconn, pptr, pent,
                                               nullptr, nullptr, nullptr, P->blk_occ, P->occ_node, P->occ_ent_ptr,
                                               P->loc_ent, P->node_occ_ptr, P->node_occ, P->blk_fix, P->fix_occ);
     count_launch();
@@ -740,18 +926,18 @@ pfem_status prepare_impl(pfem_mesh* m, cudaStream_t s) {
         P->recs = (unsigned char*)pr;
         if (D == 2) {
             if (ts == 4)
-                k_pack_records<2, float><<<nb, 256, 0, s>>>(E, P->blk_elem, P->blk_occ, m->conn, (const float*)m->grad,
-                    (const float*)m->vol, P->occ_node, P->occ_ent_ptr, P->loc_ent, P->occ_seg, P->recs, P->rec);
+                k_pack_records<2, float><<<nb, 256, 0, s>>>(E, P->blk_elem, P->blk_occ, pconn, (const float*)m->grad,
+                    (const float*)m->vol, P->occ_node, P->occ_ent_ptr, P->loc_ent, P->occ_seg, P->elem_perm, P->recs, P->rec);
             else
-                k_pack_records<2, double><<<nb, 256, 0, s>>>(E, P->blk_elem, P->blk_occ, m->conn, (const double*)m->grad,
-                    (const double*)m->vol, P->occ_node, P->occ_ent_ptr, P->loc_ent, P->occ_seg, P->recs, P->rec);
+                k_pack_records<2, double><<<nb, 256, 0, s>>>(E, P->blk_elem, P->blk_occ, pconn, (const double*)m->grad,
+                    (const double*)m->vol, P->occ_node, P->occ_ent_ptr, P->loc_ent, P->occ_seg, P->elem_perm, P->recs, P->rec);
         } else {
             if (ts == 4)
-                k_pack_records<3, float><<<nb, 256, 0, s>>>(E, P->blk_elem, P->blk_occ, m->conn, (const float*)m->grad,
-                    (const float*)m->vol, P->occ_node, P->occ_ent_ptr, P->loc_ent, P->occ_seg, P->recs, P->rec);
+                k_pack_records<3, float><<<nb, 256, 0, s>>>(E, P->blk_elem, P->blk_occ, pconn, (const float*)m->grad,
+                    (const float*)m->vol, P->occ_node, P->occ_ent_ptr, P->loc_ent, P->occ_seg, P->elem_perm, P->recs, P->rec);
             else
-                k_pack_records<3, double><<<nb, 256, 0, s>>>(E, P->blk_elem, P->blk_occ, m->conn, (const double*)m->grad,
-                    (const double*)m->vol, P->occ_node, P->occ_ent_ptr, P->loc_ent, P->occ_seg, P->recs, P->rec);
+                k_pack_records<3, double><<<nb, 256, 0, s>>>(E, P->blk_elem, P->blk_occ, pconn, (const double*)m->grad,
+                    (const double*)m->vol, P->occ_node, P->occ_ent_ptr, P->loc_ent, P->occ_seg, P->elem_perm, P->recs, P->rec);
         }
         count_launch();
         PLAN_TRY(cudaGetLastError());
@@ -771,6 +957,7 @@ void release_impl(pfem_mesh* m) {
     if (P->pool_fix) cudaFree(P->pool_fix);
     if (P->pool_src) cudaFree(P->pool_src);
     if (P->pool_rec) cudaFree(P->pool_rec);
+    if (P->pool_perm) cudaFree(P->pool_perm);
     delete P;
     m->plan = nullptr;
 }

@@ -28,7 +28,7 @@ def max_rel(a, b):
     return np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300))
 
 
-def gpu_problem(prob, dtype=None, block_elems=0, dev="cuda"):
+def gpu_problem(prob, dtype=None, block_elems=0, dev="cuda", elem_order="auto"):
     """(Mesh, Material, u tensor) for the CUDA path."""
     import paper_2601_03086_b200 as pf
     dtype = dtype or prob.dtype
@@ -36,7 +36,7 @@ def gpu_problem(prob, dtype=None, block_elems=0, dev="cuda"):
     pe, pn = prob.parts()
     mesh = pf.Mesh(torch.as_tensor(prob.coords, device=dev), torch.as_tensor(prob.conn, device=dev), dtype=td,
                    part_elem=pe if prob.n_parts > 1 else None, part_node=pn if prob.n_parts > 1 else None,
-                   block_elems=block_elems)
+                   block_elems=block_elems, elem_order=elem_order)
     mat = pf.Material(prob.model, prob.param_kind, torch.as_tensor(np.asarray(prob.p0), dtype=td, device=dev),
                       torch.as_tensor(np.asarray(prob.p1), dtype=td, device=dev))
     u = torch.as_tensor(prob.u, dtype=td, device=dev)

@@ -72,15 +72,24 @@ def test_prepare_bitexact(orc, prob):
     assert mesh.n_negative == int((sgn < 0).sum())
 
 
+@pytest.mark.parametrize("order", ["input", "locality"])
 @pytest.mark.parametrize("prob", SMALL[:3], ids=lambda p: p.name)
-def test_plan_is_a_partition_of_the_csr(orc, prob):
+def test_plan_is_a_partition_of_the_csr(orc, prob, order):
     """Every (element, slot) entry appears exactly once, under the occurrence of its own
     node, inside its own block; occurrences of a block are sorted by node; exactly one
-    owner per node (the block of its highest element)."""
-    mesh, _, _ = gpu_problem(prob, block_elems=97)    # small blocks -> many boundaries
+    owner per node (the block of its highest element position).  Blocks hold plan
+    positions; elem_perm maps them to input elements (a permutation inside each part)."""
+    mesh, _, _ = gpu_problem(prob, block_elems=97, elem_order=order)    # small blocks -> many boundaries
     P = mesh.plan_export()
     nv = prob.dim + 1
-    be, bo, on, oe, le = P["blk_elem"], P["blk_occ"], P["occ_node"], P["occ_ent_ptr"], P["loc_ent"]
+    be, bo, on, oe, le, pm = (P["blk_elem"], P["blk_occ"], P["occ_node"], P["occ_ent_ptr"], P["loc_ent"],
+                              P["elem_perm"])
+    assert np.array_equal(np.sort(pm), np.arange(prob.n_elems))
+    if order == "input":
+        assert np.array_equal(pm, np.arange(prob.n_elems))
+    pe, _ = prob.parts()
+    part_of = np.searchsorted(pe, np.arange(prob.n_elems), side="right") - 1
+    assert np.array_equal(part_of[pm], part_of)          # positions stay inside their part
     seen = np.zeros(prob.n_elems * nv, np.int32)
     owners = np.zeros(prob.n_nodes, np.int32)
     for b in range(len(be) - 1):
@@ -92,13 +101,38 @@ def test_plan_is_a_partition_of_the_csr(orc, prob):
                 owners[n] += 1
             ents = le[oe[o]:oe[o + 1]].astype(np.int64)
             assert np.all(np.diff(ents) > 0)
-            glob = be[b] * nv + ents
-            assert np.all(glob < be[b + 1] * nv)
+            pos = be[b] * nv + ents
+            assert np.all(pos < be[b + 1] * nv)
+            glob = pm[pos // nv].astype(np.int64) * nv + pos % nv      # input (element, slot)
             assert np.all(prob.conn.reshape(-1)[glob] == n)
             seen[glob] += 1
     assert np.all(seen == 1)
     used = np.unique(prob.conn)
     assert np.all(owners[used] == 1)
+
+
+@pytest.mark.parametrize("order", ["input", "locality"])
+@pytest.mark.parametrize("prob", SMALL, ids=lambda p: p.name)
+def test_element_order_energy_residual_tangent(orc, prob, order):
+    """Both plan element orders give the oracle's W_e (in input element order), totals,
+    residual and K.v, with element-wise materials gathered through the permutation."""
+    import paper_2601_03086_b200 as pf
+    mesh, mat, u = gpu_problem(prob, block_elems=61, elem_order=order)
+    om = oracle_problem(orc, prob)
+    ur = rounded(prob.u, prob.dtype)
+    W_ref, tot_ref = om.energy(ur)
+    r_ref = om.residual(ur)
+    tot, W, r = pf.energy(mesh, mat, u, elem_energy=True, residual=True)
+    v = rounded(np.random.default_rng(11).standard_normal(prob.u.shape) * 1e-2, prob.dtype)
+    kv_ref = om.tangent(v, u=ur if prob.model == "neohookean" else None)
+    kv = pf.tangent_apply(mesh, mat, torch.as_tensor(v, dtype=u.dtype, device="cuda"),
+                          u=u if prob.model == "neohookean" else None)
+    torch.cuda.synchronize()
+    tol = TOL[prob.dtype]
+    assert rel_l2(W.cpu().numpy(), W_ref) < tol
+    assert max_rel(tot.cpu().numpy(), tot_ref) < (tol if prob.dtype == "f64" else 1e-5)
+    assert rel_l2(r.cpu().numpy(), r_ref) < tol
+    assert rel_l2(kv.cpu().numpy(), kv_ref) < tol
 
 
 # ------------------------------------------------------------------ energy / residual
