@@ -287,10 +287,11 @@ __device__ __forceinline__ void stage_block(unsigned char* st, T* mst, uint64_t*
 // element-wise material of a block whose record has landed in shared memory: cp.async by
 // input element id (the plan may visit elements in a locality order)
 template <class T, int NT>
-__device__ __forceinline__ void stage_material(T* mst, const unsigned char* rec, const AsmParams<T>& p, int ne) {
-    const int32_t* eid = reinterpret_cast<const int32_t*>(rec + p.rec.eid);
+__device__ __forceinline__ void stage_material(T* mst, const unsigned char* rec, const AsmParams<T>& p, int b) {
+    const int32_t* eid = reinterpret_cast<const int32_t*>(rec + p.rec.eid);   // present iff p.perm
+    const int e0 = __ldg(p.blk_elem + b), ne = __ldg(p.blk_elem + b + 1) - e0;
     for (int el = threadIdx.x; el < ne; el += NT) {
-        const int64_t e = eid[el];
+        const int64_t e = p.perm ? eid[el] : e0 + el;
         if (p.mat.s0) cpn<sizeof(T)>(mst + el, p.mat.p0 + e * p.mat.s0);
         if (p.mat.s1) cpn<sizeof(T)>(mst + p.rec.eb + el, p.mat.p1 + e * p.mat.s1);
     }
@@ -440,7 +441,7 @@ k_assemble(const AsmParams<T> p) {
             if (pref)
                 stage_fields<D, T, NT, ST, MASKED>(ustage, stage0, staged_src, p, 0, S,
                                                    __ldg(p.blk_occ + t + 1) - __ldg(p.blk_occ + t));
-            if (has_mat) stage_material<T, NT>(mstage, stage0, p, __ldg(p.blk_elem + t + 1) - __ldg(p.blk_elem + t));
+            if (has_mat) stage_material<T, NT>(mstage, stage0, p, t);
         }
         cp_commit();
     }
@@ -482,7 +483,7 @@ k_assemble(const AsmParams<T> p) {
 #pragma unroll
             for (int q = 0; q < ST; ++q) wacc[q] = T(0);
             for (int el = tid; el < ne; el += NT) {
-                const int e = seid[el];   // input element id (W_e, flags)
+                const int e = p.perm ? seid[el] : e0 + el;   // input element id (W_e, flags)
                 Geo<D, T> G_;
                 if constexpr (D == 3) {
                     const int4 cv = *reinterpret_cast<const int4*>(sconn + el * 4);
@@ -568,8 +569,7 @@ k_assemble(const AsmParams<T> p) {
                         stage_fields<D, T, NT, ST, MASKED>(ustage + ust_sz * (cur ^ 1), sg_nxt, staged_src, p, 0, S,
                                                            __ldg(p.blk_occ + tn + 1) - __ldg(p.blk_occ + tn));
                     if (has_mat)
-                        stage_material<T, NT>(mstage + 2 * EB * (cur ^ 1), sg_nxt, p,
-                                              __ldg(p.blk_elem + tn + 1) - __ldg(p.blk_elem + tn));
+                        stage_material<T, NT>(mstage + 2 * EB * (cur ^ 1), sg_nxt, p, tn);
                 }
                 cp_commit();
             }

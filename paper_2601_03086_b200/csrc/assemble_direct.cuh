@@ -51,23 +51,22 @@ __device__ __forceinline__ void prefetch_record(const AsmParams<T>& p, int b) {
     const int e0 = __ldg(p.blk_elem + b), e1 = __ldg(p.blk_elem + b + 1);
     const size_t E = (size_t)p.E, ne = (size_t)(e1 - e0);
     if (p.perm) return;   // element-wise materials are gathered through the permutation
+
     if (p.mat.s0) l2_prefetch(p.mat.p0, E * sizeof(T), e0 * sizeof(T), ne * sizeof(T));
     if (p.mat.s1) l2_prefetch(p.mat.p1, E * sizeof(T), e0 * sizeof(T), ne * sizeof(T));
 }
 
-#ifndef PFEM_DIRECT_MINB1
-#define PFEM_DIRECT_MINB1 (65536 / (NT * 64))
-#endif
 #ifndef PFEM_DIRECT_SCALAR
 #define PFEM_DIRECT_SCALAR 0
 #endif
 #ifndef PFEM_DIRECT_MINBS
 #define PFEM_DIRECT_MINBS 6
 #endif
-// register budget (minimum resident CTAs): single-sample calls 64 registers, several-sample
-// fp32 calls 80 (measured; the compiler's default allocation is larger and costs occupancy)
-template <int D, int MODEL, class T, int OP, int ST, bool MASKED, int NT>
-__global__ void __launch_bounds__(NT, ST > 1 ? PFEM_DIRECT_MINBS : PFEM_DIRECT_MINB1)
+// register budget (measured): fp64 single-sample calls use the compiler's own allocation (an
+// explicit 64-register bound was 6% slower on config 4); fp32 single-sample calls 64
+// registers (8% faster on config 5 than the default); several-sample fp32 calls 80
+template <int D, int MODEL, class T, int OP, int ST, bool MASKED, int NT, bool PERM>
+__global__ void __launch_bounds__(NT, ST > 1 ? PFEM_DIRECT_MINBS : (sizeof(T) == 4 ? 65536 / (NT * 64) : 0))
 k_assemble_direct(const AsmParams<T> p) {
     // shared: ust[NF][OCAP][D][ST] (staged nodal fields) | [le[(d+1) EB] u16] | fbuf
     // EPOS (fp32): fbuf[(d+1) EB entries][D][ST], element vertex forces scattered to their
@@ -143,7 +142,9 @@ k_assemble_direct(const AsmParams<T> p) {
         lsc.lam1 = s_lame[1];
         // ---------------- phase 1: elements (one per thread and pass)
         for (int el = tid; el < ne; el += NT) {
-            const int e = __ldg(reinterpret_cast<const int32_t*>(rg + p.rec.eid) + el);   // input element id
+            // input element id (W_e, material, flags): identity order needs no load, and the
+            // material load then does not wait on the id
+            const int e = PERM ? __ldg(reinterpret_cast<const int32_t*>(rg + p.rec.eid) + el) : e0 + el;
             Geo<D, T> G;
             int lv[NV], ep[NV];   // vertex -> staged occurrence, vertex -> block-CSR entry
             if constexpr (D == 3) {

@@ -53,7 +53,7 @@ struct RecLayout {
     uint32_t conn = 0, g = 0, vol = 0, eid = 0, occ_node = 0, occ_ent = 0, loc_ent = 0, lconn = 0, occ_seg = 0, ent_pos = 0, bytes = 0;
 };
 
-inline RecLayout rec_layout(int D, size_t tsize, int eb, int ocap) {
+inline RecLayout rec_layout(int D, size_t tsize, int eb, int ocap, bool with_eid) {
     RecLayout L;
     L.eb = eb;
     L.ocap = ocap;
@@ -62,7 +62,7 @@ inline RecLayout rec_layout(int D, size_t tsize, int eb, int ocap) {
     L.conn = take(4 * (size_t)(D + 1) * eb);
     L.g = take(tsize * D * D * (size_t)eb);
     L.vol = take(tsize * (size_t)eb);
-    L.eid = take(4 * (size_t)eb);
+    L.eid = take(with_eid ? 4 * (size_t)eb : 0);   // identity order: no ids stored
     L.occ_node = take(4 * (size_t)ocap);
     L.occ_ent = take(2 * (size_t)(ocap + 1));
     L.loc_ent = take(2 * (size_t)(D + 1) * eb);

@@ -108,14 +108,14 @@ AsmParams<T> make_params(const Call& c) {
 template <class T>
 constexpr int direct_nt() { return sizeof(T) == 4 ? PFEM_DIRECT_NT32 : 256; }   // direct kernel threads per CTA (measured)
 
-template <int D, int MODEL, class T, int OP, int ST, bool MASKED, int NT>
+template <int D, int MODEL, class T, int OP, int ST, bool MASKED, int NT, bool PERM>
 pfem_status launch_direct(AsmParams<T> p, cudaStream_t s) {
     constexpr bool HAS_FORCE = OP != OP_ENERGY;
     constexpr int NFd = (OP == OP_TANGENT && MODEL == MODEL_NH) ? 2 : 1;
     const size_t smem = ((NFd * (size_t)p.rec.ocap * D * ST * sizeof(T) + (sizeof(T) == 4 ? 0 : 2 * (size_t)(D + 1) * p.rec.eb) +
                           15) & ~size_t(15)) +
                         (HAS_FORCE ? (size_t)ST * D * (D + 1) * p.rec.eb * sizeof(T) : 0);
-    auto kd = k_assemble_direct<D, MODEL, T, OP, ST, MASKED, NT>;
+    auto kd = k_assemble_direct<D, MODEL, T, OP, ST, MASKED, NT, PERM>;
     static size_t configured = 0;
     static int pf_auto = 0;
     if (smem > configured || pf_auto == 0) {
@@ -125,7 +125,7 @@ pfem_status launch_direct(AsmParams<T> p, cudaStream_t s) {
         PFEM_CUDA_TRY(cudaGetDevice(&dev));
         PFEM_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         PFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kd, NT, smem));
-        pf_auto = std::max(1, per_sm * nsm);
+        pf_auto = std::max(1, std::min(per_sm, 2) * nsm);   // measured: a deeper prefetch evicts
     }
     static const int pf = getenv("PFEM_PF") ? atoi(getenv("PFEM_PF")) : -1;
     p.lag = pf >= 0 ? pf : pf_auto;   // L2 prefetch distance in blocks (~ one wave ahead)
@@ -173,7 +173,8 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
     // PFEM_VARIANT=0/1 forces staged/direct (measurement switch).
     const bool direct = variant >= 0 ? variant == 1 : p.S == 1;
     if (direct) {
-        const pfem_status st = launch_direct<D, MODEL, T, OP, ST, MASKED, direct_nt<T>()>(p, s);
+        const pfem_status st = p.perm ? launch_direct<D, MODEL, T, OP, ST, MASKED, direct_nt<T>(), true>(p, s)
+                                      : launch_direct<D, MODEL, T, OP, ST, MASKED, direct_nt<T>(), false>(p, s);
         if (st != PFEM_OK) return st;
     } else {
         const int grid = std::max(1, std::min(resident, p.n_blocks));

@@ -470,7 +470,7 @@ __global__ void k_pack_records(int E, const int32_t* __restrict__ blk_elem, cons
 #pragma unroll
         for (int k = 0; k < D * D; ++k) rg[k * L.eb + el] = in ? grad[(int64_t)k * E + src] : T(0);
         rv[el] = in ? vol[src] : T(0);
-        rid[el] = in ? src : 0;
+        if (perm) rid[el] = in ? src : 0;
     }
     for (int i = threadIdx.x; i < L.ocap; i += blockDim.x) ron[i] = i < no ? occ_node[o0 + i] : 0;
     int32_t* ros = reinterpret_cast<int32_t*>(r + L.occ_seg);
@@ -919,7 +919,7 @@ pfem_status prepare_impl(pfem_mesh* m, cudaStream_t s) {
         for (int b = 0; b < nb; ++b) ocap = std::max(ocap, bo[b + 1] - bo[b]);
         ocap = (ocap + 7) / 8 * 8;
         const size_t ts = m->dtype == PFEM_F64 ? 8 : 4;
-        P->rec = rec_layout(D, ts, eb_cap, ocap);
+        P->rec = rec_layout(D, ts, eb_cap, ocap, P->elem_perm != nullptr);
         void* pr = nullptr;
         PLAN_TRY(cudaMallocAsync(&pr, (size_t)P->rec.bytes * nb, s));
         P->pool_rec = pr;
