@@ -18,11 +18,20 @@ namespace pfem {
 
 constexpr int VEC_NT = 256;
 
+constexpr int VEC_U = 4;          // independent elements per thread and pass (loads in flight)
+constexpr int VEC_MAX_GRID = 2048;
+
 struct VecRed {
     int32_t counter;
     int32_t pad[63];
-    double part[1024];
+    double part[VEC_MAX_GRID];
 };
+
+// grid-stride passes of VEC_U elements per thread: i0 + u * stride, u < VEC_U
+#define VEC_PASSES(n)                                                                       \
+    const int64_t vstride_ = (int64_t)gridDim.x * VEC_NT;                                   \
+    for (int64_t i0 = (int64_t)blockIdx.x * VEC_NT + threadIdx.x; i0 < (n); i0 += VEC_U * vstride_)
+#define VEC_IDX(u) (i0 + (int64_t)(u) * vstride_)
 
 __device__ __forceinline__ bool vec_last_block(VecRed* vr, double v, double* s_red, int* s_flag) {
     const double t = cta_sum<VEC_NT>(v, s_red);
@@ -39,7 +48,13 @@ __device__ __forceinline__ bool vec_last_block(VecRed* vr, double v, double* s_r
 __device__ __forceinline__ double vec_final(VecRed* vr, double* s_red) {
     __threadfence();
     double v = 0.0;
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += VEC_NT) v += ld_relaxed(vr->part + i);
+    for (int i0 = threadIdx.x; i0 < (int)gridDim.x; i0 += 8 * VEC_NT) {   // loads 8 at a time
+        double w[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) w[u] = i0 + u * VEC_NT < (int)gridDim.x ? ld_relaxed(vr->part + i0 + u * VEC_NT) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v += w[u];
+    }
     const double t = cta_sum<VEC_NT>(v, s_red);
     if (threadIdx.x == 0) vr->counter = 0;
     return t;
@@ -118,11 +133,22 @@ k_cg_update(int64_t n, T* __restrict__ x, T* __restrict__ r, const T* __restrict
     if (ld_relaxed_i(&cg->done)) return;
     const T alpha = (T)cg->alpha;
     double acc = 0.0;
-    for (int64_t i = (int64_t)blockIdx.x * VEC_NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * VEC_NT) {
-        x[i] = fma(alpha, p[i], x[i]);
-        const T v = fma(-alpha, q[i], r[i]);
-        r[i] = v;
-        acc += (double)v * (double)v;
+    VEC_PASSES(n) {
+        T xv[VEC_U], pv[VEC_U], qv[VEC_U], rv[VEC_U];
+#pragma unroll
+        for (int u = 0; u < VEC_U; ++u) {
+            const int64_t i = VEC_IDX(u);
+            if (i < n) { xv[u] = x[i]; pv[u] = p[i]; qv[u] = q[i]; rv[u] = r[i]; }
+        }
+#pragma unroll
+        for (int u = 0; u < VEC_U; ++u) {
+            const int64_t i = VEC_IDX(u);
+            if (i >= n) break;
+            x[i] = fma(alpha, pv[u], xv[u]);
+            const T v = fma(-alpha, qv[u], rv[u]);
+            r[i] = v;
+            acc += (double)v * (double)v;
+        }
     }
     if (!vec_last_block(vr, acc, s_red, &s_flag)) return;
     const double t = vec_final(vr, s_red);
@@ -149,8 +175,19 @@ __global__ void __launch_bounds__(VEC_NT)
 k_cg_dir(int64_t n, const T* __restrict__ r, T* __restrict__ p, const CgState* cg) {
     if (ld_relaxed_i(&cg->done)) return;
     const T beta = (T)cg->beta;
-    for (int64_t i = (int64_t)blockIdx.x * VEC_NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * VEC_NT)
-        p[i] = fma(beta, p[i], r[i]);
+    VEC_PASSES(n) {
+        T pv[VEC_U], rv[VEC_U];
+#pragma unroll
+        for (int u = 0; u < VEC_U; ++u) {
+            const int64_t i = VEC_IDX(u);
+            if (i < n) { pv[u] = p[i]; rv[u] = r[i]; }
+        }
+#pragma unroll
+        for (int u = 0; u < VEC_U; ++u) {
+            const int64_t i = VEC_IDX(u);
+            if (i < n) p[i] = fma(beta, pv[u], rv[u]);
+        }
+    }
 }
 
 // COLOUR-mode CG: p.q and alpha as a separate pass
@@ -259,7 +296,7 @@ pfem_status cg_impl(const pfem_mesh* m, const pfem_material* mat, const void* u_
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int G = std::min(1024, 2 * nsm);   // fixed grid => fixed reduction order
+    const int G = std::min(VEC_MAX_GRID, 8 * nsm);   // fixed grid => fixed reduction order
     CgState h{};
     h.tol2 = tol * tol;
     h.max_iter = max_iter;
