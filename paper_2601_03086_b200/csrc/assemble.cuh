@@ -97,6 +97,7 @@ struct AsmParams {
     int n_fix;
     int perm;              // plan positions are a permutation of the input elements
     RecLayout rec;
+    uint32_t rec_base;     // staged kernel: first record byte it copies (rec.conn or rec.g)
     const unsigned char* recs;
     // workspace
     Counters* ctr;
@@ -278,8 +279,9 @@ template <int D, class T, int NT>
 __device__ __forceinline__ void stage_block(unsigned char* st, T* mst, uint64_t* bar, const AsmParams<T>& p, int b) {
     if (threadIdx.x == 0) {
         fence_proxy_async();   // earlier generic reads of this buffer precede the async write
-        mbar_expect_tx(bar, p.rec.bytes);
-        tma_bulk_g2s(st, p.recs + (size_t)b * p.rec.bytes, p.rec.bytes, bar);
+        const uint32_t n = p.rec.bytes - p.rec_base;
+        mbar_expect_tx(bar, n);
+        tma_bulk_g2s(st, p.recs + (size_t)b * p.rec.bytes + p.rec_base, n, bar);
     }
     cp_commit();   // (empty group: keeps the one-group-per-stage accounting of cp_wait)
 }
@@ -287,8 +289,9 @@ __device__ __forceinline__ void stage_block(unsigned char* st, T* mst, uint64_t*
 // element-wise material of a block whose record has landed in shared memory: cp.async by
 // input element id (the plan may visit elements in a locality order)
 template <class T, int NT>
-__device__ __forceinline__ void stage_material(T* mst, const unsigned char* rec, const AsmParams<T>& p, int b) {
-    const int32_t* eid = reinterpret_cast<const int32_t*>(rec + p.rec.eid);   // present iff p.perm
+__device__ __forceinline__ void stage_material(T* mst, const unsigned char* rec, uint32_t base, const AsmParams<T>& p,
+                                               int b) {
+    const int32_t* eid = reinterpret_cast<const int32_t*>(rec + (p.rec.eid - base));   // present iff p.perm
     const int e0 = __ldg(p.blk_elem + b), ne = __ldg(p.blk_elem + b + 1) - e0;
     for (int el = threadIdx.x; el < ne; el += NT) {
         const int64_t e = p.perm ? eid[el] : e0 + el;
@@ -367,10 +370,11 @@ __device__ __forceinline__ void sacc(const T* __restrict__ src, T (&acc)[SD]) {
 }
 
 template <int D, class T, int NT, int ST, bool MASKED>
-__device__ __forceinline__ void stage_fields(T* ust, const unsigned char* rec, const T* src, const AsmParams<T>& p,
-                                             int s0, int nq, int no) {
+__device__ __forceinline__ void stage_fields(T* ust, const unsigned char* rec, uint32_t base, const T* src,
+                                             const AsmParams<T>& p, int s0, int nq, int no) {
     // ust[occ][D][ST] <- src[s0 + q][node(occ)][i]; masked DOFs are zero-filled (src-size 0)
-    const int32_t* socc = reinterpret_cast<const int32_t*>(rec + p.rec.occ_node);
+    // (rec holds the record from byte `base` on)
+    const int32_t* socc = reinterpret_cast<const int32_t*>(rec + (p.rec.occ_node - base));
     for (int o = threadIdx.x; o < no; o += NT) {
         const int node = socc[o] & OCC_NODE_MASK;
         T* dst = ust + (size_t)o * D * ST;
@@ -407,9 +411,11 @@ k_assemble(const AsmParams<T> p) {
     constexpr int LA = VTraits<A2>::L;
     const T* staged_src = (OP == OP_TANGENT) ? p.v : p.u;
     // shared layout: rec[2] | mat[2][2][EB] | ust[2][OCAP][D][ST] | fbuf[NV][EB][D][ST]
+    const uint32_t srb = p.rec.bytes - p.rec_base;   // staged bytes of a record
+    const bool has_conn = p.rec_base <= p.rec.conn;   // conn is staged (gathers, NH tangent state)
     unsigned char* const stage0 = smem_raw;
-    unsigned char* const stage1 = smem_raw + p.rec.bytes;
-    T* mstage = reinterpret_cast<T*>(smem_raw + 2 * (size_t)p.rec.bytes);
+    unsigned char* const stage1 = smem_raw + srb;
+    T* mstage = reinterpret_cast<T*>(smem_raw + 2 * (size_t)srb);
     T* ustage = mstage + 4 * EB;
     const size_t ust_sz = (size_t)NF * p.rec.ocap * D * ST;
     T* fbuf = ustage + 2 * ust_sz;
@@ -439,9 +445,9 @@ k_assemble(const AsmParams<T> p) {
         if (pref || has_mat) {
             mbar_wait(&s_bar[0], 0);
             if (pref)
-                stage_fields<D, T, NT, ST, MASKED>(ustage, stage0, staged_src, p, 0, S,
+                stage_fields<D, T, NT, ST, MASKED>(ustage, stage0, p.rec_base, staged_src, p, 0, S,
                                                    __ldg(p.blk_occ + t + 1) - __ldg(p.blk_occ + t));
-            if (has_mat) stage_material<T, NT>(mstage, stage0, p, t);
+            if (has_mat) stage_material<T, NT>(mstage, stage0, p.rec_base, p, t);
         }
         cp_commit();
     }
@@ -456,8 +462,8 @@ k_assemble(const AsmParams<T> p) {
         else cp_commit();
         const int e0 = __ldg(p.blk_elem + b), ne = __ldg(p.blk_elem + b + 1) - e0;
         const int o0 = __ldg(p.blk_occ + b), no = __ldg(p.blk_occ + b + 1) - o0;
-        const unsigned char* sg = sg_cur;
-        const int32_t* sconn = reinterpret_cast<const int32_t*>(sg + p.rec.conn);
+        const unsigned char* sg = sg_cur - p.rec_base;   // record byte offsets apply from here
+        const int32_t* sconn = reinterpret_cast<const int32_t*>(sg + p.rec.conn);   // valid iff rec_base <= conn
         const T* sgrad = reinterpret_cast<const T*>(sg + p.rec.g);
         const T* svol = reinterpret_cast<const T*>(sg + p.rec.vol);
         const int32_t* socc = reinterpret_cast<const int32_t*>(sg + p.rec.occ_node);
@@ -485,12 +491,17 @@ k_assemble(const AsmParams<T> p) {
             for (int el = tid; el < ne; el += NT) {
                 const int e = p.perm ? seid[el] : e0 + el;   // input element id (W_e, flags)
                 Geo<D, T> G_;
-                if constexpr (D == 3) {
-                    const int4 cv = *reinterpret_cast<const int4*>(sconn + el * 4);
-                    G_.v[0] = cv.x; G_.v[1] = cv.y; G_.v[2] = cv.z; G_.v[3] = cv.w;
+                if (has_conn) {   // node ids: only the global gathers use them
+                    if constexpr (D == 3) {
+                        const int4 cv = *reinterpret_cast<const int4*>(sconn + el * 4);
+                        G_.v[0] = cv.x; G_.v[1] = cv.y; G_.v[2] = cv.z; G_.v[3] = cv.w;
+                    } else {
+#pragma unroll
+                        for (int a = 0; a <= D; ++a) G_.v[a] = sconn[el * NV + a];
+                    }
                 } else {
 #pragma unroll
-                    for (int a = 0; a <= D; ++a) G_.v[a] = sconn[el * NV + a];
+                    for (int a = 0; a <= D; ++a) G_.v[a] = 0;
                 }
 #pragma unroll
                 for (int a = 0; a < D; ++a)
@@ -566,10 +577,10 @@ k_assemble(const AsmParams<T> p) {
                 if ((pref || has_mat) && tn < p.n_blocks) {
                     mbar_wait(&s_bar[cur ^ 1], cur ? par0 : par1);
                     if (pref)
-                        stage_fields<D, T, NT, ST, MASKED>(ustage + ust_sz * (cur ^ 1), sg_nxt, staged_src, p, 0, S,
+                        stage_fields<D, T, NT, ST, MASKED>(ustage + ust_sz * (cur ^ 1), sg_nxt, p.rec_base, staged_src, p, 0, S,
                                                            __ldg(p.blk_occ + tn + 1) - __ldg(p.blk_occ + tn));
                     if (has_mat)
-                        stage_material<T, NT>(mstage + 2 * EB * (cur ^ 1), sg_nxt, p, tn);
+                        stage_material<T, NT>(mstage + 2 * EB * (cur ^ 1), sg_nxt, p.rec_base, p, tn);
                 }
                 cp_commit();
             }

@@ -43,10 +43,11 @@ __device__ __forceinline__ void prefetch_record(const AsmParams<T>& p, int b) {
     // the fields the direct kernel reads: gradients .. occ_seg, without conn; fp32 (ent_pos
     // layout) skips loc_ent, fp64 skips ent_pos
     if (sizeof(T) == 4) {
+        l2_prefetch(p.recs, total, (size_t)b * rb + p.rec.ent_pos, p.rec.conn - p.rec.ent_pos);
         l2_prefetch(p.recs, total, (size_t)b * rb + p.rec.g, p.rec.loc_ent - p.rec.g);
         l2_prefetch(p.recs, total, (size_t)b * rb + p.rec.lconn, rb - p.rec.lconn);
     } else {
-        l2_prefetch(p.recs, total, (size_t)b * rb + p.rec.g, p.rec.ent_pos - p.rec.g);
+        l2_prefetch(p.recs, total, (size_t)b * rb + p.rec.g, rb - p.rec.g);
     }
     const int e0 = __ldg(p.blk_elem + b), e1 = __ldg(p.blk_elem + b + 1);
     const size_t E = (size_t)p.E, ne = (size_t)(e1 - e0);
@@ -127,10 +128,10 @@ k_assemble_direct(const AsmParams<T> p) {
     for (int s0 = 0; s0 < S; s0 += ST) {
         const int nq = min(ST, S - s0);
         if (OP == OP_TANGENT) {
-            stage_fields<D, T, NT, ST, MASKED>(ust, rg, p.v, p, s0, nq, no);
-            if (NF == 2) stage_fields<D, T, NT, ST, false>(ust + ust_sz, rg, p.u, p, s0, nq, no);
+            stage_fields<D, T, NT, ST, MASKED>(ust, rg, 0u, p.v, p, s0, nq, no);
+            if (NF == 2) stage_fields<D, T, NT, ST, false>(ust + ust_sz, rg, 0u, p.u, p, s0, nq, no);
         } else {
-            stage_fields<D, T, NT, ST, false>(ust, rg, p.u, p, s0, nq, no);
+            stage_fields<D, T, NT, ST, false>(ust, rg, 0u, p.u, p, s0, nq, no);
         }
         cp_commit();
         T wacc[ST];

@@ -85,6 +85,7 @@ AsmParams<T> make_params(const Call& c) {
     p.n_fix = P.n_fix;
     p.perm = P.elem_perm != nullptr;
     p.rec = P.rec;
+    p.rec_base = 0;
     p.recs = P.recs;
     const WsLayout L = ws_layout(P, c.S, sizeof(T));
     char* w = (char*)c.ws;
@@ -141,7 +142,11 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
     constexpr int EB = EbOf<D>::value;
     constexpr int NT = ASM_NT;
     constexpr int NF = 1;
-    const size_t smem = 2 * (size_t)p.rec.bytes + 4 * EB * sizeof(T) +
+    // the staged copy skips ent_pos, and conn too when the fields are staged and the NH
+    // state u is not gathered
+    const bool need_conn = p.S > ST || (OP == OP_TANGENT && MODEL == MODEL_NH);
+    p.rec_base = need_conn ? p.rec.conn : p.rec.g;
+    const size_t smem = 2 * (size_t)(p.rec.bytes - p.rec_base) + 4 * EB * sizeof(T) +
                         2 * (size_t)NF * p.rec.ocap * D * ST * sizeof(T) +
                         (HAS_FORCE ? (size_t)ST * D * (D + 1) * EB * sizeof(T) : 0);
     auto kern = k_assemble<D, MODEL, T, OP, ST, MASKED, EB, NT>;
