@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define PFEM_ABI_VERSION 2
+#define PFEM_ABI_VERSION 3
 
 typedef enum {
     PFEM_OK = 0,
@@ -246,6 +246,36 @@ pfem_status pfem_cg(const pfem_mesh* m, const pfem_material* mat, const void* u_
                     const void* rhs, const uint8_t* mask, void* x, double tol, int32_t max_iter,
                     int32_t mode, double* history, pfem_cg_report* report, void* ws,
                     size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * Newton-Raphson for the nonlinear (Neo-Hookean) warm-start stage (App. B P:1118-1139,
+ * warm start U_0 = U^NO P:1141-1166; §8(f) row f1).  One load step, dead loads (K^ext = 0):
+ *   r(U_k) = f_int(U_k) - f_ext  on free DOFs;  stop when ||r||_2 <= tol  (absolute)
+ *   dU solves K(U_k) dU = -r with the masked CG of pfem_cg (x0 = 0, relative tolerance
+ *   cg_tol, at most cg_max_iter products); constrained DOFs keep their values in u
+ *   U_{k+1} = U_k + dU
+ *   u        in: U_0 (constrained entries = prescribed values); out: the last iterate [N][d]
+ *   f_ext    nullable [N][d]
+ *   history  nullable HOST double [max_newton+1]: ||r(U_k)||
+ *   report   host; iterations = Newton steps taken (0 if U_0 already satisfies the test)
+ * Synchronises `stream` once per Newton step.  Returns PFEM_OK, PFEM_ERR_NOT_CONVERGED
+ * (max_newton reached or non-finite residual) or PFEM_ERR_BREAKDOWN (indefinite tangent
+ * met by the inner CG); the report is filled in every case.
+ * --------------------------------------------------------------------------------- */
+typedef struct {
+    int32_t iterations;
+    int32_t converged;
+    int32_t status;            /* 0 converged, 1 max_newton, 2 CG breakdown, 3 non-finite    */
+    int32_t cg_iterations;     /* inner CG products summed over the Newton steps             */
+    double res0;               /* ||r(U_0)||                                                 */
+    double res_final;          /* ||r|| of the last iterate                                  */
+} pfem_newton_report;
+
+size_t pfem_newton_workspace_bytes(const pfem_mesh* m);
+pfem_status pfem_newton(const pfem_mesh* m, const pfem_material* mat, void* u, const void* f_ext,
+                        const uint8_t* mask, double tol, int32_t max_newton, double cg_tol,
+                        int32_t cg_max_iter, int32_t mode, double* history,
+                        pfem_newton_report* report, void* ws, size_t ws_bytes, void* stream);
 
 /* Diagnostics */
 const char* pfem_last_error(void);

@@ -209,6 +209,41 @@ class Mesh:
         lib().oracle_set_dot_order(C.c_int(0))
         return x.reshape(np.shape(x0)), rep
 
+    def newton(self, u0, f_ext=None, mask=None, tol=1e-8, max_newton=20, cg_tol=1e-12, cg_max_iter=50000):
+        """Newton-Raphson, App. B, one load step with dead loads (K^ext = 0):
+            r(U_k) = f_int(U_k) - f_ext                      (free DOFs)
+            stop when ||r|| <= tol                             (absolute 2-norm)
+            dU = -(K^geo + K^mat)^{-1} r(U_k)                  (oracle masked CG, rel. tol cg_tol)
+            U_{k+1} = U_k + dU
+        Constrained DOFs keep their values from u0.  Returns (U, report with the history of
+        ||r(U_k)||)."""
+        u = _f64(u0).reshape(self.n_nodes, self.dim).copy()
+        fe = np.zeros_like(u) if f_ext is None else _f64(f_ext).reshape(u.shape)
+        free = np.ones(u.size, bool) if mask is None else np.asarray(mask).reshape(-1) == 0
+        hist, cg_its, status = [], 0, 1
+        for k in range(max_newton + 1):
+            r = (self.residual(u)[0] - fe).reshape(-1)
+            r[~free] = 0.0
+            nr = float(np.sqrt(r @ r))
+            hist.append(nr)
+            if not np.isfinite(nr):
+                status = 3
+                break
+            if nr <= tol:
+                status = 0
+                break
+            if k == max_newton:
+                break
+            du, rep = self.cg(-r.reshape(u.shape), mask, np.zeros_like(u), tol=cg_tol, max_iter=cg_max_iter,
+                              u_state=u if self.model == "neohookean" else None, history=False)
+            cg_its += rep["iterations"]
+            if rep["status"] == ERR_BREAKDOWN:
+                status = 2
+                break
+            u = u + du.reshape(u.shape)
+        return u, {"iterations": len(hist) - 1, "converged": status == 0, "exit": status, "history": np.array(hist),
+                   "cg_iterations": cg_its}
+
     def cg_spread(self, f, mask, x0, tol=1e-8, max_iter=50000, u_state=None):
         """Iteration counts of the oracle CG under the five dot-product orders (R18)."""
         return [self.cg(f, mask, x0, tol, max_iter, u_state, history=False, dot_order=o)[1]["iterations"]

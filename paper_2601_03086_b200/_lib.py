@@ -49,6 +49,11 @@ class pfem_cg_report(C.Structure):
                 ("true_rel_res_final", C.c_double), ("bnorm", C.c_double)]
 
 
+class pfem_newton_report(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("status", C.c_int32),
+                ("cg_iterations", C.c_int32), ("res0", C.c_double), ("res_final", C.c_double)]
+
+
 class PfemError(RuntimeError):
     def __init__(self, status: int, message: str, index: int):
         super().__init__(f"{STATUS.get(status, status)}: {message} (index {index})")
@@ -78,6 +83,10 @@ SIGNATURES = {
     "pfem_cg": (C.c_int, [C.POINTER(pfem_mesh), C.POINTER(pfem_material), C.c_void_p, C.c_void_p, C.c_void_p,
                           C.c_void_p, C.c_double, C.c_int32, C.c_int32, C.c_void_p, C.POINTER(pfem_cg_report),
                           C.c_void_p, C.c_size_t, C.c_void_p]),
+    "pfem_newton_workspace_bytes": (C.c_size_t, [C.POINTER(pfem_mesh)]),
+    "pfem_newton": (C.c_int, [C.POINTER(pfem_mesh), C.POINTER(pfem_material), C.c_void_p, C.c_void_p, C.c_void_p,
+                              C.c_double, C.c_int32, C.c_double, C.c_int32, C.c_int32, C.c_void_p,
+                              C.POINTER(pfem_newton_report), C.c_void_p, C.c_size_t, C.c_void_p]),
     "pfem_last_error": (C.c_char_p, []),
     "pfem_last_error_index": (C.c_int64, []),
     "pfem_abi_version": (C.c_int32, []),

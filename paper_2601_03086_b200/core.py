@@ -119,6 +119,14 @@ class Mesh:
             self._ws["cg"] = ws
         return ws
 
+    def newton_workspace(self) -> torch.Tensor:
+        ws = self._ws.get("newton")
+        if ws is None:
+            nb = L.load().pfem_newton_workspace_bytes(self.ref())
+            ws = torch.zeros(max(nb, 1), dtype=torch.uint8, device=self.coords.device)
+            self._ws["newton"] = ws
+        return ws
+
     def plan_export(self):
         """Host copies of the assembly plan (tests)."""
         import numpy as np
@@ -250,6 +258,28 @@ def cg(mesh: Mesh, mat: Material, f: torch.Tensor, x0: torch.Tensor, mask=None, 
     if st not in (L.PFEM_OK, -4, -5):
         L.check(st)
     return x, report
+
+
+def newton(mesh: Mesh, mat: Material, u0: torch.Tensor, f_ext=None, mask=None, tol: float = 1e-8,
+           max_newton: int = 20, cg_tol: float = 1e-10, cg_max_iter: int = 50000, mode: str = "csr"):
+    """pfem_newton: Newton-Raphson from u0 (constrained entries = prescribed values);
+    returns (u, report dict with the residual-norm history)."""
+    import numpy as np
+    u = _field(mesh, u0)[0].clone()
+    f = None if f_ext is None else _field(mesh, f_ext)[0]
+    hist = np.zeros(max_newton + 1, np.float64)
+    rep = L.pfem_newton_report()
+    ws = mesh.newton_workspace()
+    mc = mat.c()
+    st = L.load().pfem_newton(mesh.ref(), C.byref(mc), _ptr(u), _ptr(f), _ptr(mask), tol, max_newton, cg_tol,
+                              cg_max_iter, MODES[mode], hist.ctypes.data, C.byref(rep), _ptr(ws), ws.numel(),
+                              _stream())
+    report = {"status": st, "iterations": rep.iterations, "converged": bool(rep.converged),
+              "exit": rep.status, "cg_iterations": rep.cg_iterations, "res0": rep.res0,
+              "res_final": rep.res_final, "history": hist[: rep.iterations + 1].copy()}
+    if st not in (L.PFEM_OK, -4, -5):
+        L.check(st)
+    return u, report
 
 
 def launch_count(reset: bool = False) -> int:

@@ -26,6 +26,10 @@ void count_launch(int n) { g_launches += n; }
 pfem_status prepare_impl(pfem_mesh* m, cudaStream_t s);
 void release_impl(pfem_mesh* m);
 size_t cg_ws_bytes(const Plan& P, int dtype);
+size_t newton_ws_bytes(const Plan& P, int dtype);
+pfem_status run_newton(const pfem_mesh* m, const pfem_material* mat, void* u, const void* fext, const uint8_t* mask,
+                       double tol, int max_newton, double cg_tol, int cg_max_iter, int mode, double* history,
+                       pfem_newton_report* rep, void* ws, cudaStream_t s);
 pfem_status run_cg(const pfem_mesh* m, const pfem_material* mat, const void* u_state, const void* rhs,
                    const uint8_t* mask, void* x, double tol, int max_iter, int mode, double* history,
                    pfem_cg_report* rep, void* ws, cudaStream_t s);
@@ -266,6 +270,30 @@ pfem_status pfem_cg(const pfem_mesh* m, const pfem_material* mat, const void* u_
     if (ws_bytes < pfem_cg_workspace_bytes(m)) { set_error("pfem_cg: workspace too small"); return PFEM_ERR_CAPACITY; }
     memset(report, 0, sizeof(*report));
     return run_cg(m, mat, u_state, rhs, mask, x, tol, max_iter, mode, history, report, ws, (cudaStream_t)stream);
+}
+
+size_t pfem_newton_workspace_bytes(const pfem_mesh* m) {
+    if (check_mesh(m, true) != PFEM_OK) return 0;
+    return newton_ws_bytes(*reinterpret_cast<const Plan*>(m->plan), m->dtype);
+}
+
+pfem_status pfem_newton(const pfem_mesh* m, const pfem_material* mat, void* u, const void* f_ext,
+                        const uint8_t* mask, double tol, int32_t max_newton, double cg_tol, int32_t cg_max_iter,
+                        int32_t mode, double* history, pfem_newton_report* report, void* ws, size_t ws_bytes,
+                        void* stream) {
+    pfem_status st = check_mesh(m, true);
+    if (st) return st;
+    if ((st = check_mat(mat))) return st;
+    if (!u || !report || !ws) { set_error("pfem_newton: NULL argument"); return PFEM_ERR_ARG; }
+    if (!(tol >= 0.0) || !(cg_tol >= 0.0) || max_newton < 0 || cg_max_iter < 0) {
+        set_error("pfem_newton: bad tol / iteration limits");
+        return PFEM_ERR_ARG;
+    }
+    if (mode != PFEM_ASSEMBLE_CSR && mode != PFEM_ASSEMBLE_COLOUR) { set_error("bad assembly mode"); return PFEM_ERR_ARG; }
+    if (ws_bytes < pfem_newton_workspace_bytes(m)) { set_error("pfem_newton: workspace too small"); return PFEM_ERR_CAPACITY; }
+    memset(report, 0, sizeof(*report));
+    return run_newton(m, mat, u, f_ext, mask, tol, max_newton, cg_tol, cg_max_iter, mode, history, report, ws,
+                      (cudaStream_t)stream);
 }
 
 }  // extern "C"

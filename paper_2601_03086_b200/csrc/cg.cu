@@ -390,6 +390,176 @@ pfem_status cg_impl(const pfem_mesh* m, const pfem_material* mat, const void* u_
     return PFEM_OK;
 }
 
+// ====================================================================================
+// Newton-Raphson (App. B, warm start P:1141-1166; §8(f) row f1):
+//   r(U_k) = f_int(U_k) - f_ext on free DOFs;  stop when ||r|| <= tol;
+//   K(U_k) dU = -r by the masked CG above (dU = 0 on constrained DOFs, x0 = 0, relative
+//   tolerance cg_tol; K^ext = 0: dead loads);  U_{k+1} = U_k + dU.
+// One host sync per Newton step (the residual norm decides the loop).
+
+// rhs = f_ext - f_int on free DOFs (0 on constrained), ||rhs||^2 -> *out
+template <class T>
+__global__ void __launch_bounds__(VEC_NT)
+k_newton_rhs(int64_t n, const uint8_t* __restrict__ mask, const T* __restrict__ fext, const T* __restrict__ fint,
+             T* __restrict__ rhs, VecRed* vr, double* out) {
+    __shared__ double s_red[VEC_NT / 32];
+    __shared__ int s_flag;
+    double acc = 0.0;
+    VEC_PASSES(n) {
+        T fe[VEC_U], fi[VEC_U];
+        uint8_t mk[VEC_U];
+#pragma unroll
+        for (int u = 0; u < VEC_U; ++u) {
+            const int64_t i = VEC_IDX(u);
+            if (i < n) {
+                fe[u] = fext ? fext[i] : T(0);
+                fi[u] = fint[i];
+                mk[u] = mask ? mask[i] : 0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < VEC_U; ++u) {
+            const int64_t i = VEC_IDX(u);
+            if (i >= n) break;
+            const T v = mk[u] ? T(0) : fe[u] - fi[u];
+            rhs[i] = v;
+            acc += (double)v * (double)v;
+        }
+    }
+    if (!vec_last_block(vr, acc, s_red, &s_flag)) return;
+    const double t = vec_final(vr, s_red);
+    if (threadIdx.x == 0) *out = t;
+}
+
+template <class T>
+__global__ void __launch_bounds__(VEC_NT)
+k_newton_add(int64_t n, const T* __restrict__ du, T* __restrict__ u) {
+    VEC_PASSES(n) {
+        T a[VEC_U], b[VEC_U];
+#pragma unroll
+        for (int k = 0; k < VEC_U; ++k) {
+            const int64_t i = VEC_IDX(k);
+            if (i < n) { a[k] = u[i]; b[k] = du[i]; }
+        }
+#pragma unroll
+        for (int k = 0; k < VEC_U; ++k) {
+            const int64_t i = VEC_IDX(k);
+            if (i < n) u[i] = a[k] + b[k];
+        }
+    }
+}
+
+struct NewtonWs {
+    size_t cg, fint, rhs, du, red, total;
+};
+
+inline NewtonWs newton_layout(const Plan& P, size_t tsize) {
+    NewtonWs L;
+    size_t o = 0;
+    const size_t nvec = align_up(tsize * (size_t)P.n_nodes * P.dim, 256);
+    L.cg = o;   o += align_up(cg_layout(P, tsize).total, 256);
+    L.fint = o; o += nvec;
+    L.rhs = o;  o += nvec;
+    L.du = o;   o += nvec;
+    L.red = o;  o += align_up(sizeof(VecRed) + 256, 256);
+    L.total = o;
+    return L;
+}
+
+size_t newton_ws_bytes(const Plan& P, int dtype) {
+    return newton_layout(P, dtype == PFEM_F64 ? 8 : 4).total;
+}
+
+template <int D, class T>
+pfem_status newton_impl(const pfem_mesh* m, const pfem_material* mat, void* uv, const void* fext,
+                        const uint8_t* mask, double tol, int max_newton, double cg_tol, int cg_max_iter, int mode,
+                        double* history, pfem_newton_report* rep, void* ws, cudaStream_t s) {
+    const Plan* P = reinterpret_cast<const Plan*>(m->plan);
+    const NewtonWs L = newton_layout(*P, sizeof(T));
+    char* w = (char*)ws;
+    void* cgws = w + L.cg;
+    void* asmws = w + L.cg + cg_layout(*P, sizeof(T)).asmws;
+    T* fint = (T*)(w + L.fint);
+    T* rhs = (T*)(w + L.rhs);
+    T* du = (T*)(w + L.du);
+    VecRed* vr = (VecRed*)(w + L.red);
+    double* nrm = (double*)(w + L.red + sizeof(VecRed));
+    T* u = (T*)uv;
+    const int64_t n = (int64_t)P->n_nodes * D;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int G = std::min(VEC_MAX_GRID, 8 * nsm);
+    PFEM_CUDA_TRY(cudaMemsetAsync(vr, 0, sizeof(int32_t), s));
+    for (int k = 0;; ++k) {
+        // r = f_int(U_k) - f_ext (free DOFs)
+        Call c{};
+        c.m = m;
+        c.P = P;
+        c.op = OP_RESIDUAL;
+        c.model = mat->model;
+        c.mode = mode;
+        c.S = 1;
+        c.sstride = n;
+        c.mat = *mat;
+        c.u = u;
+        c.out = fint;
+        c.ws = asmws;
+        c.stream = s;
+        pfem_status e = run_assemble<D, T>(c);
+        if (e != PFEM_OK) return e;
+        k_newton_rhs<T><<<G, VEC_NT, 0, s>>>(n, mask, (const T*)fext, fint, rhs, vr, nrm);
+        PFEM_LAUNCH_CHECK("k_newton_rhs");
+        double r2 = 0.0;
+        PFEM_CUDA_TRY(cudaMemcpyAsync(&r2, nrm, sizeof(double), cudaMemcpyDeviceToHost, s));
+        PFEM_CUDA_TRY(cudaStreamSynchronize(s));
+        const double rn = sqrt(r2);
+        if (history) history[k] = rn;
+        if (k == 0) rep->res0 = rn;
+        rep->res_final = rn;
+        rep->iterations = k;
+        if (!(rn == rn)) {
+            rep->status = 3;
+            set_error("Newton: non-finite residual (inverted elements?)");
+            return PFEM_ERR_NOT_CONVERGED;
+        }
+        if (rn <= tol) {
+            rep->converged = 1;
+            rep->status = 0;
+            return PFEM_OK;
+        }
+        if (k >= max_newton) {
+            rep->status = 1;
+            set_error("Newton did not converge within max_newton");
+            return PFEM_ERR_NOT_CONVERGED;
+        }
+        // K(U_k) dU = f_ext - f_int  (x0 = 0, so the constrained entries of dU stay 0)
+        PFEM_CUDA_TRY(cudaMemsetAsync(du, 0, sizeof(T) * (size_t)n, s));
+        pfem_cg_report crep{};
+        e = cg_impl<D, T>(m, mat, u, rhs, mask, du, cg_tol, cg_max_iter, mode, nullptr, &crep, cgws, s);
+        rep->cg_iterations += crep.iterations;
+        if (e == PFEM_ERR_BREAKDOWN) {
+            rep->status = 2;
+            return e;
+        }
+        if (e != PFEM_OK && e != PFEM_ERR_NOT_CONVERGED) return e;   // an inexact step still progresses
+        k_newton_add<T><<<G, VEC_NT, 0, s>>>(n, du, u);
+        PFEM_LAUNCH_CHECK("k_newton_add");
+    }
+}
+
+pfem_status run_newton(const pfem_mesh* m, const pfem_material* mat, void* u, const void* fext, const uint8_t* mask,
+                       double tol, int max_newton, double cg_tol, int cg_max_iter, int mode, double* history,
+                       pfem_newton_report* rep, void* ws, cudaStream_t s) {
+    if (m->dim == 2)
+        return m->dtype == PFEM_F32
+                   ? newton_impl<2, float>(m, mat, u, fext, mask, tol, max_newton, cg_tol, cg_max_iter, mode, history, rep, ws, s)
+                   : newton_impl<2, double>(m, mat, u, fext, mask, tol, max_newton, cg_tol, cg_max_iter, mode, history, rep, ws, s);
+    return m->dtype == PFEM_F32
+               ? newton_impl<3, float>(m, mat, u, fext, mask, tol, max_newton, cg_tol, cg_max_iter, mode, history, rep, ws, s)
+               : newton_impl<3, double>(m, mat, u, fext, mask, tol, max_newton, cg_tol, cg_max_iter, mode, history, rep, ws, s);
+}
+
 pfem_status run_cg(const pfem_mesh* m, const pfem_material* mat, const void* u_state, const void* rhs,
                    const uint8_t* mask, void* x, double tol, int max_iter, int mode, double* history,
                    pfem_cg_report* rep, void* ws, cudaStream_t s) {

@@ -1,9 +1,9 @@
 """Seeded synthetic input generators (no PFEM arithmetic; shared by tests, bench, smoke)."""
 from .configs import (CONFIGS, Problem, config1, config2, config3, config4, config5,
-                      small_cube_problem, traction_load, warm_start)
+                      newton_block, small_cube_problem, traction_load, warm_start)
 from .meshes import (boundary_faces_on_plane, fourier_field, kuhn_cube, plate_with_holes,
                      square_t3)
 
 __all__ = ["CONFIGS", "Problem", "config1", "config2", "config3", "config4", "config5",
-           "small_cube_problem", "traction_load", "warm_start", "boundary_faces_on_plane",
+           "small_cube_problem", "newton_block", "traction_load", "warm_start", "boundary_faces_on_plane",
            "fourier_field", "kuhn_cube", "plate_with_holes", "square_t3"]

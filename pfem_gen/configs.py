@@ -194,4 +194,21 @@ def small_cube_problem(n_nodes: int = 12, seed_base: int = 4000, brick: int | No
     return config4(seed_base=seed_base, n_nodes=n_nodes, brick=brick, n_spheres=n_spheres)
 
 
+def newton_block(n_nodes: int = 9, traction=(0.02, 0.0, 0.01), mu: float = 0.4, lam: float = 0.6,
+                 dtype: str = "f64", brick: int | None = None) -> Problem:
+    """Nonlinear warm-start workload (§8(f) row f1; the paper's hyperelastic cantilever /
+    Cook-type rows): unit cube of n_nodes^3 nodes, Kuhn T4, compressible
+    Neo-Hookean (mu, lambda uniform), bottom face z = 0 clamped, uniform dead traction on the
+    top face z = 1 (shear + tension, large enough that Newton needs several steps).  S = 1;
+    ``u`` holds the zero start."""
+    coords, conn = kuhn_cube(n_nodes, brick=brick)
+    top = boundary_faces_on_plane(conn, coords, 2, 1.0)
+    f_ext = traction_load(coords, top, traction)
+    mask = np.zeros((len(coords), 3), np.uint8)
+    mask[np.abs(coords[:, 2]) < 1e-12, :] = 1
+    u = np.zeros((1,) + coords.shape)
+    return Problem("newton_block", 3, coords, conn, "neohookean", "lame", np.array([mu]), np.array([lam]),
+                   u, dtype, f_ext=f_ext, mask=mask.ravel())
+
+
 CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}

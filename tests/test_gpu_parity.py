@@ -333,3 +333,44 @@ def test_cg_config4_scaled(orc, n):
             assert_cg_count(rep, ro, om.cg_spread(p.f_ext, p.mask, x0, tol=1e-8))
             assert rep["true_rel_res_final"] < 2e-8
             assert rel_l2(x.cpu().numpy(), xo) < 1e-6
+
+
+# ------------------------------------------------------------------ Newton (§8(f) row f1)
+@pytest.mark.parametrize("order", ["input", "locality"])
+def test_newton_matches_oracle(orc, order):
+    """pfem_newton vs the oracle's Newton on a Neo-Hookean block (fp64): the same number of
+    Newton steps, residual histories within 1e-9 relative while above the rounding floor, and
+    the converged U within 1e-9 relative (inner CG at 1e-12)."""
+    import paper_2601_03086_b200 as pf
+    from pfem_gen import newton_block
+    p = newton_block(7, traction=(0.05, 0.0, 0.02))
+    mesh, mat, u = gpu_problem(p, elem_order=order)
+    om = oracle_problem(orc, p)
+    f = torch.as_tensor(p.f_ext, device="cuda")
+    mask = torch.as_tensor(p.mask, device="cuda")
+    tol = 1e-10
+    ug, rg = pf.newton(mesh, mat, u[0], f_ext=f, mask=mask, tol=tol, cg_tol=1e-12)
+    uo, ro = om.newton(p.u[0], p.f_ext, p.mask, tol=tol, cg_tol=1e-12)
+    assert rg["converged"] and ro["converged"]
+    assert rg["iterations"] == ro["iterations"], (rg["history"], ro["history"])
+    ho, hg = ro["history"], rg["history"]
+    big = ho > 1e-6 * ho[0]
+    assert np.max(np.abs(hg[big] - ho[big]) / ho[big]) < 1e-9
+    assert rel_l2(ug.cpu().numpy(), uo) < 1e-9
+    # warm start from the converged solution: zero Newton steps
+    _, r1 = pf.newton(mesh, mat, ug, f_ext=f, mask=mask, tol=10 * tol, cg_tol=1e-12)
+    assert r1["iterations"] == 0 and r1["converged"]
+
+
+def test_newton_linear_one_step_gpu(orc):
+    """Linear model: one Newton step reaches the CG solution (config 1)."""
+    import paper_2601_03086_b200 as pf
+    p = config1()
+    mesh, mat, _ = gpu_problem(p)
+    f = torch.as_tensor(p.f_ext, device="cuda")
+    mask = torch.as_tensor(p.mask, device="cuda")
+    b = np.linalg.norm(p.f_ext.ravel() * (1 - p.mask))
+    u, rep = pf.newton(mesh, mat, torch.zeros_like(f), f_ext=f, mask=mask, tol=1e-9 * b, cg_tol=1e-13)
+    x, _ = pf.cg(mesh, mat, f, torch.zeros_like(f), mask=mask, tol=1e-13)
+    assert rep["converged"] and rep["iterations"] == 1
+    assert rel_l2(u.cpu().numpy(), x.cpu().numpy()) < 1e-10

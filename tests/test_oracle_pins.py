@@ -499,3 +499,76 @@ def test_cg_history_and_breakdown_conventions(orc):
     assert len(h) == rep["iterations"] + 1
     assert abs(h[0] - 1.0) < 1e-15                      # zero start: r0 = b
     assert h[-1] < 1e-6 and np.all(h[:-1] >= 1e-6)
+
+
+# ---------------------------------------------------------------- Newton (§8(f) row f1)
+def _potential(m, u, f):
+    """Pi(U) = W(U) - f.U (App. B / P:164, the energy the residual differentiates)."""
+    _, tot = m.energy(u.reshape(1, m.n_nodes, m.dim), f_ext=f, want_elem=False)
+    return float(tot.sum())
+
+
+def test_newton_linear_is_one_step(orc):
+    """K does not depend on U for the linear model, so Newton from U_0 = 0
+    lands on the dense solution in one step (config 1, dense Cholesky of the masked K)."""
+    p = config1()
+    m = orc.prepare_problem(p)
+    n = p.n_nodes * 2
+    A = dense_K(m, n, mask=p.mask)
+    b = p.f_ext.ravel() * (1 - p.mask)
+    xs = np.linalg.solve(A, b)
+    tol = 1e-9 * np.linalg.norm(b)
+    u, rep = m.newton(np.zeros_like(p.coords), p.f_ext, p.mask, tol=tol, cg_tol=1e-13)
+    assert rep["converged"] and rep["iterations"] == 1
+    assert rel(u.ravel(), xs) < 1e-9
+    assert abs(rep["history"][0] - np.linalg.norm(b)) < 1e-14 * np.linalg.norm(b)
+
+
+def test_newton_neohookean_quadratic_and_stationary(orc):
+    """Neo-Hookean block under shear + tension: (i) quadratic convergence of the residual
+    norms in the asymptotic range, e_{k+1} <= 10 e_k^2 (a wrong tangent converges at best
+    linearly and fails it); (ii) the converged U makes the potential stationary: central
+    difference of Pi along a random free direction ~ 0, while at U_0 = 0 it is -f.v."""
+    from pfem_gen import newton_block
+    p = newton_block(5, traction=(0.05, 0.0, 0.02))
+    m = orc.prepare_problem(p)
+    u, rep = m.newton(p.u[0], p.f_ext, p.mask, tol=1e-11, cg_tol=1e-13)
+    assert rep["converged"] and 3 <= rep["iterations"] <= 8
+    e = rep["history"] / rep["history"][0]
+    checked = 0
+    for k in range(len(e) - 1):
+        if e[k] < 1e-2 and e[k + 1] > 1e-12:
+            assert e[k + 1] <= 10 * e[k] ** 2, (k, e)
+            checked += 1
+    assert checked >= 1
+    rng = np.random.default_rng(3)
+    v = rng.standard_normal(u.shape) * (1 - p.mask.reshape(u.shape))
+    eps = 1e-5
+    g = (_potential(m, u + eps * v, p.f_ext) - _potential(m, u - eps * v, p.f_ext)) / (2 * eps)
+    g0 = (_potential(m, eps * v, p.f_ext) - _potential(m, -eps * v, p.f_ext)) / (2 * eps)
+    scale = np.linalg.norm(p.f_ext) * np.linalg.norm(v)
+    assert abs(g0 + float(np.sum(p.f_ext * v))) < 1e-6 * scale
+    assert abs(g) < 1e-7 * scale
+
+
+def test_newton_small_load_limit_and_warm_start(orc):
+    """Small loads: the Neo-Hookean solution tends to the linear one with the same (mu, lambda),
+    the gap shrinking linearly with the load; a perturbed-exact start needs fewer Newton steps
+    than a zero start (the warm-start claim)."""
+    from pfem_gen import newton_block, warm_start
+    gaps = []
+    for s in (1e-3, 1e-4):
+        p = newton_block(4, traction=(0.05 * s, 0.0, 0.02 * s))
+        nh = orc.prepare_problem(p)
+        lin = orc.prepare(p.coords, p.conn, "linear", "lame", p.p0, p.p1)
+        un, rn = nh.newton(p.u[0], p.f_ext, p.mask, tol=1e-9 * np.linalg.norm(p.f_ext), cg_tol=1e-13)
+        ul, _ = lin.cg(p.f_ext, p.mask, np.zeros_like(p.coords), tol=1e-13)
+        assert rn["converged"]
+        gaps.append(rel(un, ul))
+    assert gaps[0] < 1e-2 and 0.05 < gaps[1] / gaps[0] < 0.2
+    p = newton_block(5, traction=(0.05, 0.0, 0.02))
+    m = orc.prepare_problem(p)
+    us, _ = m.newton(p.u[0], p.f_ext, p.mask, tol=1e-12, cg_tol=1e-13)
+    _, rz = m.newton(p.u[0], p.f_ext, p.mask, tol=1e-9, cg_tol=1e-12)
+    _, rw = m.newton(warm_start(us, p.mask, seed=77), p.f_ext, p.mask, tol=1e-9, cg_tol=1e-12)
+    assert rw["iterations"] < rz["iterations"]
