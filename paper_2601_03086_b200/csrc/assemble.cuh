@@ -801,6 +801,12 @@ k_node_finish(const AsmParams<T> p, int op_psi, int n_items) {
     __syncthreads();
     if (!s_last) return;
     __threadfence();
+    if (part_totals) {   // parts without elements have no chunk: their totals are 0 (R23)
+        for (int pair = tid; pair < S * p.K; pair += NTB) {
+            const int s = pair / p.K, k = pair - s * p.K;
+            if (__ldg(p.part_chunk + k) == __ldg(p.part_chunk + k + 1)) p.totals[(int64_t)s * p.K + k] = T(0);
+        }
+    }
     if (cgdot && warp == 0) {
         const double pq = warp_sum(lane_sum(p.chunk_sum + (int64_t)(2 * S) * p.n_chunks, 0, p.n_chunks, lane)) +
                           warp_sum(lane_sum(p.blk_sum + (int64_t)(2 * S + 1) * p.n_blocks, 0, (int)gridDim.x, lane));

@@ -374,3 +374,35 @@ def test_newton_linear_one_step_gpu(orc):
     x, _ = pf.cg(mesh, mat, f, torch.zeros_like(f), mask=mask, tol=1e-13)
     assert rep["converged"] and rep["iterations"] == 1
     assert rel_l2(u.cpu().numpy(), x.cpu().numpy()) < 1e-10
+
+
+def test_empty_and_tiny_parts(orc):
+    """Parts with no elements (their nodes, if any, carry no stiffness) get zero totals; a
+    one-element part and a large part in the same launch match the oracle (R23)."""
+    import paper_2601_03086_b200 as pf
+    ca, ta = square_t3(14, 11)
+    cb, tb = square_t3(2, 2)
+    tb = tb[:1]
+    used = np.unique(tb)
+    cb = cb[used]
+    tb = np.searchsorted(used, tb).astype(np.int32)
+    coords = np.concatenate([ca, cb + 2.0])
+    conn = np.concatenate([ta, tb + len(ca)]).astype(np.int32)
+    E, N = len(conn), len(coords)
+    pe = np.array([0, 0, len(ta), len(ta), E, E], np.int32)       # parts 0, 2 and 4 are empty
+    pn = np.array([0, 0, len(ca), len(ca), N, N], np.int32)
+    rng = np.random.default_rng(9)
+    u = 0.01 * rng.standard_normal((2,) + coords.shape)
+    prob = Problem("parts-empty", 2, coords, conn, "neohookean", "lame", np.array([0.4]), np.array([0.6]), u,
+                   "f64", part_elem=pe, part_node=pn)
+    for order in ("input", "locality"):
+        mesh, mat, ut = gpu_problem(prob, elem_order=order)
+        om = oracle_problem(orc, prob)
+        W_ref, tot_ref = om.energy(prob.u)
+        tot, W, r = pf.energy(mesh, mat, ut, elem_energy=True, residual=True)
+        torch.cuda.synchronize()
+        t = tot.cpu().numpy()
+        assert t.shape == (2, 5)
+        assert np.all(t[:, [0, 2, 4]] == 0.0)
+        assert max_rel(t[:, [1, 3]], tot_ref[:, [1, 3]]) < 1e-12
+        assert rel_l2(r.cpu().numpy(), om.residual(prob.u)) < 1e-12
