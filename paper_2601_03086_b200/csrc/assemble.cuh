@@ -34,6 +34,15 @@
 #ifndef PFEM_STAGED_MINB
 #define PFEM_STAGED_MINB 2
 #endif
+#ifndef PFEM_STAGED_EPOS
+#define PFEM_STAGED_EPOS 0
+#endif
+#ifndef PFEM_STAGED_HP2
+#define PFEM_STAGED_HP2 1
+#endif
+#ifndef PFEM_STAGED_L2PF
+#define PFEM_STAGED_L2PF 1
+#endif
 #ifndef PFEM_STAGED_SCALAR
 #define PFEM_STAGED_SCALAR 0
 #endif
@@ -97,7 +106,8 @@ struct AsmParams {
     int n_fix;
     int perm;              // plan positions are a permutation of the input elements
     RecLayout rec;
-    uint32_t rec_base;     // staged kernel: first record byte it copies (rec.conn or rec.g)
+    uint32_t rec_base;     // staged kernel: record bytes [rec_base, rec_end) are copied
+    uint32_t rec_end;      //   (RecLayout: conn / ent_pos / g .. loc_ent / end)
     const unsigned char* recs;
     // workspace
     Counters* ctr;
@@ -143,6 +153,33 @@ __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
+}
+
+// ST per-lane values summed over the warp in one fixed shuffle tree: the first log2(ST)
+// exchanges halve the values each lane carries (a lane keeps the half selected by its lane
+// bit and adds its partner's copy of that half), the remaining ones are plain butterflies.
+// Result q ends in lane q * (32 / ST).  (ST = 4: 6 shuffles instead of 20.)
+template <class T, int ST>
+__device__ __forceinline__ T warp_multi_sum(const T (&v)[ST], int lane) {
+    static_assert(ST == 1 || ST == 2 || ST == 4, "ST");
+    T c;
+    if constexpr (ST == 4) {
+        const bool h = lane & 16;
+        T k0 = h ? v[2] : v[0], k1 = h ? v[3] : v[1];
+        const T s0 = h ? v[0] : v[2], s1 = h ? v[1] : v[3];
+        k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+        k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+        const bool h8 = lane & 8;
+        c = (h8 ? k1 : k0) + __shfl_xor_sync(0xffffffffu, h8 ? k0 : k1, 8);
+    } else if constexpr (ST == 2) {
+        const bool h = lane & 16;
+        c = (h ? v[1] : v[0]) + __shfl_xor_sync(0xffffffffu, h ? v[0] : v[1], 16);
+    } else {
+        c = v[0];
+    }
+#pragma unroll
+    for (int o = 32 / ST / 2; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    return c;
 }
 
 // fixed-order lane-strided sum of a[lo, hi): lane l adds a[lo+l], a[lo+l+32], ... in ascending
@@ -279,7 +316,7 @@ template <int D, class T, int NT>
 __device__ __forceinline__ void stage_block(unsigned char* st, T* mst, uint64_t* bar, const AsmParams<T>& p, int b) {
     if (threadIdx.x == 0) {
         fence_proxy_async();   // earlier generic reads of this buffer precede the async write
-        const uint32_t n = p.rec.bytes - p.rec_base;
+        const uint32_t n = p.rec_end - p.rec_base;
         mbar_expect_tx(bar, n);
         tma_bulk_g2s(st, p.recs + (size_t)b * p.rec.bytes + p.rec_base, n, bar);
     }
@@ -369,6 +406,22 @@ __device__ __forceinline__ void sacc(const T* __restrict__ src, T (&acc)[SD]) {
     }
 }
 
+// acc += b elementwise (registers; fp32 pairs as FADD2)
+template <class T, int SD>
+__device__ __forceinline__ void sacc_reg(const T (&b)[SD], T (&acc)[SD]) {
+    if constexpr (sizeof(T) == 4 && SD % 2 == 0) {
+#pragma unroll
+        for (int c = 0; c < SD / 2; ++c) {
+            F2 a0(acc[2 * c], acc[2 * c + 1]);
+            a0 = a0 + F2(b[2 * c], b[2 * c + 1]);
+            acc[2 * c] = a0.v.x; acc[2 * c + 1] = a0.v.y;
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < SD; ++c) acc[c] += b[c];
+    }
+}
+
 template <int D, class T, int NT, int ST, bool MASKED>
 __device__ __forceinline__ void stage_fields(T* ust, const unsigned char* rec, uint32_t base, const T* src,
                                              const AsmParams<T>& p, int s0, int nq, int no) {
@@ -407,11 +460,16 @@ k_assemble(const AsmParams<T> p) {
     constexpr int NF = 1;    // staged field: u (energy / residual) or v (tangent; the NH state u is gathered)
     using V = std::conditional_t<(sizeof(T) == 4 && ST % 2 == 0 && !PFEM_STAGED_SCALAR), F2, T>;
     constexpr int L = VTraits<V>::L;
-    using A2 = std::conditional_t<(sizeof(T) == 4 && SD % 2 == 0), F2, T>;     // phase-2 accumulator
-    constexpr int LA = VTraits<A2>::L;
+    // EPOS (fp32): fbuf[(d+1) EB entries][D][ST], each element vertex's forces stored at its
+    // block-CSR entry (ent_pos), so an occurrence's entries are contiguous in phase 2.
+    // !EPOS (fp64): fbuf[NV][EB][D][ST] in element order, gathered through loc_ent.
+    constexpr bool EPOS = sizeof(T) == 4 && PFEM_STAGED_EPOS;
+    constexpr int HP = (sizeof(T) == 4 && ST == 4 && D == 3 && !EPOS && PFEM_STAGED_HP2) ? 2 : 1;   // phase-2 threads per occurrence
+    constexpr int STH = ST / HP;
+    constexpr int SDH = D * STH;
     const T* staged_src = (OP == OP_TANGENT) ? p.v : p.u;
     // shared layout: rec[2] | mat[2][2][EB] | ust[2][OCAP][D][ST] | fbuf[NV][EB][D][ST]
-    const uint32_t srb = p.rec.bytes - p.rec_base;   // staged bytes of a record
+    const uint32_t srb = p.rec_end - p.rec_base;     // staged bytes of a record
     const bool has_conn = p.rec_base <= p.rec.conn;   // conn is staged (gathers, NH tangent state)
     unsigned char* const stage0 = smem_raw;
     unsigned char* const stage1 = smem_raw + srb;
@@ -460,6 +518,12 @@ k_assemble(const AsmParams<T> p) {
         unsigned char* const sg_nxt = cur ? stage0 : stage1;
         if (tn < p.n_blocks) stage_block<D, T, NT>(sg_nxt, mstage + 2 * EB * (cur ^ 1), &s_bar[cur ^ 1], p, tn);
         else cp_commit();
+        if (PFEM_STAGED_L2PF && tid == 32 && tn + G < p.n_blocks) {
+            // the record after next into L2, so next iteration's bulk copy is an L2 hit
+            const size_t rb = p.rec.bytes, off = (size_t)(tn + G) * rb + p.rec_base;
+            const uintptr_t a0 = (uintptr_t)(p.recs + off), a1 = (uintptr_t)(p.recs + off + (p.rec_end - p.rec_base));
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((unsigned)(a1 - a0)) : "memory");
+        }
         const int e0 = __ldg(p.blk_elem + b), ne = __ldg(p.blk_elem + b + 1) - e0;
         const int o0 = __ldg(p.blk_occ + b), no = __ldg(p.blk_occ + b + 1) - o0;
         const unsigned char* sg = sg_cur - p.rec_base;   // record byte offsets apply from here
@@ -470,6 +534,7 @@ k_assemble(const AsmParams<T> p) {
         const uint16_t* soe = reinterpret_cast<const uint16_t*>(sg + p.rec.occ_ent);
         const uint16_t* sle = reinterpret_cast<const uint16_t*>(sg + p.rec.loc_ent);
         const uint16_t* slc = reinterpret_cast<const uint16_t*>(sg + p.rec.lconn);
+        const uint16_t* sep = reinterpret_cast<const uint16_t*>(sg + p.rec.ent_pos);   // valid iff EPOS
         const int32_t* sseg = reinterpret_cast<const int32_t*>(sg + p.rec.occ_seg);
         const int32_t* seid = reinterpret_cast<const int32_t*>(sg + p.rec.eid);
         const T* smat = mstage + 2 * EB * cur;
@@ -515,9 +580,21 @@ k_assemble(const AsmParams<T> p) {
                     G_.mu *= G_.V;
                     G_.lam *= G_.V;
                 }
-                int lv[NV];
+                int lv[NV], ep[NV];   // vertex -> staged occurrence, vertex -> block-CSR entry
+                if constexpr (D == 3) {
+                    const uint2 c = *reinterpret_cast<const uint2*>(slc + el * NV);
+                    lv[0] = c.x & 0xffff; lv[1] = c.x >> 16; lv[2] = c.y & 0xffff; lv[3] = c.y >> 16;
+                    if (EPOS) {
+                        const uint2 q = *reinterpret_cast<const uint2*>(sep + el * NV);
+                        ep[0] = q.x & 0xffff; ep[1] = q.x >> 16; ep[2] = q.y & 0xffff; ep[3] = q.y >> 16;
+                    }
+                } else {
 #pragma unroll
-                for (int a = 0; a < NV; ++a) lv[a] = slc[el * NV + a];
+                    for (int a = 0; a < NV; ++a) {
+                        lv[a] = slc[el * NV + a];
+                        if (EPOS) ep[a] = sep[el * NV + a];
+                    }
+                }
 #pragma unroll
                 for (int qq = 0; qq < ST; qq += L) {
                     if (qq >= nq || (p.dbg & 1)) break;
@@ -565,13 +642,22 @@ k_assemble(const AsmParams<T> p) {
                         for (int a = 0; a < NV; ++a)
 #pragma unroll
                             for (int i = 0; i < D; ++i)
-                                *reinterpret_cast<V*>(fbuf + (((size_t)a * EB + el) * D + i) * ST + qq) = f[a][i];
+                                *reinterpret_cast<V*>(fbuf + ((size_t)(EPOS ? ep[a] : a * EB + el) * D + i) * ST + qq) = f[a][i];
                         if (!HAS_PSI && !isfinite(pfem::lane(f[0][0], 0))) ++n_nonfin;
                     }
                 }
             }
 #pragma unroll
             for (int q = 0; q < ST; ++q) wsum[q] += (double)wacc[q];   // per-thread, fixed order
+            if (HAS_PSI && S <= ST && !(p.dbg & 8)) {
+                // per-warp energy sums now, while other warps finish phase 1 (s_red is free:
+                // the previous block's warp 0 read it before this block's first barrier)
+                T wv[ST];
+#pragma unroll
+                for (int q = 0; q < ST; ++q) wv[q] = q < S ? (T)wsum[q] : T(0);
+                const T r = warp_multi_sum<T, ST>(wv, lane);
+                if ((lane & (32 / ST - 1)) == 0) s_red[warp][lane / (32 / ST)] = (double)r;
+            }
             // the next block's fields: its record has had phase 1 to land
             if (s0 + ST >= S) {
                 if ((pref || has_mat) && tn < p.n_blocks) {
@@ -586,40 +672,82 @@ k_assemble(const AsmParams<T> p) {
             }
             if ((HAS_FORCE || p.f_ext) && !(p.dbg & 2)) {
                 bar_main(NT);
-                // ---------------- phase 2: block-local CSR gather, thread per occurrence
-                for (int oi = tid; oi < no; oi += NT) {
-                    const int o = o0 + oi;
+                // ---------------- phase 2: block-local CSR gather, HP threads per occurrence
+                // (fp32 ST = 4: two threads, each summing two samples of every entry, so all
+                // warps share the gather and each entry chain is half as long)
+                for (int w = tid; w < HP * no; w += NT) {
+                    const int oi = HP == 1 ? w : w / HP;
+                    const int qs = HP == 1 ? 0 : (w % HP) * STH;   // first sample of this thread
                     const int word = socc[oi];
                     const int node = word & OCC_NODE_MASK;
                     if (HAS_FORCE) {
-                        T accs[SD];
+                        T accs[SDH];   // [D][STH]
 #pragma unroll
-                        for (int k = 0; k < SD; ++k) accs[k] = T(0);
+                        for (int k = 0; k < SDH; ++k) accs[k] = T(0);
                         const int kb = soe[oi], k1 = soe[oi + 1];
-                        for (int k = kb; k < k1; ++k) {
-                            const int j = sle[k];
-                            const int el = j / NV, a = j - el * NV;
-                            sacc<T, SD>(fbuf + ((size_t)a * EB + el) * SD, accs);
+                        if constexpr (EPOS) {
+                            for (int k = kb; k < k1; ++k) sacc<T, SD>(fbuf + (size_t)k * SD, accs);
+                        } else if constexpr (HP == 1) {
+                            for (int k = kb; k < k1; ++k) {
+                                const int j = sle[k];
+                                const int el = j / NV, a = j - el * NV;
+                                sacc<T, SDH>(fbuf + ((size_t)a * EB + el) * SD, accs);
+                            }
+                        } else {
+                            // entries in pairs: both gathers in flight before the adds (the
+                            // adds stay in ascending entry order)
+                            int k = kb;
+                            for (; k + 1 < k1; k += 2) {
+                                const int j0 = sle[k], j1 = sle[k + 1];
+                                const T* b0 = fbuf + ((size_t)(j0 & 3) * EB + (j0 >> 2)) * SD + qs;
+                                const T* b1 = fbuf + ((size_t)(j1 & 3) * EB + (j1 >> 2)) * SD + qs;
+                                float2 x0[D], x1[D];
+#pragma unroll
+                                for (int i = 0; i < D; ++i) {
+                                    x0[i] = *reinterpret_cast<const float2*>(b0 + i * ST);
+                                    x1[i] = *reinterpret_cast<const float2*>(b1 + i * ST);
+                                }
+#pragma unroll
+                                for (int i = 0; i < D; ++i) {
+                                    F2 a0(accs[2 * i], accs[2 * i + 1]);
+                                    a0 = (a0 + F2(x0[i].x, x0[i].y)) + F2(x1[i].x, x1[i].y);
+                                    accs[2 * i] = a0.v.x; accs[2 * i + 1] = a0.v.y;
+                                }
+                            }
+                            if (k < k1) {
+                                const int j0 = sle[k];
+                                const T* b0 = fbuf + ((size_t)(j0 & 3) * EB + (j0 >> 2)) * SD + qs;
+#pragma unroll
+                                for (int i = 0; i < D; ++i) {
+                                    const float2 x0 = *reinterpret_cast<const float2*>(b0 + i * ST);
+                                    F2 a0(accs[2 * i], accs[2 * i + 1]);
+                                    a0 = a0 + F2(x0.x, x0.y);
+                                    accs[2 * i] = a0.v.x; accs[2 * i + 1] = a0.v.y;
+                                }
+                            }
                         }
+                        // accs layout: HP == 1 [D][ST] (sacc over SD contiguous values), HP == 2 [D][2]
                         if (word & (OCC_NONOWNER | OCC_EARLIER)) {
                             // this block's segment of a multi-block node: seg[slot][s][d], slots
                             // node-major (a node's segments contiguous, ascending block)
                             const int slot = sseg[oi];
 #pragma unroll
-                            for (int q = 0; q < ST; ++q) {
+                            for (int qq = 0; qq < STH; ++qq) {
+                                const int q = qs + qq;
                                 if (q >= nq) break;
                                 T* dst = p.partial + ((int64_t)slot * S + s0 + q) * D;
 #pragma unroll
-                                for (int i = 0; i < D; ++i) dst[i] = accs[i * ST + q];
+                                for (int i = 0; i < D; ++i) dst[i] = accs[i * STH + qq];
                             }
                         } else {
 #pragma unroll
-                            for (int q = 0; q < ST; ++q) {
+                            for (int qq = 0; qq < STH; ++qq) {
+                                const int q = qs + qq;
                                 if (q >= nq) break;
                                 const int64_t nb = (int64_t)(s0 + q) * p.sstride + (int64_t)node * D;
 #pragma unroll
                                 for (int i = 0; i < D; ++i) {
-                                    T val = accs[i * ST + q];
+                                    T val = accs[i * STH + qq];
                                     if (OP == OP_TANGENT && MASKED && __ldg(p.mask + (int64_t)node * D + i))
                                         val = __ldg(p.v + nb + i);
                                     p.out[nb + i] = val;
@@ -630,14 +758,14 @@ k_assemble(const AsmParams<T> p) {
                     }
                     if (HAS_PSI && p.f_ext && !(word & OCC_NONOWNER)) {
 #pragma unroll
-                        for (int q = 0; q < ST; ++q) {
-                            if (q >= nq) break;
+                        for (int q = 0; q < ST; ++q) {   // (compile-time q: fsum stays in registers)
+                            if (q < qs || q >= qs + STH || q >= nq) continue;
                             const int64_t nb = (int64_t)(s0 + q) * p.sstride + (int64_t)node * D;
-                            double w = 0.0;
+                            double w2 = 0.0;
 #pragma unroll
                             for (int i = 0; i < D; ++i)
-                                w += (double)__ldg(p.f_ext + (int64_t)node * D + i) * (double)__ldg(p.u + nb + i);
-                            fsum[q] += w;
+                                w2 += (double)__ldg(p.f_ext + (int64_t)node * D + i) * (double)__ldg(p.u + nb + i);
+                            fsum[q] += w2;
                         }
                     }
                 }
@@ -665,13 +793,12 @@ k_assemble(const AsmParams<T> p) {
         }
         // ---------------- per-block sums (single-chunk case) and CG dot
         if (((HAS_PSI && S <= ST) || cgdot) && !(p.dbg & 8)) {
-            if (HAS_PSI && S <= ST) {
+            if (HAS_PSI && S <= ST) {   // (the energy sums went to s_red after phase 1)
 #pragma unroll
                 for (int q = 0; q < ST; ++q) {
                     if (q >= S) break;
-                    const double a = (double)warp_sum_t<T>((T)wsum[q]);
                     const double f2 = p.f_ext ? warp_sum(fsum[q]) : 0.0;
-                    if (lane == 0) { s_red[warp][q] = a; s_red[warp][ST + q] = f2; }
+                    if (lane == 0) s_red[warp][ST + q] = f2;
                 }
             }
             if (cgdot) {

@@ -40,15 +40,10 @@ __device__ __forceinline__ void l2_prefetch(const void* base, size_t total, size
 template <class T>
 __device__ __forceinline__ void prefetch_record(const AsmParams<T>& p, int b) {
     const size_t rb = (size_t)p.rec.bytes, total = rb * p.n_blocks;
-    // the fields the direct kernel reads: gradients .. occ_seg, without conn; fp32 (ent_pos
-    // layout) skips loc_ent, fp64 skips ent_pos
-    if (sizeof(T) == 4) {
-        l2_prefetch(p.recs, total, (size_t)b * rb + p.rec.ent_pos, p.rec.conn - p.rec.ent_pos);
-        l2_prefetch(p.recs, total, (size_t)b * rb + p.rec.g, p.rec.loc_ent - p.rec.g);
-        l2_prefetch(p.recs, total, (size_t)b * rb + p.rec.lconn, rb - p.rec.lconn);
-    } else {
-        l2_prefetch(p.recs, total, (size_t)b * rb + p.rec.g, rb - p.rec.g);
-    }
+    // the fields the direct kernel reads (RecLayout order): fp32 (ent_pos layout)
+    // [ent_pos, loc_ent), fp64 (loc_ent gather) [g, end); conn is not read here
+    if (sizeof(T) == 4) l2_prefetch(p.recs, total, (size_t)b * rb + p.rec.ent_pos, p.rec.loc_ent - p.rec.ent_pos);
+    else l2_prefetch(p.recs, total, (size_t)b * rb + p.rec.g, rb - p.rec.g);
     const int e0 = __ldg(p.blk_elem + b), e1 = __ldg(p.blk_elem + b + 1);
     const size_t E = (size_t)p.E, ne = (size_t)(e1 - e0);
     if (p.perm) return;   // element-wise materials are gathered through the permutation

@@ -41,13 +41,16 @@ constexpr int32_t OCC_EARLIER = 0x20000000;    // owner, and earlier blocks hold
 // The plan keeps, per element block, one contiguous 16-byte-aligned record holding
 // everything phase 1 and phase 2 read from HBM about the block, so a single TMA bulk copy
 // (cp.async.bulk) stages it into shared memory:
-//   ent_pos [EB][d+1] uint16 (inverse of loc_ent: the block-CSR entry of each element vertex) |
-//   conn [EB][d+1] int32 | grad [d*d][EB] T | vol [EB] T | eid [EB] int32 (input element id
-//   of each position: the plan may order elements for locality) | occ_node [OCAP] int32 |
-//   occ_ent [OCAP+1] uint16 (block-relative entry offsets) | loc_ent [(d+1) EB] uint16 |
-//   lconn [EB][d+1] uint16 (block-local occurrence index of each element vertex) |
-//   occ_seg [OCAP] int32 (node-major segment slot of a multi-block node's occurrence, -1 if
-//   the node is finished inside the block)
+//   conn [EB][d+1] int32 | ent_pos [EB][d+1] uint16 (inverse of loc_ent: the block-CSR entry
+//   of each element vertex) | grad [d*d][EB] T | vol [EB] T | eid [EB] int32 (input element
+//   id of each position: the plan may order elements for locality) | occ_node [OCAP] int32 |
+//   occ_ent [OCAP+1] uint16 (block-relative entry offsets) | lconn [EB][d+1] uint16
+//   (block-local occurrence index of each element vertex) | occ_seg [OCAP] int32 (node-major
+//   segment slot of a multi-block node's occurrence, -1 if the node is finished inside the
+//   block) | loc_ent [(d+1) EB] uint16
+// The order lets every kernel form read one contiguous range: fp32 forms (force buffer in
+// entry order) [ent_pos, loc_ent), fp64 forms (loc_ent gather) [g, end), and the gathering
+// staged forms start at conn.
 struct RecLayout {
     int eb = 0, ocap = 0;
     uint32_t conn = 0, g = 0, vol = 0, eid = 0, occ_node = 0, occ_ent = 0, loc_ent = 0, lconn = 0, occ_seg = 0, ent_pos = 0, bytes = 0;
@@ -59,18 +62,16 @@ inline RecLayout rec_layout(int D, size_t tsize, int eb, int ocap, bool with_eid
     L.ocap = ocap;
     size_t o = 0;
     auto take = [&](size_t b) { size_t at = o; o += (b + 15) / 16 * 16; return (uint32_t)at; };
-    // ent_pos and conn lead, so the staged kernel's bulk copy can start at conn (gathers) or
-    // at g (staged fields) and skip what it does not read
-    L.ent_pos = take(2 * (size_t)(D + 1) * eb);
     L.conn = take(4 * (size_t)(D + 1) * eb);
+    L.ent_pos = take(2 * (size_t)(D + 1) * eb);
     L.g = take(tsize * D * D * (size_t)eb);
     L.vol = take(tsize * (size_t)eb);
     L.eid = take(with_eid ? 4 * (size_t)eb : 0);   // identity order: no ids stored
     L.occ_node = take(4 * (size_t)ocap);
     L.occ_ent = take(2 * (size_t)(ocap + 1));
-    L.loc_ent = take(2 * (size_t)(D + 1) * eb);
     L.lconn = take(2 * (size_t)(D + 1) * eb);
     L.occ_seg = take(4 * (size_t)ocap);
+    L.loc_ent = take(2 * (size_t)(D + 1) * eb);
     L.bytes = (uint32_t)o;
     return L;
 }

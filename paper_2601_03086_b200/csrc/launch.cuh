@@ -86,6 +86,7 @@ AsmParams<T> make_params(const Call& c) {
     p.perm = P.elem_perm != nullptr;
     p.rec = P.rec;
     p.rec_base = 0;
+    p.rec_end = P.rec.bytes;
     p.recs = P.recs;
     const WsLayout L = ws_layout(P, c.S, sizeof(T));
     char* w = (char*)c.ws;
@@ -142,33 +143,6 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
     constexpr int EB = EbOf<D>::value;
     constexpr int NT = ASM_NT;
     constexpr int NF = 1;
-    // the staged copy skips ent_pos, and conn too when the fields are staged and the NH
-    // state u is not gathered
-    const bool need_conn = p.S > ST || (OP == OP_TANGENT && MODEL == MODEL_NH);
-    p.rec_base = need_conn ? p.rec.conn : p.rec.g;
-    const size_t smem = 2 * (size_t)(p.rec.bytes - p.rec_base) + 4 * EB * sizeof(T) +
-                        2 * (size_t)NF * p.rec.ocap * D * ST * sizeof(T) +
-                        (HAS_FORCE ? (size_t)ST * D * (D + 1) * EB * sizeof(T) : 0);
-    auto kern = k_assemble<D, MODEL, T, OP, ST, MASKED, EB, NT>;
-    static int resident = 0;   // per instantiation: co-resident CTAs (persistent grid)
-    static size_t configured = 0;
-    if (resident == 0 || smem > configured) {
-        PFEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = smem;
-        int dev = 0, nsm = 0, per_sm = 0;
-        PFEM_CUDA_TRY(cudaGetDevice(&dev));
-        PFEM_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        PFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
-        if (per_sm < 1) {
-            set_error("CSR kernel does not fit on an SM (block record too large)");
-            return PFEM_ERR_CAPACITY;
-        }
-        resident = per_sm * nsm;
-    }
-    if (p.eb_max > EB) {
-        set_error("plan block larger than the kernel's block capacity");
-        return PFEM_ERR_CAPACITY;
-    }
     static const int dbg = getenv("PFEM_DEBUG") ? atoi(getenv("PFEM_DEBUG")) : 0;
     static const int variant = getenv("PFEM_VARIANT") ? atoi(getenv("PFEM_VARIANT")) : -1;
     p.dbg = dbg;
@@ -176,12 +150,39 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
     // where the kernel is bound by memory latency and occupancy pays; staged persistent
     // otherwise (several samples per element: arithmetic-heavy, staging amortised).
     // PFEM_VARIANT=0/1 forces staged/direct (measurement switch).
-    const bool direct = variant >= 0 ? variant == 1 : p.S == 1;
+    // Blocks larger than the staged kernel's compile-time capacity always take the direct form.
+    const bool direct = p.eb_max > EB || (variant >= 0 ? variant == 1 : p.S == 1);
     if (direct) {
         const pfem_status st = p.perm ? launch_direct<D, MODEL, T, OP, ST, MASKED, direct_nt<T>(), true>(p, s)
                                       : launch_direct<D, MODEL, T, OP, ST, MASKED, direct_nt<T>(), false>(p, s);
         if (st != PFEM_OK) return st;
     } else {
+        // the staged copy (RecLayout order) skips conn when the fields are staged and the NH
+        // state u is not gathered; fp32 (force buffer in entry order) reads ent_pos and not
+        // loc_ent, fp64 (loc_ent gather) the reverse
+        const bool need_conn = p.S > ST || (OP == OP_TANGENT && MODEL == MODEL_NH);
+        constexpr bool EPOS = sizeof(T) == 4 && PFEM_STAGED_EPOS;
+        p.rec_base = need_conn ? p.rec.conn : (EPOS ? p.rec.ent_pos : p.rec.g);
+        p.rec_end = EPOS ? p.rec.loc_ent : p.rec.bytes;
+        const size_t smem = 2 * (size_t)(p.rec_end - p.rec_base) + 4 * EB * sizeof(T) +
+                            2 * (size_t)NF * p.rec.ocap * D * ST * sizeof(T) +
+                            (HAS_FORCE ? (size_t)ST * D * (D + 1) * EB * sizeof(T) : 0);
+        auto kern = k_assemble<D, MODEL, T, OP, ST, MASKED, EB, NT>;
+        static int resident = 0;   // per instantiation: co-resident CTAs (persistent grid)
+        static size_t configured = 0;
+        if (resident == 0 || smem > configured) {
+            PFEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            configured = smem;
+            int dev = 0, nsm = 0, per_sm = 0;
+            PFEM_CUDA_TRY(cudaGetDevice(&dev));
+            PFEM_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+            PFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+            if (per_sm < 1) {
+                set_error("CSR kernel does not fit on an SM (block record too large)");
+                return PFEM_ERR_CAPACITY;
+            }
+            resident = per_sm * nsm;
+        }
         const int grid = std::max(1, std::min(resident, p.n_blocks));
         kern<<<grid, NT, smem, s>>>(p);
         PFEM_LAUNCH_CHECK("k_assemble");

@@ -648,9 +648,11 @@ pfem_status prepare_impl(pfem_mesh* m, cudaStream_t s) {
             }
     }
     // block capacity = the CSR kernel's compile-time EB (assemble.cuh EbOf): 256 T4 / 512 T3
-    const int eb_cap = D == 3 ? 256 : 512;
-    int eb = m->block_elems > 0 ? std::min(m->block_elems, eb_cap) : eb_cap;
+    // (a larger block_elems, up to PLAN_MAX_KEYS / (d+1), is served by the direct kernel form)
+    const int eb_default = D == 3 ? 256 : 512;
+    int eb = m->block_elems > 0 ? m->block_elems : eb_default;
     eb = std::min(eb, PLAN_MAX_KEYS / nv);
+    const int eb_cap = std::max(eb, eb_default);
     std::vector<int32_t> blk_elem{0}, part_blk{0};
     for (int k = 0; k < K; ++k) {
         int n = pe[k + 1] - pe[k];

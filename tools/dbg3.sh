@@ -1,0 +1,9 @@
+#!/bin/bash
+# config-3 E+R (and K.v) kernel time under PFEM_DEBUG ablation switches
+cd "$(dirname "$0")/.." || exit 1
+for d in 0 32 33 34 40 35 43 59; do
+  for op in er kv; do
+    PFEM_DEBUG=$d timeout 300 python tools/bench_kernel.py --config 3 --op $op --reps 40 2>&1 | tail -1 | \
+      python -c "import sys,json; l=sys.stdin.read(); d=json.loads(l) if l.startswith('{') else None; print('dbg=$d', '$op', round(d['median_us'],1)) if d else print(l[-200:])"
+  done
+done | tee gpurun_out/dbg3_${1:-x}.txt
