@@ -244,6 +244,33 @@ class Mesh:
         return u, {"iterations": len(hist) - 1, "converged": status == 0, "exit": status, "history": np.array(hist),
                    "cg_iterations": cg_its}
 
+    def tangent_diag(self, u=None, mask=None):
+        """Diagonal of A = (I-M) K(u) (I-M) + M: textbook element tangents' diagonals assembled
+        in ascending (e, a) order, 1 on constrained DOFs."""
+        d = np.zeros(self.n_nodes * self.dim)
+        us = None if u is None else _f64(u).reshape(-1)
+        m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8).reshape(-1)
+        st = lib().oracle_tangent_diag(*self._args(), _p(us), _p(m), _p(d))
+        _check(st, "tangent_diag")
+        return d.reshape(self.n_nodes, self.dim)
+
+    def pcg(self, f, mask, x0, tol=1e-8, max_iter=50000, u_state=None, precond=1, history=True):
+        """Jacobi-preconditioned CG (reading R27), same stop test as cg(); precond=0 is plain CG."""
+        x = _f64(x0).copy().reshape(-1)
+        f = _f64(f).reshape(-1)
+        m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8).reshape(-1)
+        us = None if u_state is None else _f64(u_state).reshape(-1)
+        hist = np.zeros(max_iter + 1) if history else None
+        it = C.c_int32(0)
+        r0, rf, tr = C.c_double(0), C.c_double(0), C.c_double(0)
+        st = lib().oracle_pcg(*self._args(), _p(us), _p(f), _p(m), C.c_int(precond), _p(x), C.c_double(tol),
+                              C.c_int32(max_iter), _p(hist), C.byref(it), C.byref(r0), C.byref(rf),
+                              C.byref(tr))
+        rep = {"status": st, "iterations": it.value, "converged": st == OK, "rel_res0": r0.value,
+               "rel_res_final": rf.value, "true_rel_res_final": tr.value,
+               "history": None if hist is None else hist[: it.value + 1].copy()}
+        return x.reshape(np.shape(x0)), rep
+
     def cg_spread(self, f, mask, x0, tol=1e-8, max_iter=50000, u_state=None):
         """Iteration counts of the oracle CG under the five dot-product orders (R18)."""
         return [self.cg(f, mask, x0, tol, max_iter, u_state, history=False, dot_order=o)[1]["iterations"]

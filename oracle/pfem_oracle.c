@@ -674,3 +674,118 @@ int oracle_cg(int dim, int64_t n_nodes, int64_t n_elems, const int32_t* conn, co
     free(r); free(p); free(q); free(xd); free(b);
     return st;
 }
+
+/* ------------------------------------------------------------------ */
+/* Jacobi preconditioner (the paper sets preconditioning beside warm  */
+/* starting as a complementary way to cut CG iterations, §5.5):                  */
+/*   diag[k] = A_kk of A = (I-M) K(u) (I-M) + M, i.e. the sum over the (e, a) entries of   */
+/*   node n of the diagonal entries K_e[a*d+i][a*d+i] of the textbook element tangent      */
+/*   (Voigt B^T D B / V (G0^T S G0 + B0^T C^SE B0), elem_tangent above), assembled in      */
+/*   ascending (e, a) order; 1 on constrained DOFs.                                        */
+/* ------------------------------------------------------------------ */
+int oracle_tangent_diag(int dim, int64_t n_nodes, int64_t n_elems, const int32_t* conn,
+                        const double* grad, const double* vol, int model, const double* mu,
+                        const double* lam, const double* u, const uint8_t* mask, double* diag) {
+    const int nv = dim + 1, ne = nv * dim;
+    double* de = (double*)malloc(sizeof(double) * (size_t)n_elems * ne);
+    if (!de) return OR_ERR_CAPACITY;
+    int64_t first_bad = -1;
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < n_elems; ++e) {
+        double g[4][3], K[12][12];
+        elem_grads(dim, grad, e, g);
+        if (elem_tangent(dim, model, g, vol[e], mu[e], lam[e], conn + e * nv, u, K) != OR_OK) {
+#pragma omp critical
+            { if (first_bad < 0 || e < first_bad) first_bad = e; }
+        }
+        for (int p = 0; p < ne; ++p) de[e * ne + p] = K[p][p];
+    }
+    for (int64_t k = 0; k < n_nodes * dim; ++k) diag[k] = 0.0;
+    for (int64_t e = 0; e < n_elems; ++e)
+        for (int a = 0; a < nv; ++a)
+            for (int i = 0; i < dim; ++i) diag[(int64_t)conn[e * nv + a] * dim + i] += de[e * ne + a * dim + i];
+    if (mask)
+        for (int64_t k = 0; k < n_nodes * dim; ++k)
+            if (mask[k]) diag[k] = 1.0;
+    free(de);
+    if (first_bad >= 0) { g_err_index = first_bad; return OR_ERR_INVERTED; }
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* Preconditioned CG (textbook Hestenes-Stiefel PCG with M^-1 = diag(A)^-1, reading R27):   */
+/*   r0 = b - A x0 (free DOFs), z0 = M^-1 r0, p0 = z0, rho = r.z                             */
+/*   q = A p; pi = p.q; alpha = rho / pi; x += alpha p; r -= alpha q                          */
+/*   stop when ||r|| < tol ||b_free|| (the same unpreconditioned test as oracle_cg, R8)       */
+/*   z = M^-1 r; rho' = r.z; beta = rho' / rho; p = z + beta p                               */
+/* M^-1_k = 1 / diag_k where diag_k > 0, else 1.  precond 0 runs plain CG (z = r).           */
+/* ------------------------------------------------------------------ */
+int oracle_pcg(int dim, int64_t n_nodes, int64_t n_elems, const int32_t* conn, const double* grad,
+               const double* vol, int model, const double* mu, const double* lam,
+               const double* u_state, const double* f, const uint8_t* mask, int precond, double* x,
+               double tol, int32_t max_iter, double* history, int32_t* iterations, double* rel_res0,
+               double* rel_res_final, double* true_rel_res_final) {
+    const int64_t n = n_nodes * dim;
+    double* r = (double*)malloc(sizeof(double) * n);
+    double* z = (double*)malloc(sizeof(double) * n);
+    double* p = (double*)malloc(sizeof(double) * n);
+    double* q = (double*)malloc(sizeof(double) * n);
+    double* xd = (double*)malloc(sizeof(double) * n);
+    double* b = (double*)malloc(sizeof(double) * n);
+    double* minv = (double*)malloc(sizeof(double) * n);
+    if (!r || !z || !p || !q || !xd || !b || !minv) return OR_ERR_CAPACITY;
+    int st = OR_OK;
+    if (precond) {
+        oracle_tangent_diag(dim, n_nodes, n_elems, conn, grad, vol, model, mu, lam, u_state, mask, minv);
+        for (int64_t i = 0; i < n; ++i) minv[i] = minv[i] > 0.0 ? 1.0 / minv[i] : 1.0;
+    } else {
+        for (int64_t i = 0; i < n; ++i) minv[i] = 1.0;
+    }
+    for (int64_t i = 0; i < n; ++i) xd[i] = (mask && mask[i]) ? x[i] : 0.0;
+    oracle_tangent(dim, n_nodes, n_elems, conn, grad, vol, model, mu, lam, 1, u_state, xd, NULL, q);
+    for (int64_t i = 0; i < n; ++i) b[i] = (mask && mask[i]) ? 0.0 : f[i] - q[i];
+    double bnorm = sqrt(dot(n, b, b));
+    oracle_tangent(dim, n_nodes, n_elems, conn, grad, vol, model, mu, lam, 1, u_state, x, mask, q);
+    for (int64_t i = 0; i < n; ++i) r[i] = (mask && mask[i]) ? 0.0 : b[i] - q[i];
+    double rr = dot(n, r, r);
+    *rel_res0 = bnorm > 0 ? sqrt(rr) / bnorm : 0.0;
+    if (history) history[0] = *rel_res0;
+    int32_t k = 0;
+    if (bnorm == 0.0) {
+        for (int64_t i = 0; i < n; ++i) x[i] = (mask && mask[i]) ? x[i] : 0.0;
+        rr = 0.0;
+    } else if (sqrt(rr) < tol * bnorm) {
+        /* skip rule */
+    } else {
+        for (int64_t i = 0; i < n; ++i) z[i] = minv[i] * r[i];
+        memcpy(p, z, sizeof(double) * n);
+        double rho = dot(n, r, z);
+        st = OR_ERR_NOT_CONVERGED;
+        for (k = 1; k <= max_iter; ++k) {
+            oracle_tangent(dim, n_nodes, n_elems, conn, grad, vol, model, mu, lam, 1, u_state, p, mask, q);
+            double pi = dot(n, p, q);
+            if (!(pi > 0.0)) { st = OR_ERR_BREAKDOWN; break; }
+            double alpha = rho / pi;
+            for (int64_t i = 0; i < n; ++i) x[i] += alpha * p[i];
+            for (int64_t i = 0; i < n; ++i) r[i] -= alpha * q[i];
+            rr = dot(n, r, r);
+            if (history) history[k] = sqrt(rr) / bnorm;
+            if (sqrt(rr) < tol * bnorm) { st = OR_OK; break; }
+            for (int64_t i = 0; i < n; ++i) z[i] = minv[i] * r[i];
+            double rho_new = dot(n, r, z);
+            double beta = rho_new / rho;
+            for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+            rho = rho_new;
+        }
+        if (k > max_iter) k = max_iter;
+    }
+    *iterations = k;
+    *rel_res_final = bnorm > 0 ? sqrt(rr) / bnorm : 0.0;
+    oracle_tangent(dim, n_nodes, n_elems, conn, grad, vol, model, mu, lam, 1, u_state, x, mask, q);
+    double tr = 0.0;
+    for (int64_t i = 0; i < n; ++i)
+        if (!(mask && mask[i])) tr += (b[i] - q[i]) * (b[i] - q[i]);
+    *true_rel_res_final = bnorm > 0 ? sqrt(tr) / bnorm : 0.0;
+    free(r); free(z); free(p); free(q); free(xd); free(b); free(minv);
+    return st;
+}

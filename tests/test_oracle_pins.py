@@ -572,3 +572,90 @@ def test_newton_small_load_limit_and_warm_start(orc):
     _, rz = m.newton(p.u[0], p.f_ext, p.mask, tol=1e-9, cg_tol=1e-12)
     _, rw = m.newton(warm_start(us, p.mask, seed=77), p.f_ext, p.mask, tol=1e-9, cg_tol=1e-12)
     assert rw["iterations"] < rz["iterations"]
+
+
+# ---------------------------------------------------------------- Jacobi PCG (§8(f) row f3)
+@pytest.mark.parametrize("kind", ["t3", "t4"])
+@pytest.mark.parametrize("model", ["linear", "neohookean"])
+def test_tangent_diag_is_operator_diagonal(orc, kind, model):
+    """diag(A) of A = (I-M) K(u) (I-M) + M equals the brute-force diagonal e_i . A e_i of the
+    matrix-free operator (reading R27; P:1104-1115 for K), mask rows 1."""
+    coords, conn = MESHES[kind]()
+    d = coords.shape[1]
+    m = orc.prepare(coords, conn, model, "lame", [0.4], [0.6])
+    rng = np.random.default_rng(5)
+    u = 0.05 * rng.standard_normal(coords.shape) if model == "neohookean" else None
+    mask = (rng.random(coords.size) < 0.2).astype(np.uint8)
+    n = coords.size
+    diag_bf = np.empty(n)
+    for i in range(n):
+        e = np.zeros(n)
+        e[i] = 1.0
+        us = None if u is None else u.reshape(1, -1, d)
+        diag_bf[i] = m.tangent(e.reshape(1, -1, d), u=us, mask=mask).ravel()[i]
+    dg = m.tangent_diag(u=u, mask=mask).ravel()
+    assert rel(dg, diag_bf) < 1e-14
+    assert np.all(dg[mask == 1] == 1.0) and np.all(dg > 0)
+
+
+def test_tangent_diag_closed_form_single_element(orc):
+    """Reference T3 / T4, linear law: the diagonal of V B^T D B is
+    V [(lam + 2 mu) g_ai^2 + mu sum_{j != i} g_aj^2] (textbook isotropic stiffness, P:527-536);
+    Neo-Hookean at F = I has the same diagonal (K(0) = K_lin)."""
+    mu, lam = 0.4, 0.6
+    for coords in (np.array([[0., 0], [1, 0], [0, 1]]), np.array([[0., 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]])):
+        d = coords.shape[1]
+        V = 1.0 / (2 if d == 2 else 6)
+        g = np.vstack([-np.ones(d), np.eye(d)])          # grad N_a of the reference simplex
+        ref = np.array([[V * ((lam + 2 * mu) * g[a, i] ** 2 + mu * (g[a] @ g[a] - g[a, i] ** 2)) for i in range(d)]
+                        for a in range(d + 1)])
+        conn = np.arange(d + 1)[None, :]
+        for model in ("linear", "neohookean"):
+            m = orc.prepare(coords, conn, model, "lame", [mu], [lam])
+            u0 = np.zeros_like(coords) if model == "neohookean" else None
+            assert rel(m.tangent_diag(u=u0), ref) < 1e-15
+
+
+def _dense_cg(A, b, k):
+    """Textbook Hestenes-Stiefel CG, k steps from 0 (numpy, dense)."""
+    x = np.zeros_like(b)
+    r = b.copy()
+    p = r.copy()
+    rho = r @ r
+    for _ in range(k):
+        q = A @ p
+        a = rho / (p @ q)
+        x += a * p
+        r -= a * q
+        rn = r @ r
+        p = r + (rn / rho) * p
+        rho = rn
+    return x
+
+
+def test_pcg_is_cg_on_the_jacobi_scaled_system(orc):
+    """Jacobi PCG iterates are x_k = D^-1/2 y_k with y_k the CG iterates of
+    (D^-1/2 A D^-1/2) y = D^-1/2 b (the classical equivalence of split preconditioning);
+    PCG solves to the dense Cholesky solution; precond 0 is plain CG bit for bit; an exact
+    initial guess takes 0 iterations."""
+    p = config1()
+    m = orc.prepare_problem(p)
+    n = p.n_nodes * 2
+    A = dense_K(m, n, mask=p.mask)
+    b = p.f_ext.ravel() * (1 - p.mask)
+    dg = m.tangent_diag(mask=p.mask).ravel()
+    assert rel(dg, np.diag(A)) < 1e-15
+    s = 1.0 / np.sqrt(dg)
+    Ah = A * s[:, None] * s[None, :]
+    for k in (1, 3, 10, 25):
+        xk, _ = m.pcg(p.f_ext, p.mask, np.zeros(n), tol=1e-30, max_iter=k, history=False)
+        assert rel(xk.ravel(), s * _dense_cg(Ah, s * b, k)) < 1e-10
+    x_ref = np.linalg.solve(A, b)
+    x, rep = m.pcg(p.f_ext, p.mask, np.zeros(n), tol=1e-12)
+    assert rep["converged"] and rel(x, x_ref) < 1e-9 and rep["true_rel_res_final"] < 1e-11
+    xc, rc = m.cg(p.f_ext, p.mask, np.zeros(n), tol=1e-8)
+    x0, r0 = m.pcg(p.f_ext, p.mask, np.zeros(n), tol=1e-8, precond=0)
+    assert r0["iterations"] == rc["iterations"] and np.array_equal(r0["history"], rc["history"])
+    assert np.array_equal(x0, xc)
+    _, rs = m.pcg(p.f_ext, p.mask, x_ref, tol=1e-8)
+    assert rs["iterations"] == 0 and rs["converged"]
