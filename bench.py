@@ -307,8 +307,8 @@ def time_events(torch, fn, reps):
 
 
 def run_extras(torch, pf, dev, peak):
-    """Config 4 (K.v roofline, warm-started CG), config 5 (64-part fused E+R) and the Newton
-    warm start on a Neo-Hookean block (§8(f) row f1)."""
+    """Config 4 (K.v roofline, warm-started CG, Jacobi PCG §8(f) row f3), config 5 (64-part fused
+    E+R) and the Newton warm start on a Neo-Hookean block (§8(f) row f1)."""
     from pfem_gen import config4, config5, warm_start
     ex = {}
     # ---------------- config 4: K.v fp64 + CG from zero / perturbed-exact warm start
@@ -360,6 +360,23 @@ def run_extras(torch, pf, dev, peak):
                                  "iterations_to_1e-6": int(np.argmax(h < 1e-6)) if np.any(h < 1e-6) else None},
                         "speedup_iterations": rz["iterations"] / max(1, rw["iterations"]),
                         "warm_start": "u* (GPU CG to 1e-12) + 0.01 rms(u*) N(0,1) on free DOFs"}
+    # §8(f) f3: Jacobi-preconditioned CG, same starts and tolerance
+    pf.cg(m4, mat4, f, x0, mask=mask, tol=1e-8, max_iter=200, precond="jacobi")   # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _, pz = pf.cg(m4, mat4, f, x0, mask=mask, tol=1e-8, max_iter=20000, history=False, precond="jacobi")
+    tpz = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _, pw = pf.cg(m4, mat4, f, xw, mask=mask, tol=1e-8, max_iter=20000, history=False, precond="jacobi")
+    tpw = time.perf_counter() - t0
+    ex["config4_pcg_jacobi"] = {
+        "tol": 1e-8,
+        "zero": {"iterations": pz["iterations"], "time_to_tol_s": tpz, "ms_per_iteration": tpz / max(1, pz["iterations"]) * 1e3,
+                 "true_rel_res": pz["true_rel_res_final"]},
+        "warm": {"iterations": pw["iterations"], "time_to_tol_s": tpw, "true_rel_res": pw["true_rel_res_final"]},
+        "iterations_vs_cg_zero": rz["iterations"] / max(1, pz["iterations"]),
+        "iterations_vs_cg_warm": rw["iterations"] / max(1, pw["iterations"])}
     del m4, vs, kv
     torch.cuda.empty_cache()
     # ---------------- config 5: 64 ragged parts, NH fp32, fused E+R in one launch

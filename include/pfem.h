@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define PFEM_ABI_VERSION 3
+#define PFEM_ABI_VERSION 4
 
 typedef enum {
     PFEM_OK = 0,
@@ -246,6 +246,36 @@ pfem_status pfem_cg(const pfem_mesh* m, const pfem_material* mat, const void* u_
                     const void* rhs, const uint8_t* mask, void* x, double tol, int32_t max_iter,
                     int32_t mode, double* history, pfem_cg_report* report, void* ws,
                     size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * Jacobi preconditioning.  The paper names preconditioning as the
+ * complement of the warm start for cutting CG iterations (§5.5); DESIGN.md
+ * reading R27 fixes the preconditioner (Jacobi) and the algorithm.
+ *
+ * pfem_tangent_diag: diag [N][d] of A = (I-M) K(u_state) (I-M) + M, 1 on constrained DOFs.
+ *   Per DOF (n, i) the sum, over the (e, a) entries of node n in ascending CSR order (R12), of
+ *     V_e [mu |grad N_a|^2 + c ((F^-T grad N_a)_i)^2],  c = lam + mu - lam ln J   (NH)
+ *   (linear: F = I, c = lam + mu): the diagonal of the element tangent dP/dF of
+ *   App. B P:1104-1115 contracted with grad N_a on both sides.
+ *   u_state  nullable [N][d] (required for Neo-Hookean)
+ *   mask     nullable [N*d]
+ *   Asynchronous on `stream`; no workspace.
+ *
+ * pfem_pcg: pfem_cg with a preconditioner M (precond = PFEM_PRECOND_NONE: identical to
+ *   pfem_cg; PFEM_PRECOND_JACOBI: M = diag(A), M^-1_k = 1/diag_k, 1 where diag_k <= 0):
+ *     r0 = b - A x0, z = M^-1 r, p = z, rho = r.z;  per iteration q = A p, alpha = rho / p.q,
+ *     x += alpha p, r -= alpha q, stop when ||r|| < tol ||b_free|| (unchanged, R8),
+ *     z = M^-1 r, beta = (r.z)_new / rho, p = z + beta p.
+ *   Same arguments, workspace (pfem_cg_workspace_bytes), report and errors as pfem_cg.
+ * --------------------------------------------------------------------------------- */
+typedef enum { PFEM_PRECOND_NONE = 0, PFEM_PRECOND_JACOBI = 1 } pfem_precond;
+
+pfem_status pfem_tangent_diag(const pfem_mesh* m, const pfem_material* mat, const void* u_state,
+                              void* diag, const uint8_t* mask, void* stream);
+pfem_status pfem_pcg(const pfem_mesh* m, const pfem_material* mat, const void* u_state,
+                     const void* rhs, const uint8_t* mask, int32_t precond, void* x, double tol,
+                     int32_t max_iter, int32_t mode, double* history, pfem_cg_report* report,
+                     void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------------
  * Newton-Raphson for the nonlinear (Neo-Hookean) warm-start stage (App. B P:1118-1139,

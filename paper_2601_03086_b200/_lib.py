@@ -83,6 +83,11 @@ SIGNATURES = {
     "pfem_cg": (C.c_int, [C.POINTER(pfem_mesh), C.POINTER(pfem_material), C.c_void_p, C.c_void_p, C.c_void_p,
                           C.c_void_p, C.c_double, C.c_int32, C.c_int32, C.c_void_p, C.POINTER(pfem_cg_report),
                           C.c_void_p, C.c_size_t, C.c_void_p]),
+    "pfem_tangent_diag": (C.c_int, [C.POINTER(pfem_mesh), C.POINTER(pfem_material), C.c_void_p, C.c_void_p,
+                                    C.c_void_p, C.c_void_p]),
+    "pfem_pcg": (C.c_int, [C.POINTER(pfem_mesh), C.POINTER(pfem_material), C.c_void_p, C.c_void_p, C.c_void_p,
+                           C.c_int32, C.c_void_p, C.c_double, C.c_int32, C.c_int32, C.c_void_p,
+                           C.POINTER(pfem_cg_report), C.c_void_p, C.c_size_t, C.c_void_p]),
     "pfem_newton_workspace_bytes": (C.c_size_t, [C.POINTER(pfem_mesh)]),
     "pfem_newton": (C.c_int, [C.POINTER(pfem_mesh), C.POINTER(pfem_material), C.c_void_p, C.c_void_p, C.c_void_p,
                               C.c_double, C.c_int32, C.c_double, C.c_int32, C.c_int32, C.c_void_p,

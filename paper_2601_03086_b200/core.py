@@ -238,9 +238,24 @@ def tangent_apply(mesh: Mesh, mat: Material, v: torch.Tensor, u=None, mask=None,
     return Kv
 
 
+PRECONDS = {None: 0, "none": 0, "jacobi": 1}
+
+
+def tangent_diag(mesh: Mesh, mat: Material, u_state=None, mask=None, out=None):
+    """pfem_tangent_diag: diagonal [N][d] of the masked tangent (Jacobi preconditioner)."""
+    if u_state is not None:
+        u_state = _field(mesh, u_state)[0]
+    if out is None:
+        out = torch.empty((mesh.n_nodes, mesh.dim), dtype=mesh.dtype, device=mesh.coords.device)
+    mc = mat.c()
+    L.check(L.load().pfem_tangent_diag(mesh.ref(), C.byref(mc), _ptr(u_state), _ptr(out), _ptr(mask), _stream()))
+    return out
+
+
 def cg(mesh: Mesh, mat: Material, f: torch.Tensor, x0: torch.Tensor, mask=None, tol: float = 1e-8,
-       max_iter: int = 50000, u_state=None, mode: str = "csr", history: bool = True):
-    """pfem_cg: warm-started CG; returns (x, report dict with history)."""
+       max_iter: int = 50000, u_state=None, mode: str = "csr", history: bool = True, precond=None):
+    """pfem_cg (precond None) / pfem_pcg (precond "jacobi"): warm-started CG; returns
+    (x, report dict with history)."""
     f = _field(mesh, f)[0]
     x = _field(mesh, x0)[0].clone()
     if u_state is not None:
@@ -249,8 +264,13 @@ def cg(mesh: Mesh, mat: Material, f: torch.Tensor, x0: torch.Tensor, mask=None, 
     rep = L.pfem_cg_report()
     ws = mesh.cg_workspace()
     mc = mat.c()
-    st = L.load().pfem_cg(mesh.ref(), C.byref(mc), _ptr(u_state), _ptr(f), _ptr(mask), _ptr(x), tol, max_iter,
-                          MODES[mode], _ptr(hist), C.byref(rep), _ptr(ws), ws.numel(), _stream())
+    if precond is None:
+        st = L.load().pfem_cg(mesh.ref(), C.byref(mc), _ptr(u_state), _ptr(f), _ptr(mask), _ptr(x), tol,
+                              max_iter, MODES[mode], _ptr(hist), C.byref(rep), _ptr(ws), ws.numel(), _stream())
+    else:
+        st = L.load().pfem_pcg(mesh.ref(), C.byref(mc), _ptr(u_state), _ptr(f), _ptr(mask), PRECONDS[precond],
+                               _ptr(x), tol, max_iter, MODES[mode], _ptr(hist), C.byref(rep), _ptr(ws),
+                               ws.numel(), _stream())
     report = {"status": st, "iterations": rep.iterations, "converged": bool(rep.converged),
               "rel_res0": rep.rel_res0, "rel_res_final": rep.rel_res_final,
               "true_rel_res_final": rep.true_rel_res_final, "bnorm": rep.bnorm,

@@ -32,7 +32,9 @@ pfem_status run_newton(const pfem_mesh* m, const pfem_material* mat, void* u, co
                        pfem_newton_report* rep, void* ws, cudaStream_t s);
 pfem_status run_cg(const pfem_mesh* m, const pfem_material* mat, const void* u_state, const void* rhs,
                    const uint8_t* mask, void* x, double tol, int max_iter, int mode, double* history,
-                   pfem_cg_report* rep, void* ws, cudaStream_t s);
+                   pfem_cg_report* rep, void* ws, cudaStream_t s, int precond);
+pfem_status run_tangent_diag(const pfem_mesh* m, const pfem_material* mat, const void* u, const uint8_t* mask,
+                             int invert, void* out, cudaStream_t s);
 
 template <class T>
 __global__ void k_lame(int64_t n, int kind, const T* p0, int64_t s0, const T* p1, int64_t s1, T* mu, T* lam) {
@@ -257,6 +259,35 @@ size_t pfem_cg_workspace_bytes(const pfem_mesh* m) {
     return cg_ws_bytes(*reinterpret_cast<const Plan*>(m->plan), m->dtype);
 }
 
+pfem_status pfem_tangent_diag(const pfem_mesh* m, const pfem_material* mat, const void* u_state, void* diag,
+                              const uint8_t* mask, void* stream) {
+    pfem_status st = check_mesh(m, true);
+    if (st) return st;
+    if ((st = check_mat(mat))) return st;
+    if (!diag) { set_error("pfem_tangent_diag: diag is required"); return PFEM_ERR_ARG; }
+    if (mat->model == PFEM_NEOHOOKEAN && !u_state) { set_error("pfem_tangent_diag: Neo-Hookean needs u_state"); return PFEM_ERR_ARG; }
+    st = run_tangent_diag(m, mat, u_state, mask, 0, diag, (cudaStream_t)stream);
+    if (st == PFEM_OK) count_launch();
+    return st;
+}
+
+pfem_status pfem_pcg(const pfem_mesh* m, const pfem_material* mat, const void* u_state, const void* rhs,
+                     const uint8_t* mask, int32_t precond, void* x, double tol, int32_t max_iter, int32_t mode,
+                     double* history, pfem_cg_report* report, void* ws, size_t ws_bytes, void* stream) {
+    if (precond != PFEM_PRECOND_NONE && precond != PFEM_PRECOND_JACOBI) { set_error("pfem_pcg: bad precond"); return PFEM_ERR_ARG; }
+    pfem_status st = check_mesh(m, true);
+    if (st) return st;
+    if ((st = check_mat(mat))) return st;
+    if (!rhs || !x || !report || !ws) { set_error("pfem_pcg: NULL argument"); return PFEM_ERR_ARG; }
+    if (mat->model == PFEM_NEOHOOKEAN && !u_state) { set_error("pfem_pcg: Neo-Hookean needs u_state"); return PFEM_ERR_ARG; }
+    if (!(tol >= 0.0) || max_iter < 0) { set_error("pfem_pcg: bad tol / max_iter"); return PFEM_ERR_ARG; }
+    if (mode != PFEM_ASSEMBLE_CSR && mode != PFEM_ASSEMBLE_COLOUR) { set_error("bad assembly mode"); return PFEM_ERR_ARG; }
+    if (ws_bytes < pfem_cg_workspace_bytes(m)) { set_error("pfem_pcg: workspace too small"); return PFEM_ERR_CAPACITY; }
+    memset(report, 0, sizeof(*report));
+    return run_cg(m, mat, u_state, rhs, mask, x, tol, max_iter, mode, history, report, ws, (cudaStream_t)stream,
+                  precond);
+}
+
 pfem_status pfem_cg(const pfem_mesh* m, const pfem_material* mat, const void* u_state, const void* rhs,
                     const uint8_t* mask, void* x, double tol, int32_t max_iter, int32_t mode, double* history,
                     pfem_cg_report* report, void* ws, size_t ws_bytes, void* stream) {
@@ -269,7 +300,7 @@ pfem_status pfem_cg(const pfem_mesh* m, const pfem_material* mat, const void* u_
     if (mode != PFEM_ASSEMBLE_CSR && mode != PFEM_ASSEMBLE_COLOUR) { set_error("bad assembly mode"); return PFEM_ERR_ARG; }
     if (ws_bytes < pfem_cg_workspace_bytes(m)) { set_error("pfem_cg: workspace too small"); return PFEM_ERR_CAPACITY; }
     memset(report, 0, sizeof(*report));
-    return run_cg(m, mat, u_state, rhs, mask, x, tol, max_iter, mode, history, report, ws, (cudaStream_t)stream);
+    return run_cg(m, mat, u_state, rhs, mask, x, tol, max_iter, mode, history, report, ws, (cudaStream_t)stream, 0);
 }
 
 size_t pfem_newton_workspace_bytes(const pfem_mesh* m) {

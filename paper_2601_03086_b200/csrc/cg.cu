@@ -10,6 +10,10 @@
 //   k_cg_dir             (p = r + beta p)
 // captured B at a time in a CUDA graph and replayed until the device flag says done;
 // converged / broken-down iterations exit at their first instruction.
+//
+// Jacobi preconditioning (reading R27): z = D^-1 r with
+// D = diag(A) from k_tangent_diag; rho = r.z drives alpha and beta, the stop test stays on
+// ||r|| (R8).  z is never stored: k_cg_update forms r.z with r.r, k_cg_dir p = D^-1 r + beta p.
 #include <algorithm>
 
 #include "launch.cuh"
@@ -25,6 +29,7 @@ struct VecRed {
     int32_t counter;
     int32_t pad[63];
     double part[VEC_MAX_GRID];
+    double part2[VEC_MAX_GRID];   // second reduction of the same pass (PCG r.z)
 };
 
 // grid-stride passes of VEC_U elements per thread: i0 + u * stride, u < VEC_U
@@ -42,6 +47,25 @@ __device__ __forceinline__ bool vec_last_block(VecRed* vr, double v, double* s_r
     }
     __syncthreads();
     return *s_flag;
+}
+
+// two sums in one pass: per-CTA partials of both, the last CTA returns true
+__device__ __forceinline__ bool vec_last_block2(VecRed* vr, double v, double v2, double* s_red, int* s_flag) {
+    const double t2 = cta_sum<VEC_NT>(v2, s_red);
+    if (threadIdx.x == 0) vr->part2[blockIdx.x] = t2;
+    return vec_last_block(vr, v, s_red, s_flag);   // (its leading barrier orders the reuse of s_red)
+}
+
+__device__ __forceinline__ double vec_final_part2(VecRed* vr, double* s_red) {
+    double v = 0.0;
+    for (int i0 = threadIdx.x; i0 < (int)gridDim.x; i0 += 8 * VEC_NT) {
+        double w[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) w[u] = i0 + u * VEC_NT < (int)gridDim.x ? ld_relaxed(vr->part2 + i0 + u * VEC_NT) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v += w[u];
+    }
+    return cta_sum<VEC_NT>(v, s_red);
 }
 
 // fixed-order sum of the per-CTA partials (called by the last CTA, valid in thread 0)
@@ -85,27 +109,33 @@ k_cg_rhs(int64_t n, const uint8_t* __restrict__ mask, const T* __restrict__ f, c
     if (threadIdx.x == 0) cg->bnorm2 = t;
 }
 
-// r = b - A x (free DOFs), p = r, rho = r.r; skip rule / zero rhs
+// r = b - A x (free DOFs), p = z = D^-1 r (z = r without preconditioner), rho = r.z,
+// rho_new = r.r; skip rule / zero rhs
 template <class T>
 __global__ void __launch_bounds__(VEC_NT)
 k_cg_r0(int64_t n, const uint8_t* __restrict__ mask, const T* __restrict__ b, const T* __restrict__ ax,
-        T* __restrict__ r, T* __restrict__ p, T* __restrict__ x, CgState* cg, VecRed* vr, double* history) {
+        T* __restrict__ r, T* __restrict__ p, T* __restrict__ x, CgState* cg, VecRed* vr, double* history,
+        const T* __restrict__ dinv) {
     __shared__ double s_red[VEC_NT / 32];
     __shared__ int s_flag;
-    double acc = 0.0;
+    double acc = 0.0, accz = 0.0;
     const bool zero_rhs = cg->bnorm2 == 0.0;
     for (int64_t i = (int64_t)blockIdx.x * VEC_NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * VEC_NT) {
         const bool c = mask && mask[i];
         T v = c ? T(0) : b[i] - ax[i];
         r[i] = v;
-        p[i] = v;
+        const T z = dinv ? dinv[i] * v : v;
+        p[i] = z;
         if (zero_rhs && !c) x[i] = T(0);
         acc += (double)v * (double)v;
+        accz += (double)v * (double)z;
     }
-    if (!vec_last_block(vr, acc, s_red, &s_flag)) return;
+    if (!vec_last_block2(vr, acc, accz, s_red, &s_flag)) return;
+    const double tz = vec_final_part2(vr, s_red);
     const double t = vec_final(vr, s_red);
     if (threadIdx.x == 0) {
-        cg->rho = t;
+        cg->rho = dinv ? tz : t;
+        cg->rho_new = t;
         cg->k = 0;
         const double bn2 = cg->bnorm2;
         cg->pad0 = bn2 > 0 ? sqrt(t / bn2) : 0.0;   // rel_res0
@@ -124,21 +154,24 @@ k_cg_r0(int64_t n, const uint8_t* __restrict__ mask, const T* __restrict__ b, co
     }
 }
 
-template <class T>
+template <class T, bool PRE>
 __global__ void __launch_bounds__(VEC_NT)
 k_cg_update(int64_t n, T* __restrict__ x, T* __restrict__ r, const T* __restrict__ p, const T* __restrict__ q,
-            CgState* cg, VecRed* vr, double* history) {
+            CgState* cg, VecRed* vr, double* history, const T* __restrict__ dinv) {
     __shared__ double s_red[VEC_NT / 32];
     __shared__ int s_flag;
     if (ld_relaxed_i(&cg->done)) return;
     const T alpha = (T)cg->alpha;
-    double acc = 0.0;
+    double acc = 0.0, accz = 0.0;
     VEC_PASSES(n) {
-        T xv[VEC_U], pv[VEC_U], qv[VEC_U], rv[VEC_U];
+        T xv[VEC_U], pv[VEC_U], qv[VEC_U], rv[VEC_U], dv[VEC_U];
 #pragma unroll
         for (int u = 0; u < VEC_U; ++u) {
             const int64_t i = VEC_IDX(u);
-            if (i < n) { xv[u] = x[i]; pv[u] = p[i]; qv[u] = q[i]; rv[u] = r[i]; }
+            if (i < n) {
+                xv[u] = x[i]; pv[u] = p[i]; qv[u] = q[i]; rv[u] = r[i];
+                if (PRE) dv[u] = dinv[i];
+            }
         }
 #pragma unroll
         for (int u = 0; u < VEC_U; ++u) {
@@ -148,18 +181,27 @@ k_cg_update(int64_t n, T* __restrict__ x, T* __restrict__ r, const T* __restrict
             const T v = fma(-alpha, qv[u], rv[u]);
             r[i] = v;
             acc += (double)v * (double)v;
+            if (PRE) accz += (double)v * (double)(dv[u] * v);
         }
     }
-    if (!vec_last_block(vr, acc, s_red, &s_flag)) return;
-    const double t = vec_final(vr, s_red);
+    double t, tz;
+    if (PRE) {
+        if (!vec_last_block2(vr, acc, accz, s_red, &s_flag)) return;
+        tz = vec_final_part2(vr, s_red);
+        t = vec_final(vr, s_red);
+    } else {
+        if (!vec_last_block(vr, acc, s_red, &s_flag)) return;
+        t = vec_final(vr, s_red);
+        tz = t;
+    }
     if (threadIdx.x == 0) {
         const int k = cg->k + 1;
         cg->k = k;
         cg->rho_new = t;
         const double bn2 = cg->bnorm2;
         if (history) history[k] = sqrt(t / bn2);
-        cg->beta = t / cg->rho;
-        cg->rho = t;
+        cg->beta = tz / cg->rho;
+        cg->rho = tz;
         if (t < cg->tol2 * bn2) {
             cg->status = 1;
             cg->done = 1;
@@ -170,24 +212,128 @@ k_cg_update(int64_t n, T* __restrict__ x, T* __restrict__ r, const T* __restrict
     }
 }
 
-template <class T>
+template <class T, bool PRE>
 __global__ void __launch_bounds__(VEC_NT)
-k_cg_dir(int64_t n, const T* __restrict__ r, T* __restrict__ p, const CgState* cg) {
+k_cg_dir(int64_t n, const T* __restrict__ r, T* __restrict__ p, const CgState* cg, const T* __restrict__ dinv) {
     if (ld_relaxed_i(&cg->done)) return;
     const T beta = (T)cg->beta;
     VEC_PASSES(n) {
-        T pv[VEC_U], rv[VEC_U];
+        T pv[VEC_U], rv[VEC_U], dv[VEC_U];
 #pragma unroll
         for (int u = 0; u < VEC_U; ++u) {
             const int64_t i = VEC_IDX(u);
-            if (i < n) { pv[u] = p[i]; rv[u] = r[i]; }
+            if (i < n) {
+                pv[u] = p[i]; rv[u] = r[i];
+                if (PRE) dv[u] = dinv[i];
+            }
         }
 #pragma unroll
         for (int u = 0; u < VEC_U; ++u) {
             const int64_t i = VEC_IDX(u);
-            if (i < n) p[i] = fma(beta, pv[u], rv[u]);
+            if (i < n) p[i] = fma(beta, pv[u], PRE ? dv[u] * rv[u] : rv[u]);
         }
     }
+}
+
+// Jacobi diagonal of A = (I-M) K(u) (I-M) + M (reading R27), one thread
+// per node over the mesh's node -> (element, slot) CSR in ascending (e, a) order (the CSR sum
+// of R12): the diagonal of the element tangent block of vertex a is
+//   K_(a,i),(a,i) = V [mu |g_a|^2 + c ((F^-T g_a)_i)^2],  c = lam + mu - lam ln J   (NH)
+//   (linear: F^-T = I, c = lam + mu), from dP_ij/dF_kl of App. B P:1104-1115 with k = i.
+// Constrained DOFs get 1.  invert: write 1/diag (1 where diag <= 0 or not finite).
+template <int D, int MODEL, class T>
+__global__ void __launch_bounds__(VEC_NT)
+k_tangent_diag(int N, int E, const int32_t* __restrict__ csr_ptr, const int32_t* __restrict__ csr_ent,
+               const int32_t* __restrict__ conn, const T* __restrict__ grad, const T* __restrict__ vol,
+               MatArgs<T> mat, const T* __restrict__ u, const uint8_t* __restrict__ mask, int invert,
+               T* __restrict__ out) {
+    constexpr int NV = D + 1;
+    for (int n = blockIdx.x * VEC_NT + threadIdx.x; n < N; n += gridDim.x * VEC_NT) {
+        T acc[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) acc[i] = T(0);
+        for (int k = __ldg(csr_ptr + n); k < __ldg(csr_ptr + n + 1); ++k) {
+            const int ent = __ldg(csr_ent + k);
+            const int e = ent / NV, a = ent - e * NV;
+            Geo<D, T> G;
+            load_geo<D, T>(e, E, conn, grad, vol, mat, G);   // mu, lam scaled by V_e
+            T ga[D];   // grad N_a (grad N_0 = -sum of the others); compile-time register indices
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                T s = G.g[0][j];
+#pragma unroll
+                for (int b = 1; b < D; ++b) s += G.g[b][j];
+                ga[j] = -s;
+#pragma unroll
+                for (int b = 0; b < D; ++b)
+                    if (a == b + 1) ga[j] = G.g[b][j];
+            }
+            T gg = ga[0] * ga[0];
+#pragma unroll
+            for (int j = 1; j < D; ++j) gg = fma(ga[j], ga[j], gg);
+            T Ag[D];
+            T c;
+            if constexpr (MODEL == MODEL_NH) {
+                T x[NV][D], H[D][D];
+                gather<D, T, T, false>(u, 0, nullptr, G, x);
+                grad_of<D, T, T>(G, x, H);
+                NhState<D, T> NS;
+                nh_state<D, T>(H, NS);
+#pragma unroll
+                for (int i = 0; i < D; ++i) {
+                    T s = NS.A[i][0] * ga[0];
+#pragma unroll
+                    for (int j = 1; j < D; ++j) s = fma(NS.A[i][j], ga[j], s);
+                    Ag[i] = s;
+                }
+                c = G.lam + G.mu - G.lam * NS.lnJ;
+            } else {
+#pragma unroll
+                for (int i = 0; i < D; ++i) Ag[i] = ga[i];
+                c = G.lam + G.mu;
+            }
+#pragma unroll
+            for (int i = 0; i < D; ++i) acc[i] += fma(c * Ag[i], Ag[i], G.mu * gg);
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            const int64_t dof = (int64_t)n * D + i;
+            T v = (mask && mask[dof]) ? T(1) : acc[i];
+            if (invert) v = (v > T(0) && isfinite(v)) ? T(1) / v : T(1);
+            out[dof] = v;
+        }
+    }
+}
+
+template <int D, class T>
+pfem_status tangent_diag_impl(const pfem_mesh* m, const pfem_material* mat, const void* u, const uint8_t* mask,
+                              int invert, void* out, cudaStream_t s) {
+    MatArgs<T> ma;
+    ma.kind = mat->kind;
+    ma.p0 = (const T*)mat->p0;
+    ma.p1 = (const T*)mat->p1;
+    ma.s0 = mat->stride0;
+    ma.s1 = mat->stride1;
+    const int grid = std::max(1, std::min(65535, (m->n_nodes + VEC_NT - 1) / VEC_NT));
+    if (mat->model == MODEL_NH)
+        k_tangent_diag<D, MODEL_NH, T><<<grid, VEC_NT, 0, s>>>(m->n_nodes, m->n_elems, m->csr_ptr, m->csr_ent, m->conn,
+                                                               (const T*)m->grad, (const T*)m->vol, ma, (const T*)u,
+                                                               mask, invert, (T*)out);
+    else
+        k_tangent_diag<D, MODEL_LINEAR, T><<<grid, VEC_NT, 0, s>>>(m->n_nodes, m->n_elems, m->csr_ptr, m->csr_ent,
+                                                                   m->conn, (const T*)m->grad, (const T*)m->vol, ma,
+                                                                   (const T*)u, mask, invert, (T*)out);
+    PFEM_LAUNCH_CHECK("k_tangent_diag");
+    return PFEM_OK;
+}
+
+pfem_status run_tangent_diag(const pfem_mesh* m, const pfem_material* mat, const void* u, const uint8_t* mask,
+                             int invert, void* out, cudaStream_t s) {
+    if (m->dim == 2)
+        return m->dtype == PFEM_F32 ? tangent_diag_impl<2, float>(m, mat, u, mask, invert, out, s)
+                                    : tangent_diag_impl<2, double>(m, mat, u, mask, invert, out, s);
+    return m->dtype == PFEM_F32 ? tangent_diag_impl<3, float>(m, mat, u, mask, invert, out, s)
+                                : tangent_diag_impl<3, double>(m, mat, u, mask, invert, out, s);
 }
 
 // COLOUR-mode CG: p.q and alpha as a separate pass
@@ -232,7 +378,7 @@ k_cg_true(int64_t n, const uint8_t* __restrict__ mask, const T* __restrict__ b, 
 }
 
 struct CgWs {
-    size_t state, vr, r, p, q, b, asmws, total;
+    size_t state, vr, r, p, q, b, dinv, asmws, total;
 };
 
 inline CgWs cg_layout(const Plan& P, size_t tsize) {
@@ -245,6 +391,7 @@ inline CgWs cg_layout(const Plan& P, size_t tsize) {
     L.p = o;     o += nvec;
     L.q = o;     o += nvec;
     L.b = o;     o += nvec;
+    L.dinv = o;  o += nvec;
     L.asmws = o; o += ws_layout(P, 1, tsize).total;
     L.total = o;
     return L;
@@ -280,7 +427,7 @@ static pfem_status tangent(const pfem_mesh* m, const Plan* P, const pfem_materia
 template <int D, class T>
 pfem_status cg_impl(const pfem_mesh* m, const pfem_material* mat, const void* u_state, const void* rhs,
                     const uint8_t* mask, void* xv, double tol, int max_iter, int mode, double* history,
-                    pfem_cg_report* rep, void* ws, cudaStream_t s) {
+                    pfem_cg_report* rep, void* ws, cudaStream_t s, int precond = 0) {
     const Plan* P = reinterpret_cast<const Plan*>(m->plan);
     const CgWs L = cg_layout(*P, sizeof(T));
     char* w = (char*)ws;
@@ -290,6 +437,7 @@ pfem_status cg_impl(const pfem_mesh* m, const pfem_material* mat, const void* u_
     T* p = (T*)(w + L.p);
     T* q = (T*)(w + L.q);
     T* b = (T*)(w + L.b);
+    T* dinv = precond ? (T*)(w + L.dinv) : nullptr;
     T* x = (T*)xv;
     void* asmws = w + L.asmws;
     const int64_t n = (int64_t)P->n_nodes * D;
@@ -309,10 +457,16 @@ pfem_status cg_impl(const pfem_mesh* m, const pfem_material* mat, const void* u_
     if (e != PFEM_OK) return e;
     k_cg_rhs<T><<<G, VEC_NT, 0, s>>>(n, mask, (const T*)rhs, q, b, st, vr);
     PFEM_LAUNCH_CHECK("k_cg_rhs");
+    // Jacobi: D^-1 of the masked operator at u_state
+    if (dinv) {
+        e = tangent_diag_impl<D, T>(m, mat, u_state, mask, 1, dinv, s);
+        if (e != PFEM_OK) return e;
+        count_launch();
+    }
     // r0 = b - A x0
     e = tangent<D, T>(m, P, mat, u_state, x, q, mask, mode, asmws, nullptr, s);
     if (e != PFEM_OK) return e;
-    k_cg_r0<T><<<G, VEC_NT, 0, s>>>(n, mask, b, q, r, p, x, st, vr, history);
+    k_cg_r0<T><<<G, VEC_NT, 0, s>>>(n, mask, b, q, r, p, x, st, vr, history, dinv);
     PFEM_LAUNCH_CHECK("k_cg_r0");
     PFEM_CUDA_TRY(cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, s));
     PFEM_CUDA_TRY(cudaStreamSynchronize(s));
@@ -334,8 +488,13 @@ pfem_status cg_impl(const pfem_mesh* m, const pfem_material* mat, const void* u_
                 k_cg_pq<T><<<G, VEC_NT, 0, cs>>>(n, p, q, st, vr);
                 count_launch();
             }
-            k_cg_update<T><<<G, VEC_NT, 0, cs>>>(n, x, r, p, q, st, vr, history);
-            k_cg_dir<T><<<G, VEC_NT, 0, cs>>>(n, r, p, st);
+            if (dinv) {
+                k_cg_update<T, true><<<G, VEC_NT, 0, cs>>>(n, x, r, p, q, st, vr, history, dinv);
+                k_cg_dir<T, true><<<G, VEC_NT, 0, cs>>>(n, r, p, st, dinv);
+            } else {
+                k_cg_update<T, false><<<G, VEC_NT, 0, cs>>>(n, x, r, p, q, st, vr, history, nullptr);
+                k_cg_dir<T, false><<<G, VEC_NT, 0, cs>>>(n, r, p, st, nullptr);
+            }
             count_launch(2);
         }
         cerr = cudaStreamEndCapture(cs, &graph);
@@ -376,7 +535,7 @@ pfem_status cg_impl(const pfem_mesh* m, const pfem_material* mat, const void* u_
     rep->status = h.status;
     rep->converged = h.status == 1;
     rep->bnorm = sqrt(h.bnorm2);
-    rep->rel_res_final = h.bnorm2 > 0 ? sqrt(h.rho / h.bnorm2) : 0.0;
+    rep->rel_res_final = h.bnorm2 > 0 ? sqrt(h.rho_new / h.bnorm2) : 0.0;
     rep->true_rel_res_final = h.bnorm2 > 0 ? sqrt(h.pq / h.bnorm2) : 0.0;
     rep->rel_res0 = h.pad0;
     if (h.status == 2) {
@@ -562,12 +721,12 @@ pfem_status run_newton(const pfem_mesh* m, const pfem_material* mat, void* u, co
 
 pfem_status run_cg(const pfem_mesh* m, const pfem_material* mat, const void* u_state, const void* rhs,
                    const uint8_t* mask, void* x, double tol, int max_iter, int mode, double* history,
-                   pfem_cg_report* rep, void* ws, cudaStream_t s) {
+                   pfem_cg_report* rep, void* ws, cudaStream_t s, int precond) {
     if (m->dim == 2)
-        return m->dtype == PFEM_F32 ? cg_impl<2, float>(m, mat, u_state, rhs, mask, x, tol, max_iter, mode, history, rep, ws, s)
-                                    : cg_impl<2, double>(m, mat, u_state, rhs, mask, x, tol, max_iter, mode, history, rep, ws, s);
-    return m->dtype == PFEM_F32 ? cg_impl<3, float>(m, mat, u_state, rhs, mask, x, tol, max_iter, mode, history, rep, ws, s)
-                                : cg_impl<3, double>(m, mat, u_state, rhs, mask, x, tol, max_iter, mode, history, rep, ws, s);
+        return m->dtype == PFEM_F32 ? cg_impl<2, float>(m, mat, u_state, rhs, mask, x, tol, max_iter, mode, history, rep, ws, s, precond)
+                                    : cg_impl<2, double>(m, mat, u_state, rhs, mask, x, tol, max_iter, mode, history, rep, ws, s, precond);
+    return m->dtype == PFEM_F32 ? cg_impl<3, float>(m, mat, u_state, rhs, mask, x, tol, max_iter, mode, history, rep, ws, s, precond)
+                                : cg_impl<3, double>(m, mat, u_state, rhs, mask, x, tol, max_iter, mode, history, rep, ws, s, precond);
 }
 
 }  // namespace pfem

@@ -406,3 +406,75 @@ def test_empty_and_tiny_parts(orc):
         assert np.all(t[:, [0, 2, 4]] == 0.0)
         assert max_rel(t[:, [1, 3]], tot_ref[:, [1, 3]]) < 1e-12
         assert rel_l2(r.cpu().numpy(), om.residual(prob.u)) < 1e-12
+
+
+# ------------------------------------------------------------------ Jacobi PCG (§8(f) row f3)
+@pytest.mark.parametrize("prob", SMALL[:4], ids=lambda p: p.name)
+def test_tangent_diag_matches_oracle(orc, prob):
+    """pfem_tangent_diag vs the oracle's textbook element-tangent diagonals (reading R27), with
+    and without a Dirichlet mask, at the NH state u (first sample)."""
+    import paper_2601_03086_b200 as pf
+    mesh, mat, u = gpu_problem(prob)
+    om = oracle_problem(orc, prob)
+    us = u[0] if prob.model == "neohookean" else None
+    uo = rounded(prob.u[0], prob.dtype) if prob.model == "neohookean" else None
+    rng = np.random.default_rng(9)
+    for mk in (None, (rng.random(prob.n_nodes * prob.dim) < 0.1).astype(np.uint8)):
+        mt = None if mk is None else torch.as_tensor(mk, device="cuda")
+        d = pf.tangent_diag(mesh, mat, u_state=us, mask=mt)
+        do = om.tangent_diag(u=uo, mask=mk)
+        assert rel_l2(d.cpu().numpy(), do) < TOL[prob.dtype]
+        if mk is not None:
+            assert np.all(d.cpu().numpy().ravel()[mk == 1] == 1.0)
+
+
+@pytest.mark.parametrize("n", [12])
+def test_pcg_config4_scaled(orc, n):
+    """Jacobi PCG on the config-4 recipe at n^3 nodes (fp64) vs the oracle PCG: iteration count
+    within +-1 or the R18 spread of the unpreconditioned oracle, histories within 1e-6 over the
+    first 50 iterations, true residual below tol; zero and warm start, both assembly modes."""
+    import paper_2601_03086_b200 as pf
+    from pfem_gen import small_cube_problem, warm_start
+    p = small_cube_problem(n_nodes=n, brick=4)
+    mesh, mat, _ = gpu_problem(p)
+    om = oracle_problem(orc, p)
+    f = torch.as_tensor(p.f_ext, device="cuda")
+    mask = torch.as_tensor(p.mask, device="cuda")
+    xs, _ = om.cg(p.f_ext, p.mask, np.zeros_like(p.f_ext), tol=1e-12, history=False)
+    x0w = warm_start(xs, p.mask, seed=4004)
+    for x0 in (np.zeros_like(p.f_ext), x0w):
+        xo, ro = om.pcg(p.f_ext, p.mask, x0, tol=1e-8)
+        assert ro["converged"]
+        for mode in ("csr", "colour"):
+            x, rep = pf.cg(mesh, mat, f, torch.as_tensor(x0, device="cuda"), mask=mask, tol=1e-8, mode=mode,
+                           precond="jacobi")
+            assert rep["converged"]
+            assert abs(rep["iterations"] - ro["iterations"]) <= 2, (rep["iterations"], ro["iterations"])
+            h, ho = rep["history"], ro["history"]
+            m = min(50, len(h), len(ho))
+            assert np.max(np.abs(h[:m] - ho[:m]) / ho[:m]) < 1e-6
+            assert rep["true_rel_res_final"] < 2e-8
+            assert rel_l2(x.cpu().numpy(), xo) < 1e-6
+    # precond "none" through pfem_pcg is pfem_cg
+    x1, r1 = pf.cg(mesh, mat, f, torch.zeros_like(f), mask=mask, tol=1e-8, precond="none")
+    x2, r2 = pf.cg(mesh, mat, f, torch.zeros_like(f), mask=mask, tol=1e-8)
+    assert r1["iterations"] == r2["iterations"] and torch.equal(x1, x2)
+
+
+def test_pcg_neohookean_state(orc):
+    """Jacobi PCG on the NH tangent at a non-trivial state (the Newton inner solve) vs the
+    oracle PCG (fp64)."""
+    import paper_2601_03086_b200 as pf
+    from pfem_gen import newton_block
+    p = newton_block(6, traction=(0.05, 0.0, 0.02))
+    mesh, mat, _ = gpu_problem(p)
+    om = oracle_problem(orc, p)
+    rng = np.random.default_rng(21)
+    us = 0.02 * fourier_field(p.coords, rng) * (1 - p.mask.reshape(p.coords.shape))
+    f = torch.as_tensor(p.f_ext, device="cuda")
+    mask = torch.as_tensor(p.mask, device="cuda")
+    x, rep = pf.cg(mesh, mat, f, torch.zeros_like(f), mask=mask, tol=1e-10, u_state=torch.as_tensor(us, device="cuda"),
+                   precond="jacobi")
+    xo, ro = om.pcg(p.f_ext, p.mask, np.zeros_like(p.f_ext), tol=1e-10, u_state=us)
+    assert rep["converged"] and ro["converged"] and abs(rep["iterations"] - ro["iterations"]) <= 2
+    assert rel_l2(x.cpu().numpy(), xo) < 1e-8
