@@ -179,6 +179,24 @@ class Mesh:
         _check(st, "residual")
         return r
 
+    def pretrain_loss(self, H, phi=None, f_ext=None):
+        """Energy-based pretraining loss and its gradient w.r.t. the network output (SURVEY §8(f)
+        row f2; P:518-541 linear, P:700-723 Neo-Hookean; reading R28):
+            u = phi (.) H                                   (hard-BC ansatz u = (x/L) (.) H_theta)
+            Pi_{s,k} = W_{s,k}(u) - f_ext . u               (discrete L of P:518-524 per sample / part)
+            loss = mean over (s, k) of Pi_{s,k}             (batch mean, Eq. 2)
+            dloss/dH = phi (.) (f_int(u) - f_ext) / (S K)   (chain rule; f_int = dW/du, App. B)
+        H [S, N, d]; phi [N, d] or None (= 1); returns (loss, Pi [S, K], grad [S, N, d], u)."""
+        H = _f64(H).reshape(-1, self.n_nodes, self.dim)
+        ph = np.ones((self.n_nodes, self.dim)) if phi is None else _f64(phi).reshape(self.n_nodes, self.dim)
+        fe = np.zeros((self.n_nodes, self.dim)) if f_ext is None else _f64(f_ext).reshape(self.n_nodes, self.dim)
+        u = ph[None] * H
+        _, Pi = self.energy(u, f_ext=fe, want_elem=False)
+        S, K = Pi.shape
+        loss = float(Pi.sum()) / (S * K)
+        grad = ph[None] * (self.residual(u) - fe[None]) / (S * K)
+        return loss, Pi, grad, u
+
     def tangent(self, v, u=None, mask=None):
         """K(u) v  [S, N, d]; with mask: (I-M) K (I-M) v + M v."""
         v = _f64(v).reshape(-1, self.n_nodes, self.dim)

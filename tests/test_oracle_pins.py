@@ -659,3 +659,40 @@ def test_pcg_is_cg_on_the_jacobi_scaled_system(orc):
     assert np.array_equal(x0, xc)
     _, rs = m.pcg(p.f_ext, p.mask, x_ref, tol=1e-8)
     assert rs["iterations"] == 0 and rs["converged"]
+
+
+# ---------------------------------------------------------------- pretraining loss (§8(f) row f2)
+@pytest.mark.parametrize("model", ["linear", "neohookean"])
+def test_pretrain_loss_gradient_is_finite_difference(orc, model):
+    """dloss/dH of the energy loss through the hard-BC ansatz u = phi (.) H
+    equals the central finite difference of the loss (two parts, two samples: the batch mean
+    divides by S K); phi = 0 rows (the clamped edge) have zero gradient."""
+    ca, ta = jittered_square(4, 31)
+    cb, tb = jittered_square(3, 32)
+    coords = np.concatenate([ca, cb + 2.0])
+    conn = np.concatenate([ta, tb + len(ca)])
+    pe = np.array([0, len(ta), len(conn)], np.int32)
+    pn = np.array([0, len(ca), len(coords)], np.int32)
+    m = orc.prepare(coords, conn, model, "lame", [0.4], [0.6], pe, pn)
+    rng = np.random.default_rng(4)
+    phi = (coords[:, :1] - np.where(np.arange(len(coords)) < len(ca), 0.0, 2.0)[:, None]) * np.ones((1, 2))
+    f = 0.01 * rng.standard_normal(coords.shape)
+    H = 0.05 * rng.standard_normal((2,) + coords.shape)
+    loss, Pi, grad, u = m.pretrain_loss(H, phi, f)
+    assert Pi.shape == (2, 2) and abs(loss - Pi.mean()) < 1e-15
+    # Pi = W - f.u per part (P:518-524), W from energy() without f
+    _, W = m.energy(u, want_elem=False)
+    fu = np.stack([[np.sum(f[pn[k]:pn[k + 1]] * u[s, pn[k]:pn[k + 1]]) for k in range(2)] for s in range(2)])
+    assert np.max(np.abs(Pi - (W - fu))) < 1e-15
+    h = 1e-6
+    idx = [(0, 1, 0), (1, 3, 1), (0, len(ca) + 4, 0), (1, len(coords) - 1, 1), (0, 0, 1)]
+    for s, n, i in idx:
+        Hp, Hm = H.copy(), H.copy()
+        Hp[s, n, i] += h
+        Hm[s, n, i] -= h
+        fd = (m.pretrain_loss(Hp, phi, f)[0] - m.pretrain_loss(Hm, phi, f)[0]) / (2 * h)
+        assert abs(fd - grad[s, n, i]) < 1e-8 * max(1.0, abs(grad).max()), (s, n, i, fd, grad[s, n, i])
+    assert np.all(grad[:, phi[:, 0] == 0] == 0)
+    # phi = 1: the gradient is the potential's gradient f_int - f_ext over S K
+    _, _, g1, _ = m.pretrain_loss(H, None, f)
+    assert rel(g1, (m.residual(H) - f[None]) / 4) < 1e-15
