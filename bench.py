@@ -397,6 +397,23 @@ def run_extras(torch, pf, dev, peak):
     ex["config5_energy_residual"] = {"E": E5, "us": t5 * 1e3, "algorithmic_bytes": B5,
                                      "GBps": B5 / (t5 * 1e-3) / 1e9, "frac": B5 / (t5 * 1e-3) / 1e9 / peak,
                                      "note": "timed back-to-back on one copy: partly L2-resident (upper bound)"}
+    # §8(f) f2: the pretraining loss of the 64-sample batch through the hard-BC ansatz
+    # u = phi (.) H, phi = distance to each plate's left edge / plate width (R28)
+    phi5 = np.empty((N5, 2))
+    for k in range(len(pn) - 1):
+        x = p5.coords[pn[k]:pn[k + 1], 0]
+        phi5[pn[k]:pn[k + 1]] = ((x - x.min()) / (x.max() - x.min()))[:, None]
+    phi5t = torch.as_tensor(phi5, dtype=torch.float32, device=dev)
+    f5 = torch.zeros_like(u5[0])
+    pl_out = (torch.empty((), dtype=torch.float64, device=dev), torch.empty((1, 64), dtype=torch.float32, device=dev),
+              torch.empty_like(u5), torch.empty_like(u5))
+    for _ in range(5):
+        pf.pretrain_loss(m5, mat5, u5, phi=phi5t, f_ext=f5, out=pl_out)
+    tpl = time_events(torch, lambda: pf.pretrain_loss(m5, mat5, u5, phi=phi5t, f_ext=f5, out=pl_out), 50)
+    ex["config5_pretrain_loss"] = {"us": tpl * 1e3, "samples": 64, "samples_per_s": 64 / (tpl * 1e-3),
+                                   "loss": float(pl_out[0]),
+                                   "launches": "ansatz + fused energy/residual (A + B) + epilogue",
+                                   "note": "timed back-to-back on one copy (partly L2-resident)"}
     del m5, outs
     torch.cuda.empty_cache()
     # ---------------- §8(f) f1: Newton-Raphson warm start on a Neo-Hookean block (fp64)

@@ -197,6 +197,31 @@ pfem_status pfem_energy(const pfem_mesh* m, const pfem_material* mat, int32_t n_
                         void* elem_energy, void* totals, void* residual, int32_t mode,
                         pfem_flags* flags, void* ws, size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------------
+ * Pretraining loss and its gradient w.r.t. the network output: the
+ * energy-based loss of P:518-541 (linear) / P:700-723 (Neo-Hookean) through the hard-BC
+ * ansatz u = (x/L) (.) H_theta, batch-averaged as in Eq. 2 over samples and parts
+ * (reading R28):
+ *   u = phi (.) H                                   (phi NULL: u = H, no copy)
+ *   totals[s][k] = Pi_{s,k} = W_{s,k}(u) - sum_{n in part k} f_ext,n . u_n
+ *   *loss = sum_{s,k} Pi_{s,k} / (S K)              (device double, row order)
+ *   grad[s][n] = phi_n (.) (f_int(u)_n - f_ext,n) / (S K)
+ * Arguments:
+ *   H        [S][N][d] network output, sample stride `sample_stride`
+ *   phi      nullable [N][d] ansatz multiplier (e.g. x/L per component, or the distance to a
+ *            clamped edge broadcast over components), shared by all samples
+ *   f_ext    nullable [N][d]
+ *   u        [S][N][d] output (the ansatz field), required iff phi != NULL
+ *   totals   [S][n_parts];  grad [S][N][d];  loss: device double
+ *   mode, flags, ws, ws_bytes: as pfem_energy (same workspace)
+ * Launches: the ansatz (if phi), the fused energy + residual of pfem_energy, the epilogue.
+ * --------------------------------------------------------------------------------- */
+pfem_status pfem_pretrain_loss(const pfem_mesh* m, const pfem_material* mat, int32_t n_samples,
+                               const void* H, int64_t sample_stride, const void* phi,
+                               const void* f_ext, void* u, void* totals, void* grad, double* loss,
+                               int32_t mode, pfem_flags* flags, void* ws, size_t ws_bytes,
+                               void* stream);
+
 /* Internal force only (no energy arithmetic), see pfem_energy. */
 pfem_status pfem_residual(const pfem_mesh* m, const pfem_material* mat, int32_t n_samples,
                           const void* u, int64_t sample_stride, void* residual, int32_t mode,

@@ -83,6 +83,9 @@ SIGNATURES = {
     "pfem_cg": (C.c_int, [C.POINTER(pfem_mesh), C.POINTER(pfem_material), C.c_void_p, C.c_void_p, C.c_void_p,
                           C.c_void_p, C.c_double, C.c_int32, C.c_int32, C.c_void_p, C.POINTER(pfem_cg_report),
                           C.c_void_p, C.c_size_t, C.c_void_p]),
+    "pfem_pretrain_loss": (C.c_int, [C.POINTER(pfem_mesh), C.POINTER(pfem_material), C.c_int32, C.c_void_p,
+                                     C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "pfem_tangent_diag": (C.c_int, [C.POINTER(pfem_mesh), C.POINTER(pfem_material), C.c_void_p, C.c_void_p,
                                     C.c_void_p, C.c_void_p]),
     "pfem_pcg": (C.c_int, [C.POINTER(pfem_mesh), C.POINTER(pfem_material), C.c_void_p, C.c_void_p, C.c_void_p,

@@ -211,6 +211,28 @@ def energy(mesh: Mesh, mat: Material, u: torch.Tensor, f_ext=None, elem_energy=F
     return totals, W, r
 
 
+def pretrain_loss(mesh: Mesh, mat: Material, H: torch.Tensor, phi=None, f_ext=None, mode: str = "csr",
+                  flags=None, out=None):
+    """pfem_pretrain_loss: (loss [device double scalar], Pi totals [S, K], grad [S, N, d], u) of the
+    energy loss through the ansatz u = phi (.) H (u is H itself when phi is None)."""
+    H = _field(mesh, H)
+    S = H.shape[0]
+    dev = H.device
+    if out is None:
+        totals = torch.empty((S, mesh.n_parts), dtype=mesh.dtype, device=dev)
+        grad = torch.empty_like(H)
+        u = torch.empty_like(H) if phi is not None else None
+        loss = torch.empty((), dtype=torch.float64, device=dev)
+    else:
+        loss, totals, grad, u = out
+    ws = mesh.workspace(S)
+    mc = mat.c()
+    L.check(L.load().pfem_pretrain_loss(mesh.ref(), C.byref(mc), S, _ptr(H), H[0].numel(), _ptr(phi), _ptr(f_ext),
+                                        _ptr(u), _ptr(totals), _ptr(grad), _ptr(loss), MODES[mode], _ptr(flags),
+                                        _ptr(ws), ws.numel(), _stream()))
+    return loss, totals, grad, (u if phi is not None else H)
+
+
 def residual(mesh: Mesh, mat: Material, u: torch.Tensor, mode: str = "csr", flags=None, out=None):
     """pfem_residual: internal force f_int(u) [S, N, d]."""
     u = _field(mesh, u)

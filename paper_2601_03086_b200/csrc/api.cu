@@ -35,6 +35,9 @@ pfem_status run_cg(const pfem_mesh* m, const pfem_material* mat, const void* u_s
                    pfem_cg_report* rep, void* ws, cudaStream_t s, int precond);
 pfem_status run_tangent_diag(const pfem_mesh* m, const pfem_material* mat, const void* u, const uint8_t* mask,
                              int invert, void* out, cudaStream_t s);
+pfem_status run_pretrain_stage(const pfem_mesh* m, int S, int64_t sstride, const void* H, const void* phi, void* u,
+                               int stage, const void* f_ext, void* grad, const void* totals, double* loss,
+                               cudaStream_t s);
 
 template <class T>
 __global__ void k_lame(int64_t n, int kind, const T* p0, int64_t s0, const T* p1, int64_t s1, T* mu, T* lam) {
@@ -201,6 +204,42 @@ pfem_status pfem_energy(const pfem_mesh* m, const pfem_material* mat, int32_t n_
     c.ws_bytes = ws_bytes;
     c.stream = (cudaStream_t)stream;
     return run(c);
+}
+
+pfem_status pfem_pretrain_loss(const pfem_mesh* m, const pfem_material* mat, int32_t n_samples, const void* H,
+                               int64_t sample_stride, const void* phi, const void* f_ext, void* u, void* totals,
+                               void* grad, double* loss, int32_t mode, pfem_flags* flags, void* ws, size_t ws_bytes,
+                               void* stream) {
+    pfem_status st = common_checks(m, mat, n_samples, sample_stride, mode, ws, ws_bytes);
+    if (st) return st;
+    if (!H || !totals || !grad || !loss) { set_error("pfem_pretrain_loss: H, totals, grad and loss are required"); return PFEM_ERR_ARG; }
+    if (phi && !u) { set_error("pfem_pretrain_loss: u (the ansatz field) is required with phi"); return PFEM_ERR_ARG; }
+    cudaStream_t s = (cudaStream_t)stream;
+    const void* uu = H;
+    if (phi) {
+        if ((st = run_pretrain_stage(m, n_samples, sample_stride, H, phi, u, 0, nullptr, nullptr, nullptr, nullptr, s)))
+            return st;
+        uu = u;
+    }
+    Call c{};
+    c.m = m;
+    c.P = reinterpret_cast<const Plan*>(m->plan);
+    c.op = OP_ENERGY_RESIDUAL;
+    c.model = mat->model;
+    c.mode = mode;
+    c.S = n_samples;
+    c.sstride = sample_stride;
+    c.mat = *mat;
+    c.u = uu;
+    c.f_ext = f_ext;
+    c.totals = totals;
+    c.out = grad;
+    c.flags = flags;
+    c.ws = ws;
+    c.ws_bytes = ws_bytes;
+    c.stream = s;
+    if ((st = run(c))) return st;
+    return run_pretrain_stage(m, n_samples, sample_stride, nullptr, phi, nullptr, 1, f_ext, grad, totals, loss, s);
 }
 
 pfem_status pfem_residual(const pfem_mesh* m, const pfem_material* mat, int32_t n_samples, const void* u,

@@ -478,3 +478,29 @@ def test_pcg_neohookean_state(orc):
     xo, ro = om.pcg(p.f_ext, p.mask, np.zeros_like(p.f_ext), tol=1e-10, u_state=us)
     assert rep["converged"] and ro["converged"] and abs(rep["iterations"] - ro["iterations"]) <= 2
     assert rel_l2(x.cpu().numpy(), xo) < 1e-8
+
+
+# ------------------------------------------------------------------ pretraining loss (§8(f) row f2)
+@pytest.mark.parametrize("prob", [SMALL[1], SMALL[2], SMALL[4]], ids=lambda p: p.name)
+@pytest.mark.parametrize("with_phi", [True, False])
+def test_pretrain_loss_matches_oracle(orc, prob, with_phi):
+    """pfem_pretrain_loss vs the oracle: u = phi (.) H with phi = x_1 / L (distance to the
+    clamped edge x_1 = min, broadcast over components; R28), Pi per (sample, part), the batch
+    mean loss and dloss/dH = phi (.) (f_int - f_ext) / (S K)."""
+    import paper_2601_03086_b200 as pf
+    mesh, mat, H = gpu_problem(prob)
+    om = oracle_problem(orc, prob)
+    x = prob.coords[:, 0]
+    phi = np.repeat(((x - x.min()) / (x.max() - x.min()))[:, None], prob.dim, axis=1) if with_phi else None
+    rng = np.random.default_rng(17)
+    f = 1e-3 * rng.standard_normal(prob.coords.shape)
+    fr, phr = rounded(f, prob.dtype), None if phi is None else rounded(phi, prob.dtype)
+    dt = H.dtype
+    loss, tot, grad, u = pf.pretrain_loss(mesh, mat, H, phi=None if phi is None else torch.as_tensor(phr, dtype=dt, device="cuda"),
+                                          f_ext=torch.as_tensor(fr, dtype=dt, device="cuda"))
+    lo, Po, go, uo = om.pretrain_loss(rounded(prob.u, prob.dtype), phr, fr)
+    tol = TOL[prob.dtype]
+    assert rel_l2(u.cpu().numpy(), uo) < tol
+    assert max_rel(tot.cpu().numpy(), Po) < (1e-10 if prob.dtype == "f64" else 1e-4)
+    assert abs(float(loss) - lo) <= (1e-10 if prob.dtype == "f64" else 1e-4) * abs(lo)
+    assert rel_l2(grad.cpu().numpy(), go) < tol
