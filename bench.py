@@ -412,7 +412,7 @@ def run_extras(torch, pf, dev, peak):
     tpl = time_events(torch, lambda: pf.pretrain_loss(m5, mat5, u5, phi=phi5t, f_ext=f5, out=pl_out), 50)
     ex["config5_pretrain_loss"] = {"us": tpl * 1e3, "samples": 64, "samples_per_s": 64 / (tpl * 1e-3),
                                    "loss": float(pl_out[0]),
-                                   "launches": "ansatz + fused energy/residual (A + B) + epilogue",
+                                   "launches": "ansatz + fused energy/residual with the gradient epilogue in its writes and the loss in kernel B's last CTA",
                                    "note": "timed back-to-back on one copy (partly L2-resident)"}
     del m5, outs
     torch.cuda.empty_cache()

@@ -238,7 +238,14 @@ pfem_status pfem_pretrain_loss(const pfem_mesh* m, const pfem_material* mat, int
     c.ws = ws;
     c.ws_bytes = ws_bytes;
     c.stream = s;
+    // CSR: the epilogue is applied where kernels A / B write each DOF, and kernel B's last CTA
+    // writes the loss; COLOUR (read-modify-write passes): a separate epilogue pass
+    const bool fused = mode == PFEM_ASSEMBLE_CSR;
+    c.ep = fused ? 1 : 0;
+    c.ep_phi = phi;
+    c.ep_loss = loss;
     if ((st = run(c))) return st;
+    if (fused) return PFEM_OK;
     return run_pretrain_stage(m, n_samples, sample_stride, nullptr, phi, nullptr, 1, f_ext, grad, totals, loss, s);
 }
 

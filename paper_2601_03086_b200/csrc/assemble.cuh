@@ -119,6 +119,12 @@ struct AsmParams {
     int32_t* part_cnt;     // [K] reduced chunks per part (0 at rest)
     T* partial;            // [n_occ][S][D]
     CgState* cg;           // non-null: fused p.q and alpha epilogue (S == 1)
+    // pretraining-loss epilogue (§8(f) row f2), applied where the assembled value is written:
+    // out = phi (.) (value - f_ext) * ep_scale; the last kernel-B CTA writes the batch-mean loss
+    int ep;
+    const T* ep_phi;       // nullable (1)
+    T ep_scale;
+    double* ep_loss;       // nullable
 };
 
 // deterministic CTA reduction of one double per thread (fixed shuffle tree + fixed order)
@@ -237,6 +243,15 @@ __device__ __forceinline__ void sst(T* p, const T* v) {
 #pragma unroll
         for (int k = 0; k < N; ++k) p[k] = v[k];
     }
+}
+
+// the value written for DOF (node, i): the assembled sum, or the pretraining-loss gradient
+template <class T>
+__device__ __forceinline__ T out_value(const AsmParams<T>& p, int64_t dof, T val) {
+    if (!p.ep) return val;
+    const T fe = p.f_ext ? __ldg(p.f_ext + dof) : T(0);
+    const T ph = p.ep_phi ? __ldg(p.ep_phi + dof) : T(1);
+    return ph * (val - fe) * p.ep_scale;
 }
 
 // one chunk arrival; returns true (in all threads) if this CTA completed the chunk and
@@ -750,7 +765,7 @@ k_assemble(const AsmParams<T> p) {
                                     T val = accs[i * STH + qq];
                                     if (OP == OP_TANGENT && MASKED && __ldg(p.mask + (int64_t)node * D + i))
                                         val = __ldg(p.v + nb + i);
-                                    p.out[nb + i] = val;
+                                    p.out[nb + i] = out_value(p, (int64_t)node * D + i, val);
                                     if (cgdot) dot_acc += (double)__ldg(p.v + nb + i) * (double)val;
                                 }
                             }
@@ -870,7 +885,7 @@ k_node_finish(const AsmParams<T> p, int op_psi, int n_items) {
             for (int i = 0; i < D; ++i) {
                 T val = acc[q * D + i];
                 if (MASKED && __ldg(p.mask + (int64_t)node * D + i)) val = __ldg(p.v + nb + i);
-                p.out[nb + i] = val;
+                p.out[nb + i] = out_value(p, (int64_t)node * D + i, val);
                 if (cgdot) dot_acc += (double)__ldg(p.v + nb + i) * (double)val;
             }
         }
@@ -932,6 +947,14 @@ k_node_finish(const AsmParams<T> p, int op_psi, int n_items) {
         for (int pair = tid; pair < S * p.K; pair += NTB) {
             const int s = pair / p.K, k = pair - s * p.K;
             if (__ldg(p.part_chunk + k) == __ldg(p.part_chunk + k + 1)) p.totals[(int64_t)s * p.K + k] = T(0);
+        }
+    }
+    if (part_totals && p.ep_loss) {   // pretraining loss: batch mean of Pi over (s, k), row order
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int j = 0; j < S * p.K; ++j) t += (double)ld_relaxed(p.totals + j);
+            *p.ep_loss = t / ((double)S * (double)p.K);
         }
     }
     if (cgdot && warp == 0) {

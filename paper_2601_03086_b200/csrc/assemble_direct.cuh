@@ -263,7 +263,7 @@ k_assemble_direct(const AsmParams<T> p) {
                                 T val = accs[i * ST + q];
                                 if (OP == OP_TANGENT && MASKED && __ldg(p.mask + (int64_t)node * D + i))
                                     val = __ldg(p.v + nb + i);
-                                p.out[nb + i] = val;
+                                p.out[nb + i] = out_value(p, (int64_t)node * D + i, val);
                                 if (cgdot) dot_acc += (double)__ldg(p.v + nb + i) * (double)val;
                             }
                         }

@@ -33,6 +33,10 @@ struct Call {
     size_t ws_bytes;
     cudaStream_t stream;
     CgState* cg;
+    // pretraining-loss epilogue (pretrain.cu): out = phi (.) (f_int - f_ext) / (S K), loss
+    int ep;
+    const void* ep_phi;
+    double* ep_loss;
 };
 
 template <class T>
@@ -99,6 +103,10 @@ AsmParams<T> make_params(const Call& c) {
     p.partial = (T*)(w + L.partial);
     p.part_cnt = (int32_t*)(w + L.part_cnt);
     p.cg = c.cg;
+    p.ep = c.ep;
+    p.ep_phi = (const T*)c.ep_phi;
+    p.ep_scale = (T)(1.0 / ((double)c.S * (double)P.n_parts));
+    p.ep_loss = c.ep_loss;
     p.dbg = 0;
     p.lag = 0;
     return p;

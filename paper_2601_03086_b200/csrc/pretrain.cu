@@ -4,20 +4,37 @@
 //   loss = sum_{s,k} Pi_{s,k} / (S K)   batch mean (Eq. 2): samples and parts are the batch
 //   dloss/dH = phi (.) (f_int(u) - f_ext) / (S K)
 // The network itself is out of scope; these are the values its backward consumes.
+#include <type_traits>
+
 #include "launch.cuh"
 
 namespace pfem {
 
 constexpr int PT_NT = 256;
 
-// u[s][n][i] = phi[n][i] * H[s][n][i]
-template <class T>
+// u[s][n][i] = phi[n][i] * H[s][n][i]; VEC: 16-byte vectors (nd and sstride multiples of W)
+template <class T, bool VEC>
 __global__ void __launch_bounds__(PT_NT)
 k_ansatz(int S, int64_t nd, int64_t sstride, const T* __restrict__ H, const T* __restrict__ phi, T* __restrict__ u) {
+    constexpr int W = VEC ? 16 / sizeof(T) : 1;
     const int64_t stride = (int64_t)gridDim.x * PT_NT;
-    for (int64_t i = (int64_t)blockIdx.x * PT_NT + threadIdx.x; i < nd; i += stride) {
-        const T ph = phi[i];
-        for (int s = 0; s < S; ++s) u[(int64_t)s * sstride + i] = ph * H[(int64_t)s * sstride + i];
+    for (int64_t i = ((int64_t)blockIdx.x * PT_NT + threadIdx.x) * W; i < nd; i += stride * W) {
+        if constexpr (VEC) {
+            using V4 = std::conditional_t<sizeof(T) == 4, float4, double2>;
+            const V4 ph = __ldg(reinterpret_cast<const V4*>(phi + i));
+            for (int s = 0; s < S; ++s) {
+                V4 h = __ldcs(reinterpret_cast<const V4*>(H + (int64_t)s * sstride + i));
+                if constexpr (sizeof(T) == 4) {
+                    h.x *= ph.x; h.y *= ph.y; h.z *= ph.z; h.w *= ph.w;
+                } else {
+                    h.x *= ph.x; h.y *= ph.y;
+                }
+                *reinterpret_cast<V4*>(u + (int64_t)s * sstride + i) = h;
+            }
+        } else {
+            const T ph = phi[i];
+            for (int s = 0; s < S; ++s) u[(int64_t)s * sstride + i] = ph * H[(int64_t)s * sstride + i];
+        }
     }
 }
 
@@ -52,7 +69,10 @@ pfem_status pretrain_epilogue_impl(const pfem_mesh* m, int S, int64_t sstride, c
     const int64_t nd = (int64_t)m->n_nodes * m->dim;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(4 * 148, (nd + PT_NT - 1) / PT_NT));
     if (stage == 0) {
-        k_ansatz<T><<<grid, PT_NT, 0, s>>>(S, nd, sstride, (const T*)H, (const T*)phi, (T*)u);
+        constexpr int W = 16 / sizeof(T);
+        const bool vec = nd % W == 0 && sstride % W == 0 && ((uintptr_t)H | (uintptr_t)phi | (uintptr_t)u) % 16 == 0;
+        if (vec) k_ansatz<T, true><<<grid, PT_NT, 0, s>>>(S, nd, sstride, (const T*)H, (const T*)phi, (T*)u);
+        else k_ansatz<T, false><<<grid, PT_NT, 0, s>>>(S, nd, sstride, (const T*)H, (const T*)phi, (T*)u);
         PFEM_LAUNCH_CHECK("k_ansatz");
     } else {
         const Plan* P = reinterpret_cast<const Plan*>(m->plan);

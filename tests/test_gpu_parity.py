@@ -496,11 +496,13 @@ def test_pretrain_loss_matches_oracle(orc, prob, with_phi):
     f = 1e-3 * rng.standard_normal(prob.coords.shape)
     fr, phr = rounded(f, prob.dtype), None if phi is None else rounded(phi, prob.dtype)
     dt = H.dtype
-    loss, tot, grad, u = pf.pretrain_loss(mesh, mat, H, phi=None if phi is None else torch.as_tensor(phr, dtype=dt, device="cuda"),
-                                          f_ext=torch.as_tensor(fr, dtype=dt, device="cuda"))
     lo, Po, go, uo = om.pretrain_loss(rounded(prob.u, prob.dtype), phr, fr)
     tol = TOL[prob.dtype]
-    assert rel_l2(u.cpu().numpy(), uo) < tol
-    assert max_rel(tot.cpu().numpy(), Po) < (1e-10 if prob.dtype == "f64" else 1e-4)
-    assert abs(float(loss) - lo) <= (1e-10 if prob.dtype == "f64" else 1e-4) * abs(lo)
-    assert rel_l2(grad.cpu().numpy(), go) < tol
+    for mode in ("csr", "colour"):   # CSR: epilogue fused into the assembly writes; COLOUR: own pass
+        loss, tot, grad, u = pf.pretrain_loss(mesh, mat, H, mode=mode,
+                                              phi=None if phi is None else torch.as_tensor(phr, dtype=dt, device="cuda"),
+                                              f_ext=torch.as_tensor(fr, dtype=dt, device="cuda"))
+        assert rel_l2(u.cpu().numpy(), uo) < tol
+        assert max_rel(tot.cpu().numpy(), Po) < (1e-10 if prob.dtype == "f64" else 1e-4)
+        assert abs(float(loss) - lo) <= (1e-10 if prob.dtype == "f64" else 1e-4) * abs(lo)
+        assert rel_l2(grad.cpu().numpy(), go) < tol
