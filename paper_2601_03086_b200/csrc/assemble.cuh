@@ -472,7 +472,9 @@ k_assemble(const AsmParams<T> p) {
     constexpr bool HAS_PSI = OP == OP_ENERGY || OP == OP_ENERGY_RESIDUAL;
     constexpr int NV = D + 1;
     constexpr int SD = ST * D;
-    constexpr int NF = 1;    // staged field: u (energy / residual) or v (tangent; the NH state u is gathered)
+    // staged fields (one buffer, refilled for the next block after phase 1): u (energy /
+    // residual), v (linear tangent), v then u (NH tangent: the linearisation state)
+    constexpr int NF = (OP == OP_TANGENT && MODEL == MODEL_NH) ? 2 : 1;
     using V = std::conditional_t<(sizeof(T) == 4 && ST % 2 == 0 && !PFEM_STAGED_SCALAR), F2, T>;
     constexpr int L = VTraits<V>::L;
     // EPOS (fp32): fbuf[(d+1) EB entries][D][ST], each element vertex's forces stored at its
@@ -490,8 +492,9 @@ k_assemble(const AsmParams<T> p) {
     unsigned char* const stage1 = smem_raw + srb;
     T* mstage = reinterpret_cast<T*>(smem_raw + 2 * (size_t)srb);
     T* ustage = mstage + 4 * EB;
-    const size_t ust_sz = (size_t)NF * p.rec.ocap * D * ST;
-    T* fbuf = ustage + 2 * ust_sz;
+    const size_t ust1 = (size_t)p.rec.ocap * D * ST;   // one staged field
+    const size_t ust_sz = (size_t)NF * ust1;
+    T* fbuf = ustage + ust_sz;
     __shared__ __align__(8) uint64_t s_bar[2];
     __shared__ double s_red[NT / 32][2 * ST + 1];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -517,9 +520,11 @@ k_assemble(const AsmParams<T> p) {
         stage_block<D, T, NT>(stage0, mstage, &s_bar[0], p, t);
         if (pref || has_mat) {
             mbar_wait(&s_bar[0], 0);
-            if (pref)
-                stage_fields<D, T, NT, ST, MASKED>(ustage, stage0, p.rec_base, staged_src, p, 0, S,
-                                                   __ldg(p.blk_occ + t + 1) - __ldg(p.blk_occ + t));
+            if (pref) {
+                const int no0 = __ldg(p.blk_occ + t + 1) - __ldg(p.blk_occ + t);
+                stage_fields<D, T, NT, ST, MASKED>(ustage, stage0, p.rec_base, staged_src, p, 0, S, no0);
+                if (NF == 2) stage_fields<D, T, NT, ST, false>(ustage + ust1, stage0, p.rec_base, p.u, p, 0, S, no0);
+            }
             if (has_mat) stage_material<T, NT>(mstage, stage0, p.rec_base, p, t);
         }
         cp_commit();
@@ -553,7 +558,7 @@ k_assemble(const AsmParams<T> p) {
         const int32_t* sseg = reinterpret_cast<const int32_t*>(sg + p.rec.occ_seg);
         const int32_t* seid = reinterpret_cast<const int32_t*>(sg + p.rec.eid);
         const T* smat = mstage + 2 * EB * cur;
-        const T* ust = ustage + ust_sz * cur;
+        const T* ust = ustage;
         mbar_wait(&s_bar[cur], cur ? par1 : par0);   // this block's record
         if (cur) par1 ^= 1u; else par0 ^= 1u;
         cp_wait<1>();                          // this thread's material + field copies of block b
@@ -621,7 +626,8 @@ k_assemble(const AsmParams<T> p) {
                         NhState<D, V> NS;
                         if constexpr (MODEL == MODEL_NH) {
                             V Hu[D][D];
-                            gather<D, T, V, false>(p.u + (int64_t)s * p.sstride, lstride, nullptr, G_, x);
+                            if (pref) load_staged_field<D, T, V, ST>(ust + ust1, lv, qq, x);
+                            else gather<D, T, V, false>(p.u + (int64_t)s * p.sstride, lstride, nullptr, G_, x);
                             grad_of<D, T, V>(G_, x, Hu);
                             nh_state<D, V>(Hu, NS);
                             bad = n_bad(NS.x);
@@ -673,20 +679,25 @@ k_assemble(const AsmParams<T> p) {
                 const T r = warp_multi_sum<T, ST>(wv, lane);
                 if ((lane & (32 / ST - 1)) == 0) s_red[warp][lane / (32 / ST)] = (double)r;
             }
-            // the next block's fields: its record has had phase 1 to land
+            // the next block's fields, into the same buffer once every thread's phase-1 reads
+            // are done (the barrier before phase 2); its record has had phase 1 to land, and
+            // the copies have phase 2 to complete
+            const bool do_p2 = (HAS_FORCE || p.f_ext) && !(p.dbg & 2);
+            if (do_p2 || (pref && s0 + ST >= S)) bar_main(NT);
             if (s0 + ST >= S) {
                 if ((pref || has_mat) && tn < p.n_blocks) {
                     mbar_wait(&s_bar[cur ^ 1], cur ? par0 : par1);
-                    if (pref)
-                        stage_fields<D, T, NT, ST, MASKED>(ustage + ust_sz * (cur ^ 1), sg_nxt, p.rec_base, staged_src, p, 0, S,
-                                                           __ldg(p.blk_occ + tn + 1) - __ldg(p.blk_occ + tn));
+                    if (pref) {
+                        const int non = __ldg(p.blk_occ + tn + 1) - __ldg(p.blk_occ + tn);
+                        stage_fields<D, T, NT, ST, MASKED>(ustage, sg_nxt, p.rec_base, staged_src, p, 0, S, non);
+                        if (NF == 2) stage_fields<D, T, NT, ST, false>(ustage + ust1, sg_nxt, p.rec_base, p.u, p, 0, S, non);
+                    }
                     if (has_mat)
                         stage_material<T, NT>(mstage + 2 * EB * (cur ^ 1), sg_nxt, p.rec_base, p, tn);
                 }
                 cp_commit();
             }
-            if ((HAS_FORCE || p.f_ext) && !(p.dbg & 2)) {
-                bar_main(NT);
+            if (do_p2) {
                 // ---------------- phase 2: block-local CSR gather, HP threads per occurrence
                 // (fp32 ST = 4: two threads, each summing two samples of every entry, so all
                 // warps share the gather and each entry chain is half as long)

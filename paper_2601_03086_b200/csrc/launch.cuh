@@ -150,7 +150,7 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
     constexpr bool HAS_PSI = OP == OP_ENERGY || OP == OP_ENERGY_RESIDUAL;
     constexpr int EB = EbOf<D>::value;
     constexpr int NT = ASM_NT;
-    constexpr int NF = 1;
+    constexpr int NF = (OP == OP_TANGENT && MODEL == MODEL_NH) ? 2 : 1;   // staged fields (single buffer)
     static const int dbg = getenv("PFEM_DEBUG") ? atoi(getenv("PFEM_DEBUG")) : 0;
     static const int variant = getenv("PFEM_VARIANT") ? atoi(getenv("PFEM_VARIANT")) : -1;
     p.dbg = dbg;
@@ -168,12 +168,12 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
         // the staged copy (RecLayout order) skips conn when the fields are staged and the NH
         // state u is not gathered; fp32 (force buffer in entry order) reads ent_pos and not
         // loc_ent, fp64 (loc_ent gather) the reverse
-        const bool need_conn = p.S > ST || (OP == OP_TANGENT && MODEL == MODEL_NH);
+        const bool need_conn = p.S > ST;   // (the NH tangent state is staged with the fields)
         constexpr bool EPOS = sizeof(T) == 4 && PFEM_STAGED_EPOS;
         p.rec_base = need_conn ? p.rec.conn : (EPOS ? p.rec.ent_pos : p.rec.g);
         p.rec_end = EPOS ? p.rec.loc_ent : p.rec.bytes;
         const size_t smem = 2 * (size_t)(p.rec_end - p.rec_base) + 4 * EB * sizeof(T) +
-                            2 * (size_t)NF * p.rec.ocap * D * ST * sizeof(T) +
+                            (size_t)NF * p.rec.ocap * D * ST * sizeof(T) +
                             (HAS_FORCE ? (size_t)ST * D * (D + 1) * EB * sizeof(T) : 0);
         auto kern = k_assemble<D, MODEL, T, OP, ST, MASKED, EB, NT>;
         static int resident = 0;   // per instantiation: co-resident CTAs (persistent grid)
