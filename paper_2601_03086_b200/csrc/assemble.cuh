@@ -34,6 +34,12 @@
 #ifndef PFEM_STAGED_MINB
 #define PFEM_STAGED_MINB 2
 #endif
+#ifndef PFEM_EB3
+#define PFEM_EB3 256          // staged-kernel block capacity for T4 (measurement switch)
+#endif
+#ifndef PFEM_STAGED_NT
+#define PFEM_STAGED_NT 256    // staged-kernel threads per CTA (measurement switch)
+#endif
 #ifndef PFEM_STAGED_EPOS
 #define PFEM_STAGED_EPOS 0
 #endif
@@ -57,7 +63,7 @@ constexpr int CHUNK = 32;     // blocks per reduction chunk (== CHUNK_BLOCKS of 
 
 template <int D>
 struct EbOf {
-    static constexpr int value = D == 3 ? 256 : 512;   // compile-time block capacity
+    static constexpr int value = D == 3 ? PFEM_EB3 : 512;   // compile-time block capacity
 };
 
 struct CgState {

@@ -149,7 +149,7 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
     constexpr bool HAS_FORCE = OP != OP_ENERGY;
     constexpr bool HAS_PSI = OP == OP_ENERGY || OP == OP_ENERGY_RESIDUAL;
     constexpr int EB = EbOf<D>::value;
-    constexpr int NT = ASM_NT;
+    constexpr int NT = PFEM_STAGED_NT;
     constexpr int NF = (OP == OP_TANGENT && MODEL == MODEL_NH) ? 2 : 1;   // staged fields (single buffer)
     static const int dbg = getenv("PFEM_DEBUG") ? atoi(getenv("PFEM_DEBUG")) : 0;
     static const int variant = getenv("PFEM_VARIANT") ? atoi(getenv("PFEM_VARIANT")) : -1;
@@ -159,7 +159,8 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
     // otherwise (several samples per element: arithmetic-heavy, staging amortised).
     // PFEM_VARIANT=0/1 forces staged/direct (measurement switch).
     // Blocks larger than the staged kernel's compile-time capacity always take the direct form.
-    const bool direct = p.eb_max > EB || (variant >= 0 ? variant == 1 : p.S == 1);
+    // (the staged form reads the record with its compile-time stride EB)
+    const bool direct = p.eb_max > EB || p.rec.eb != EB || (variant >= 0 ? variant == 1 : p.S == 1);
     if (direct) {
         const pfem_status st = p.perm ? launch_direct<D, MODEL, T, OP, ST, MASKED, direct_nt<T>(), true>(p, s)
                                       : launch_direct<D, MODEL, T, OP, ST, MASKED, direct_nt<T>(), false>(p, s);
