@@ -40,6 +40,9 @@
 #ifndef PFEM_STAGED_NT
 #define PFEM_STAGED_NT 256    // staged-kernel threads per CTA (measurement switch)
 #endif
+#ifndef PFEM_STAGED_OPERM
+#define PFEM_STAGED_OPERM 1   // phase-2 threads take occurrences in descending entry count
+#endif
 #ifndef PFEM_STAGED_EPOS
 #define PFEM_STAGED_EPOS 0
 #endif
@@ -707,8 +710,9 @@ k_assemble(const AsmParams<T> p) {
                 // ---------------- phase 2: block-local CSR gather, HP threads per occurrence
                 // (fp32 ST = 4: two threads, each summing two samples of every entry, so all
                 // warps share the gather and each entry chain is half as long)
+                const uint16_t* sop = reinterpret_cast<const uint16_t*>(sg + p.rec.occ_perm);
                 for (int w = tid; w < HP * no; w += NT) {
-                    const int oi = HP == 1 ? w : w / HP;
+                    const int oi = PFEM_STAGED_OPERM ? (int)sop[HP == 1 ? w : w / HP] : (HP == 1 ? w : w / HP);
                     const int qs = HP == 1 ? 0 : (w % HP) * STH;   // first sample of this thread
                     const int word = socc[oi];
                     const int node = word & OCC_NODE_MASK;

@@ -47,13 +47,16 @@ constexpr int32_t OCC_EARLIER = 0x20000000;    // owner, and earlier blocks hold
 //   occ_ent [OCAP+1] uint16 (block-relative entry offsets) | lconn [EB][d+1] uint16
 //   (block-local occurrence index of each element vertex) | occ_seg [OCAP] int32 (node-major
 //   segment slot of a multi-block node's occurrence, -1 if the node is finished inside the
-//   block) | loc_ent [(d+1) EB] uint16
+//   block) | occ_perm [OCAP] uint16 (the block's occurrences ordered by descending entry count,
+//   ties by index: the staged kernel's phase-2 thread order, so each warp gathers occurrences
+//   of similar length) | loc_ent [(d+1) EB] uint16
 // The order lets every kernel form read one contiguous range: fp32 forms (force buffer in
 // entry order) [ent_pos, loc_ent), fp64 forms (loc_ent gather) [g, end), and the gathering
 // staged forms start at conn.
 struct RecLayout {
     int eb = 0, ocap = 0;
-    uint32_t conn = 0, g = 0, vol = 0, eid = 0, occ_node = 0, occ_ent = 0, loc_ent = 0, lconn = 0, occ_seg = 0, ent_pos = 0, bytes = 0;
+    uint32_t conn = 0, g = 0, vol = 0, eid = 0, occ_node = 0, occ_ent = 0, loc_ent = 0, lconn = 0, occ_seg = 0, ent_pos = 0,
+             occ_perm = 0, bytes = 0;
 };
 
 inline RecLayout rec_layout(int D, size_t tsize, int eb, int ocap, bool with_eid) {
@@ -71,6 +74,7 @@ inline RecLayout rec_layout(int D, size_t tsize, int eb, int ocap, bool with_eid
     L.occ_ent = take(2 * (size_t)(ocap + 1));
     L.lconn = take(2 * (size_t)(D + 1) * eb);
     L.occ_seg = take(4 * (size_t)ocap);
+    L.occ_perm = take(2 * (size_t)ocap);   // occurrences by descending entry count (phase-2 balance)
     L.loc_ent = take(2 * (size_t)(D + 1) * eb);
     L.bytes = (uint32_t)o;
     return L;

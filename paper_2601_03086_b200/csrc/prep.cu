@@ -499,6 +499,21 @@ __global__ void k_pack_records(int E, const int32_t* __restrict__ blk_elem, cons
         }
         rlc[k] = idx;
     }
+    // phase-2 order: occurrences by descending entry count, ties by index (a permutation)
+    uint16_t* rop = reinterpret_cast<uint16_t*>(r + L.occ_perm);
+    for (int i = threadIdx.x; i < L.ocap; i += blockDim.x) {
+        if (i >= no) {
+            rop[i] = (uint16_t)i;
+            continue;
+        }
+        const int ci = occ_ent_ptr[o0 + i + 1] - occ_ent_ptr[o0 + i];
+        int rank = 0;
+        for (int j = 0; j < no; ++j) {
+            const int cj = occ_ent_ptr[o0 + j + 1] - occ_ent_ptr[o0 + j];
+            rank += (cj > ci || (cj == ci && j < i)) ? 1 : 0;
+        }
+        rop[rank] = (uint16_t)i;
+    }
 }
 
 // ------------------------------------------------------------------ host driver
