@@ -506,3 +506,14 @@ def test_pretrain_loss_matches_oracle(orc, prob, with_phi):
         assert max_rel(tot.cpu().numpy(), Po) < (1e-10 if prob.dtype == "f64" else 1e-4)
         assert abs(float(loss) - lo) <= (1e-10 if prob.dtype == "f64" else 1e-4) * abs(lo)
         assert rel_l2(grad.cpu().numpy(), go) < tol
+
+
+# ------------------------------------------------------------------ large blocks (direct form)
+@pytest.mark.parametrize("prob", SMALL, ids=lambda p: p.name)
+def test_large_blocks_direct_form(orc, prob):
+    """Blocks above the staged kernel's capacity (T4 > 256, T3 > 512 elements) are served by the
+    direct form for every sample count: energy, residual and K.v (masked) still match the oracle."""
+    be = 700 if prob.dim == 3 else 1200
+    check_energy(orc, prob, "csr", block_elems=be)
+    mask = (np.random.default_rng(3).random(prob.n_nodes * prob.dim) < 0.2).astype(np.uint8)
+    check_tangent(orc, prob, "csr", mask=mask, block_elems=be)
