@@ -1,29 +1,28 @@
-// assemble.cuh — the fused element kernels of the hot path (§8 rows a2-a6).
+// assemble.cuh — the fused element kernels of the hot path (§8 rows a2-a6) and their
+// deterministic CSR-mode assembly.
 //
-// CSR mode (the reported path).  The plan (prep.cu) cuts the elements into blocks of at
-// most EB consecutive elements.  A persistent grid (resident CTAs) loops over tickets
-// (atomic counter, so every awaited block is held by a running CTA); the ticket after next
-// is requested and the next block's element arrays (conn, grad N, V, material) are
-// prefetched into shared memory with cp.async while the current block computes.
-// Ticket t:
-//   main (t < n_blocks), block b = t:
-//     phase 1, thread per element: gather u (or v), H, P / dP, psi; the d+1 nodal force
-//       vectors of all ST samples -> shared fbuf[slot][element][dim][sample] (fp32 samples
-//       are processed in FFMA2 pairs and stored as float2); W_e; per-sample energy sums
-//     phase 2, thread per node occurrence of the block: sum the block-local CSR entries
-//       (ascending element, slot) with vector loads of all ST samples at once.
-//       owner nodes without earlier partials: final value; owners with earlier partials:
-//       own segment (fixed up later); nodes owned by a later block: partial.
-//     publish: flag[b] = epoch + 1.
-//   lagged fix-up (t >= L), block c = t - L: for every owned node of c that has partials
-//     in earlier blocks: out = ((p_1 + p_2) + ...) + own, ascending block order.  The lag L
-//     (= resident CTAs) makes the awaited flags (blocks [min_dep(c), c]) almost always
-//     already set, so CTAs do not idle on dependencies.
-// Every sum has a fixed order: no floating-point atomics anywhere (north star); the
-// result is independent of scheduling and bitwise reproducible.
-// Reductions (energies, f.u, CG p.q): per block -> per chunk (<= 32 blocks of one part,
-// reduced by the CTA completing the chunk's 2 arrivals per block) -> per part (the CTA
-// completing the last chunk; it also writes CG alpha and resets the workspace counters).
+// The plan (prep.cu) cuts the elements into blocks of at most EB consecutive plan positions,
+// inside parts, and packs one record per block (RecLayout, common.cuh).
+//
+// Kernel A, staged form (k_assemble, several samples per call): a persistent grid of resident
+// CTAs; CTA i takes blocks i, i+G, ... with no cross-CTA synchronisation.  Per block:
+//   stage    one cp.async.bulk (TMA) copy of the block's record into shared memory, issued one
+//            block ahead and completed on an mbarrier; the block's nodal fields (u, or v and the
+//            NH state u for the tangent) copied into one shared buffer with cp.async
+//   phase 1  thread per element: H, P / dP, psi; the d+1 nodal force vectors of all ST samples
+//            -> fbuf[slot][element][dim][sample] (fp32 samples in FFMA2 pairs); W_e; per-warp
+//            energy sums right after the element loop
+//   phase 2  after one barrier (the next block's fields are then copied into the freed field
+//            buffer): HP threads per node occurrence, occurrences in descending entry count,
+//            sum the block-local CSR entries in ascending (element, slot) order.  A node touched
+//            only by this block gets its final value; otherwise the block writes its segment
+//            seg[slot][s][d] (slots node-major, ascending block)
+// Kernel A, direct form (assemble_direct.cuh, one sample per call): one CTA per block.
+// Kernel B (k_node_finish): thread per multi-block node sums its segments in ascending block
+// order (its CSR row segment by segment, reading R24), applies the mask and the CG p.q; per
+// chunk and per part energy / f.u sums; the last CTA forms CG alpha, the flags and the
+// pretraining loss.  Every floating-point sum has a fixed order: no float atomics anywhere
+// (north star); results are independent of scheduling and bitwise reproducible.
 #pragma once
 
 #include <type_traits>
