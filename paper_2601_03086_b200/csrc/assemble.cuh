@@ -39,6 +39,12 @@
 #ifndef PFEM_STAGED_NT
 #define PFEM_STAGED_NT 256    // staged-kernel threads per CTA (measurement switch)
 #endif
+#ifndef PFEM_MAT_HOIST
+#define PFEM_MAT_HOIST 1      // uniform material: Lame constants hoisted out of the element loop
+#endif
+#ifndef PFEM_P2_UNROLL4
+#define PFEM_P2_UNROLL4 0     // phase-2 gathers four entries at a time (measured slower: off)
+#endif
 #ifndef PFEM_STAGED_OPERM
 #define PFEM_STAGED_OPERM 1   // phase-2 threads take occurrences in descending entry count
 #endif
@@ -519,6 +525,10 @@ k_assemble(const AsmParams<T> p) {
     __syncthreads();
     int n_inv = 0, first_inv = INT32_MAX, n_nonfin = 0;
     const LameScale<T> lsc = lame_scale<T>(p.mat);
+    // uniform material: the Lame constants once per thread (the same arithmetic per element)
+    const bool mat_uniform = PFEM_MAT_HOIST && p.mat.s0 == 0 && p.mat.s1 == 0;
+    T mu_u = T(0), lam_u = T(0);
+    if (mat_uniform) lame_elem<T>(p.mat, lsc, __ldg(p.mat.p0), __ldg(p.mat.p1), mu_u, lam_u);
     const int G = gridDim.x;
     int t = blockIdx.x;
     uint32_t par0 = 0u, par1 = 0u;   // mbarrier phase of each record buffer (registers, no arrays)
@@ -601,7 +611,10 @@ k_assemble(const AsmParams<T> p) {
 #pragma unroll
                     for (int j = 0; j < D; ++j) G_.g[a][j] = sgrad[(a * D + j) * EB + el];
                 G_.V = svol[el];
-                {
+                if (mat_uniform) {
+                    G_.mu = mu_u * G_.V;
+                    G_.lam = lam_u * G_.V;
+                } else {
                     const T m0 = p.mat.s0 ? smat[el] : __ldg(p.mat.p0);
                     const T m1 = p.mat.s1 ? smat[EB + el] : __ldg(p.mat.p1);
                     lame_elem<T>(p.mat, lsc, m0, m1, G_.mu, G_.lam);
@@ -732,6 +745,30 @@ k_assemble(const AsmParams<T> p) {
                             // entries in pairs: both gathers in flight before the adds (the
                             // adds stay in ascending entry order)
                             int k = kb;
+#if PFEM_P2_UNROLL4
+                            for (; k + 3 < k1; k += 4) {   // four entries' gathers in flight
+                                const int j0 = sle[k], j1 = sle[k + 1], j2 = sle[k + 2], j3 = sle[k + 3];
+                                const T* b0 = fbuf + ((size_t)(j0 & 3) * EB + (j0 >> 2)) * SD + qs;
+                                const T* b1 = fbuf + ((size_t)(j1 & 3) * EB + (j1 >> 2)) * SD + qs;
+                                const T* b2 = fbuf + ((size_t)(j2 & 3) * EB + (j2 >> 2)) * SD + qs;
+                                const T* b3 = fbuf + ((size_t)(j3 & 3) * EB + (j3 >> 2)) * SD + qs;
+                                float2 x0[D], x1[D], x2[D], x3[D];
+#pragma unroll
+                                for (int i = 0; i < D; ++i) {
+                                    x0[i] = *reinterpret_cast<const float2*>(b0 + i * ST);
+                                    x1[i] = *reinterpret_cast<const float2*>(b1 + i * ST);
+                                    x2[i] = *reinterpret_cast<const float2*>(b2 + i * ST);
+                                    x3[i] = *reinterpret_cast<const float2*>(b3 + i * ST);
+                                }
+#pragma unroll
+                                for (int i = 0; i < D; ++i) {
+                                    F2 a0(accs[2 * i], accs[2 * i + 1]);
+                                    a0 = (((a0 + F2(x0[i].x, x0[i].y)) + F2(x1[i].x, x1[i].y)) + F2(x2[i].x, x2[i].y)) +
+                                         F2(x3[i].x, x3[i].y);
+                                    accs[2 * i] = a0.v.x; accs[2 * i + 1] = a0.v.y;
+                                }
+                            }
+#endif
                             for (; k + 1 < k1; k += 2) {
                                 const int j0 = sle[k], j1 = sle[k + 1];
                                 const T* b0 = fbuf + ((size_t)(j0 & 3) * EB + (j0 >> 2)) * SD + qs;
