@@ -664,7 +664,10 @@ pfem_status prepare_impl(pfem_mesh* m, cudaStream_t s) {
     }
     // block capacity = the CSR kernel's compile-time EB (assemble.cuh EbOf): 256 T4 / 512 T3
     // (a larger block_elems, up to PLAN_MAX_KEYS / (d+1), is served by the direct kernel form)
-    const int eb_default = D == 3 ? 256 : 512;
+    // defaults: the staged kernel's capacity (T4 256, T3 512); fp64 T4 plans 384 — their calls
+    // are single-sample solves (K.v in CG / Newton) served by the direct form, where larger
+    // blocks mean fewer multi-block nodes (measured on config 4: 131 -> 123 us)
+    const int eb_default = D == 3 ? (m->dtype == PFEM_F64 ? 384 : 256) : 512;
     int eb = m->block_elems > 0 ? m->block_elems : eb_default;
     eb = std::min(eb, PLAN_MAX_KEYS / nv);
     const int eb_cap = std::max(eb, eb_default);
