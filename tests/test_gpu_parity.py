@@ -517,3 +517,52 @@ def test_large_blocks_direct_form(orc, prob):
     check_energy(orc, prob, "csr", block_elems=be)
     mask = (np.random.default_rng(3).random(prob.n_nodes * prob.dim) < 0.2).astype(np.uint8)
     check_tangent(orc, prob, "csr", mask=mask, block_elems=be)
+
+
+# ------------------------------------------------------------------ edge cases
+def test_prepare_errors_and_single_element(orc):
+    """Degenerate element -> PFEM_ERR_DEGENERATE with its index; connectivity out of range ->
+    PFEM_ERR_ARG with the element; a one-element mesh matches the oracle (and the golden
+    single-element values of tests/golden/single_element.json via the oracle pins)."""
+    import paper_2601_03086_b200 as pf
+    from paper_2601_03086_b200 import PfemError
+    dev = "cuda"
+    coords = torch.tensor([[0., 0], [1, 0], [0, 1], [2, 0]], dtype=torch.float64, device=dev)
+    bad = torch.tensor([[0, 1, 2], [0, 1, 3]], dtype=torch.int32, device=dev)      # element 1 collinear
+    with pytest.raises(PfemError) as ei:
+        pf.Mesh(coords, bad)
+    assert ei.value.status == -2 and ei.value.index == 1
+    oob = torch.tensor([[0, 1, 2], [1, 2, 7]], dtype=torch.int32, device=dev)
+    with pytest.raises(PfemError) as ei:
+        pf.Mesh(coords, oob)
+    assert ei.value.status == -1 and ei.value.index == 1
+    # one element, NH fp64, 3 samples (staged) and 1 sample (direct)
+    c1 = np.array([[0., 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]])
+    t1 = np.array([[0, 1, 2, 3]], np.int32)
+    rng = np.random.default_rng(8)
+    for S in (3, 1):
+        u = 0.05 * rng.standard_normal((S, 4, 3))
+        p = Problem("one-tet", 3, c1, t1, "neohookean", "lame", np.array([0.4]), np.array([0.6]), u, "f64")
+        check_energy(orc, p, "csr")
+        check_tangent(orc, p, "csr")
+
+
+def test_cg_edge_cases(orc):
+    """Zero right-hand side with zero prescribed values -> x = 0 after 0 iterations; every DOF
+    constrained -> x = x0 (prescribed) after 0 iterations; max_iter reached ->
+    PFEM_ERR_NOT_CONVERGED (status -4) with the partial iterate and a filled report."""
+    import paper_2601_03086_b200 as pf
+    p = config1()
+    mesh, mat, _ = gpu_problem(p)
+    f = torch.as_tensor(p.f_ext, device="cuda")
+    mask = torch.as_tensor(p.mask, device="cuda")
+    x, rep = pf.cg(mesh, mat, torch.zeros_like(f), torch.zeros_like(f), mask=mask, tol=1e-8)
+    assert rep["iterations"] == 0 and rep["converged"] and torch.count_nonzero(x) == 0
+    allm = torch.ones_like(mask)
+    x0 = torch.as_tensor(np.random.default_rng(1).standard_normal(p.f_ext.shape), device="cuda")
+    x, rep = pf.cg(mesh, mat, f, x0, mask=allm, tol=1e-8)
+    assert rep["iterations"] == 0 and torch.equal(x, x0)
+    x, rep = pf.cg(mesh, mat, f, torch.zeros_like(f), mask=mask, tol=1e-12, max_iter=3)
+    assert rep["status"] == -4 and not rep["converged"] and rep["iterations"] == 3
+    xo, ro = oracle_problem(orc, p).cg(p.f_ext, p.mask, np.zeros_like(p.f_ext), tol=1e-12, max_iter=3)
+    assert rel_l2(x.cpu().numpy(), xo) < 1e-10
