@@ -495,9 +495,33 @@ def cpu_baseline(prob, samples=1):
     om.residual(u)
     om.tangent(v, u=u)
     dt = time.perf_counter() - t0
+    # the same oracle on one thread, on a leading sub-mesh of 200k tets
+    sub = submesh(prob, 200_000)
+    oms = oracle.prepare_problem(sub)
+    oracle.set_threads(1)
+    t0 = time.perf_counter()
+    oms.energy(u)
+    oms.residual(u)
+    oms.tangent(v, u=u)
+    dt1 = time.perf_counter() - t0
+    oracle.set_threads(0)
     return {"value": prob.n_elems * samples / dt, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
             "sample": f"config 3, {samples} of {prob.n_samples} fields, full mesh ({prob.n_elems} tets): "
-                      f"energy + residual + tangent, fp64, {dt:.1f} s"}
+                      f"energy + residual + tangent, fp64, {dt:.1f} s",
+            "single_thread": {"value": sub.n_elems * samples / dt1, "unit": UNIT, "cores": 1,
+                              "sample": f"leading {sub.n_elems} tets of config 3, 1 field, {dt1:.1f} s"},
+            "cpu_model": cpu_model()}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def submesh(prob, n_elems):

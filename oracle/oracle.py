@@ -72,6 +72,11 @@ def _check(st, what):
 I64 = C.c_int64
 
 
+def set_threads(n: int = 0):
+    """OpenMP threads of the oracle (0 = all); results do not depend on it."""
+    lib().oracle_set_threads(C.c_int(n))
+
+
 def lame(kind: str, p0, p1, n: int):
     """(mu, lambda) per element from (E, nu) or (mu, lambda); uniform arrays of length 1 broadcast."""
     p0 = _f64(np.atleast_1d(p0))

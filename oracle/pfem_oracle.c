@@ -789,3 +789,12 @@ int oracle_pcg(int dim, int64_t n_nodes, int64_t n_elems, const int32_t* conn, c
     free(r); free(z); free(p); free(q); free(xd); free(b); free(minv);
     return st;
 }
+
+/* OpenMP threads of the oracle's parallel loops (timing only: every result is independent of
+ * the thread count, since the assembly sums run sequentially) */
+#ifdef _OPENMP
+#include <omp.h>
+void oracle_set_threads(int n) { omp_set_num_threads(n > 0 ? n : omp_get_num_procs()); }
+#else
+void oracle_set_threads(int n) { (void)n; }
+#endif
