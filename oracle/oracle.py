@@ -202,6 +202,24 @@ class Mesh:
         grad = ph[None] * (self.residual(u) - fe[None]) / (S * K)
         return loss, Pi, grad, u
 
+    def heat(self, T, k, f=None):
+        """Steady heat conduction: (W_e [S, E],
+        totals [S, K] = sum W_e - f.T per part, r [S, N] = dW/dT).  k: per element or length 1."""
+        T = _f64(T).reshape(-1, self.n_nodes)
+        S = T.shape[0]
+        K = len(self.part_elem) - 1
+        k = _f64(np.atleast_1d(k))
+        W = np.zeros((S, self.n_elems))
+        tot = np.zeros((S, K))
+        r = np.zeros((S, self.n_nodes))
+        fe = None if f is None else _f64(f).reshape(self.n_nodes)
+        st = lib().oracle_heat(C.c_int(self.dim), I64(self.n_nodes), I64(self.n_elems), _p(self.conn),
+                               _p(self.grad), _p(self.vol), _p(k), I64(0 if len(k) == 1 else 1), C.c_int(S),
+                               _p(T), C.c_int(K), _p(self.part_elem), _p(self.part_node), _p(fe), _p(W),
+                               _p(tot), _p(r))
+        _check(st, "heat")
+        return W, tot, r
+
     def tangent(self, v, u=None, mask=None):
         """K(u) v  [S, N, d]; with mask: (I-M) K (I-M) v + M v."""
         v = _f64(v).reshape(-1, self.n_nodes, self.dim)

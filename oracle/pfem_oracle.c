@@ -798,3 +798,53 @@ void oracle_set_threads(int n) { omp_set_num_threads(n > 0 ? n : omp_get_num_pro
 #else
 void oracle_set_threads(int n) { (void)n; }
 #endif
+
+/* ------------------------------------------------------------------ */
+/* Steady-state heat conduction, the paper's scalar example (Eq.          */
+/* poisson_equation P:186-198 and its energy form P:249-284), on P1 elements:                  */
+/*   grad T_e = sum_{a>=1} (T_a - T_0) grad N_a  (= sum_a T_a grad N_a, grad N_0 = -sum)         */
+/*   W_e = 1/2 k_e V_e |grad T_e|^2                                                              */
+/*   totals[s][k] = sum_{e in part k} W_e - sum_{n in part k} f_n T_n   (f: consistent nodal    */
+/*                  loads of the source and the boundary flux, nullable)                        */
+/*   r_n = sum_{(e,a): v_a(e) = n} k_e V_e grad T_e . grad N_a  (dW/dT_n; the tangent is r(v))  */
+/* assembled sequentially in ascending (e, a) order.                                             */
+/* ------------------------------------------------------------------ */
+int oracle_heat(int dim, int64_t n_nodes, int64_t n_elems, const int32_t* conn, const double* grad,
+                const double* vol, const double* k, int64_t k_stride, int n_samples, const double* T,
+                int n_parts, const int32_t* part_elem, const int32_t* part_node, const double* f,
+                double* W, double* totals, double* r) {
+    const int nv = dim + 1;
+    for (int s = 0; s < n_samples; ++s) {
+        const double* Ts = T + (int64_t)s * n_nodes;
+        double* rs = r ? r + (int64_t)s * n_nodes : NULL;
+        if (rs)
+            for (int64_t n = 0; n < n_nodes; ++n) rs[n] = 0.0;
+        for (int p = 0; p < n_parts; ++p) {
+            double tot = 0.0;
+            for (int64_t e = part_elem[p]; e < part_elem[p + 1]; ++e) {
+                double g[4][3], gT[3] = {0.0, 0.0, 0.0};
+                elem_grads(dim, grad, e, g);
+                const int32_t* c = conn + e * nv;
+                /* difference form (as the kinematics, c1 item 2): a constant field gives 0 exactly */
+                for (int a = 1; a < nv; ++a)
+                    for (int j = 0; j < dim; ++j) gT[j] += (Ts[c[a]] - Ts[c[0]]) * g[a][j];
+                double gg = 0.0;
+                for (int j = 0; j < dim; ++j) gg += gT[j] * gT[j];
+                const double ke = k[e * k_stride];
+                const double w = 0.5 * ke * vol[e] * gg;
+                if (W) W[(int64_t)s * n_elems + e] = w;
+                tot += w;
+                if (rs)
+                    for (int a = 0; a < nv; ++a) {
+                        double dg = 0.0;
+                        for (int j = 0; j < dim; ++j) dg += gT[j] * g[a][j];
+                        rs[c[a]] += ke * vol[e] * dg;
+                    }
+            }
+            if (f)
+                for (int64_t n = part_node[p]; n < part_node[p + 1]; ++n) tot -= f[n] * Ts[n];
+            if (totals) totals[(int64_t)s * n_parts + p] = tot;
+        }
+    }
+    return OR_OK;
+}

@@ -696,3 +696,49 @@ def test_pretrain_loss_gradient_is_finite_difference(orc, model):
     # phi = 1: the gradient is the potential's gradient f_int - f_ext over S K
     _, _, g1, _ = m.pretrain_loss(H, None, f)
     assert rel(g1, (m.residual(H) - f[None]) / 4) < 1e-15
+
+
+# ---------------------------------------------------------------- heat conduction (§8(f) row f4)
+@pytest.mark.parametrize("kind", ["t3", "t4"])
+def test_heat_patch_rigid_and_gradient(orc, kind):
+    """Scalar heat conduction (energy form P:249-284): an affine field T = g.x + c
+    has W = 1/2 k |g|^2 |Omega| (|Omega| = 1) and zero interior residual (patch test); a
+    constant field has W = 0 and r = 0 exactly; r is the central finite difference of W
+    (exact up to rounding: W is quadratic) and T.r(T) = 2W; r is linear and symmetric."""
+    coords, conn = MESHES[kind]()
+    d = coords.shape[1]
+    rng = np.random.default_rng(6)
+    kk = rng.uniform(0.5, 2.0, len(conn))
+    m = orc.prepare(coords, conn, "linear", "lame", [1.0], [1.0])
+    g = rng.standard_normal(d)
+    W, tot, r = m.heat((coords @ g + 0.7)[None], [1.3])
+    assert abs(tot[0, 0] - 0.5 * 1.3 * g @ g) < 1e-13
+    interior = np.all((coords > 1e-9) & (coords < 1 - 1e-9), axis=1)
+    assert np.max(np.abs(r[0, interior])) < 1e-13
+    W0, tot0, r0 = m.heat(np.full((1, len(coords)), 3.25), kk)
+    assert np.all(W0 == 0) and np.all(r0 == 0)
+    T = rng.standard_normal((2, len(coords)))
+    W, tot, r = m.heat(T, kk)
+    h = 1e-6
+    for s, n in [(0, 1), (1, 5), (0, len(coords) - 1)]:
+        Tp, Tm = T.copy(), T.copy()
+        Tp[s, n] += h
+        Tm[s, n] -= h
+        fd = (m.heat(Tp, kk)[1][s, 0] - m.heat(Tm, kk)[1][s, 0]) / (2 * h)
+        assert abs(fd - r[s, n]) < 1e-7 * max(1.0, np.abs(r).max())
+    assert abs(T[0] @ r[0] - 2 * tot[0, 0]) < 1e-12 * abs(tot[0, 0])
+    v, w = rng.standard_normal((2, len(coords)))
+    Kv, Kw = m.heat(v[None], kk)[2][0], m.heat(w[None], kk)[2][0]
+    assert abs(w @ Kv - v @ Kw) < 1e-12 * abs(w @ Kv)
+    # nodal loads enter the totals as - f.T
+    f = rng.standard_normal(len(coords))
+    _, totf, _ = m.heat(T[:1], kk, f=f)
+    assert abs(totf[0, 0] - (tot[0, 0] - f @ T[0])) < 1e-12
+
+
+def test_heat_single_element_closed_form(orc):
+    """Reference T3 with T = (0, 1, 0): grad T = (1, 0), W = 1/2 k V = k / 4; the nodal fluxes
+    are k V grad N_a . (1, 0) = k/2 (-1, 1, 0)."""
+    m = orc.prepare(np.array([[0., 0], [1, 0], [0, 1]]), np.array([[0, 1, 2]]), "linear", "lame", [1.0], [1.0])
+    W, tot, r = m.heat(np.array([[0.0, 1.0, 0.0]]), [2.0])
+    assert abs(W[0, 0] - 0.5) < 1e-16 and np.allclose(r[0], [-1.0, 1.0, 0.0], atol=1e-16, rtol=0)
