@@ -222,6 +222,30 @@ pfem_status pfem_pretrain_loss(const pfem_mesh* m, const pfem_material* mat, int
                                int32_t mode, pfem_flags* flags, void* ws, size_t ws_bytes,
                                void* stream);
 
+/* ---------------------------------------------------------------------------------
+ * Steady heat conduction, the paper's scalar example (energy
+ * form P:249-284), one DOF per node on the prepared mesh (geometry and CSR of
+ * pfem_mesh_prepare):
+ *   grad T_e = sum_a T_a grad N_a,   W_e = 1/2 k_e V_e |grad T_e|^2
+ *   totals[s][k] = sum_{e in part k} W_e - sum_{n in part k} f_n T_n
+ *   flux[s][n]   = sum_{(e,a): v_a(e) = n} k_e V_e grad T_e . grad N_a   (= dW/dT_n; the
+ *                  operator is linear, so flux(v) is also K v)
+ * Arguments:
+ *   k            conductivity per element (k_stride 1) or uniform (k_stride 0), the mesh dtype
+ *   T            [S][N], element stride `sample_stride` between samples
+ *   f_nodal      nullable [N] consistent nodal loads of the source and the boundary flux
+ *   elem_energy  nullable [S][E]; required when totals is given
+ *   totals       nullable [S][n_parts];  flux: nullable [S][N]
+ *   ws, ws_bytes per-call workspace for the totals (pfem_heat_workspace_bytes), may be NULL
+ *                without totals
+ * Sums in fixed order (per part: 64 fixed slices, each a CTA tree, then the slices in order;
+ * per node: CSR order); asynchronous on `stream`.
+ * --------------------------------------------------------------------------------- */
+size_t pfem_heat_workspace_bytes(const pfem_mesh* m, int32_t n_samples);
+pfem_status pfem_heat(const pfem_mesh* m, const void* k, int64_t k_stride, int32_t n_samples,
+                      const void* T, int64_t sample_stride, const void* f_nodal, void* elem_energy,
+                      void* totals, void* flux, void* ws, size_t ws_bytes, void* stream);
+
 /* Internal force only (no energy arithmetic), see pfem_energy. */
 pfem_status pfem_residual(const pfem_mesh* m, const pfem_material* mat, int32_t n_samples,
                           const void* u, int64_t sample_stride, void* residual, int32_t mode,

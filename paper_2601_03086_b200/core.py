@@ -233,6 +233,26 @@ def pretrain_loss(mesh: Mesh, mat: Material, H: torch.Tensor, phi=None, f_ext=No
     return loss, totals, grad, (u if phi is not None else H)
 
 
+def heat(mesh: Mesh, k: torch.Tensor, T: torch.Tensor, f=None, elem_energy=True, totals=True, flux=True):
+    """pfem_heat: steady heat conduction on the prepared mesh.  T: [S, N] (or [N]); k: per element
+    or numel 1.  Returns (W_e [S, E] or None, totals [S, K] or None, flux [S, N] or None)."""
+    _require_cuda(T, k)
+    T = T.reshape(-1, mesh.n_nodes).contiguous()
+    S = T.shape[0]
+    dev = T.device
+    W = torch.empty((S, mesh.n_elems), dtype=mesh.dtype, device=dev) if (elem_energy or totals) else None
+    tot = torch.empty((S, mesh.n_parts), dtype=mesh.dtype, device=dev) if totals else None
+    r = torch.empty_like(T) if flux else None
+    nb = L.load().pfem_heat_workspace_bytes(mesh.ref(), S)
+    ws = mesh._ws.get(("heat", S))
+    if ws is None:
+        ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=dev)
+        mesh._ws[("heat", S)] = ws
+    L.check(L.load().pfem_heat(mesh.ref(), _ptr(k), 0 if k.numel() == 1 else 1, S, _ptr(T), T.shape[1], _ptr(f),
+                               _ptr(W), _ptr(tot), _ptr(r), _ptr(ws), ws.numel(), _stream()))
+    return W, tot, r
+
+
 def residual(mesh: Mesh, mat: Material, u: torch.Tensor, mode: str = "csr", flags=None, out=None):
     """pfem_residual: internal force f_int(u) [S, N, d]."""
     u = _field(mesh, u)

@@ -35,6 +35,9 @@ pfem_status run_cg(const pfem_mesh* m, const pfem_material* mat, const void* u_s
                    pfem_cg_report* rep, void* ws, cudaStream_t s, int precond);
 pfem_status run_tangent_diag(const pfem_mesh* m, const pfem_material* mat, const void* u, const uint8_t* mask,
                              int invert, void* out, cudaStream_t s);
+pfem_status run_heat(const pfem_mesh* m, const void* k, int64_t kstride, int S, const void* Tf, int64_t sstride,
+                     const void* f, void* W, void* totals, void* r, void* ws, cudaStream_t s);
+size_t heat_ws_bytes(const pfem_mesh* m, int S);
 pfem_status run_pretrain_stage(const pfem_mesh* m, int S, int64_t sstride, const void* H, const void* phi, void* u,
                                int stage, const void* f_ext, void* grad, const void* totals, double* loss,
                                cudaStream_t s);
@@ -247,6 +250,30 @@ pfem_status pfem_pretrain_loss(const pfem_mesh* m, const pfem_material* mat, int
     if ((st = run(c))) return st;
     if (fused) return PFEM_OK;
     return run_pretrain_stage(m, n_samples, sample_stride, nullptr, phi, nullptr, 1, f_ext, grad, totals, loss, s);
+}
+
+size_t pfem_heat_workspace_bytes(const pfem_mesh* m, int32_t n_samples) {
+    if (check_mesh(m, false) != PFEM_OK || n_samples <= 0) return 0;
+    return heat_ws_bytes(m, n_samples);
+}
+
+pfem_status pfem_heat(const pfem_mesh* m, const void* k, int64_t k_stride, int32_t n_samples, const void* T,
+                      int64_t sample_stride, const void* f_nodal, void* elem_energy, void* totals, void* flux,
+                      void* ws, size_t ws_bytes, void* stream) {
+    pfem_status st = check_mesh(m, false);
+    if (st) return st;
+    if (!k || !T) { set_error("pfem_heat: k and T are required"); return PFEM_ERR_ARG; }
+    if (k_stride < 0) { set_error("pfem_heat: negative k_stride"); return PFEM_ERR_ARG; }
+    if (n_samples <= 0) { set_error("n_samples must be positive"); return PFEM_ERR_ARG; }
+    if (sample_stride < m->n_nodes && n_samples > 1) { set_error("sample_stride smaller than n_nodes"); return PFEM_ERR_ARG; }
+    if (totals && !elem_energy) { set_error("pfem_heat: totals need elem_energy"); return PFEM_ERR_ARG; }
+    if (totals && (!ws || ws_bytes < heat_ws_bytes(m, n_samples))) {
+        set_error("pfem_heat: workspace too small (pfem_heat_workspace_bytes)");
+        return PFEM_ERR_CAPACITY;
+    }
+    if (flux && (!m->csr_ptr || !m->csr_ent)) { set_error("pfem_heat: mesh CSR missing (prepare first)"); return PFEM_ERR_ARG; }
+    return run_heat(m, k, k_stride, n_samples, T, sample_stride, f_nodal, elem_energy, totals, flux, ws,
+                    (cudaStream_t)stream);
 }
 
 pfem_status pfem_residual(const pfem_mesh* m, const pfem_material* mat, int32_t n_samples, const void* u,

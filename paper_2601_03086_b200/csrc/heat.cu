@@ -1,0 +1,207 @@
+// heat.cu — steady heat conduction, the paper's scalar example (Eq.
+// poisson_equation P:186-198 and its energy form P:249-284), on the same P1 geometry and CSR:
+//   grad T_e = sum_{a>=1} (T_a - T_0) grad N_a
+//   W_e = 1/2 k_e V_e |grad T_e|^2
+//   totals[s][k] = sum_{e in part k} W_e - sum_{n in part k} f_n T_n
+//   r_n = sum_{(e,a): v_a(e) = n} k_e V_e grad T_e . grad N_a    (the tangent is r(v): linear)
+// One DOF per node.  Energies: thread per element; totals: one CTA per (sample, part), fixed
+// order; fluxes: thread per node over its CSR row in ascending (e, a) order, each entry
+// re-forming its element's gradient from the gathered nodal values (the per-element work is a
+// few FMAs, so the recomputation is cheaper than a force buffer).  No float atomics.
+#include "launch.cuh"
+
+namespace pfem {
+
+constexpr int HT_NT = 256;
+
+template <int D, class T>
+__device__ __forceinline__ void heat_grad(const int32_t* __restrict__ conn, const T* __restrict__ grad, int E,
+                                          int e, const T* __restrict__ Ts, T g[D][D], T gT[D]) {
+    constexpr int NV = D + 1;
+    int c[NV];
+#pragma unroll
+    for (int a = 0; a < NV; ++a) c[a] = __ldg(conn + (int64_t)e * NV + a);
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int j = 0; j < D; ++j) g[a][j] = __ldg(grad + (int64_t)(a * D + j) * E + e);
+    const T t0 = __ldg(Ts + c[0]);
+    T dt[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) dt[a] = __ldg(Ts + c[a + 1]) - t0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        T s = dt[0] * g[0][j];
+#pragma unroll
+        for (int a = 1; a < D; ++a) s = fma(dt[a], g[a][j], s);
+        gT[j] = s;
+    }
+}
+
+template <int D, class T>
+__global__ void __launch_bounds__(HT_NT)
+k_heat_elem(int E, int N, int S, int64_t sstride, const int32_t* __restrict__ conn, const T* __restrict__ grad,
+            const T* __restrict__ vol, const T* __restrict__ k, int64_t kstride, const T* __restrict__ Tf,
+            T* __restrict__ W) {
+    for (int e = blockIdx.x * HT_NT + threadIdx.x; e < E; e += gridDim.x * HT_NT) {
+        const T hv = T(0.5) * __ldg(k + (int64_t)e * kstride) * __ldg(vol + e);
+        for (int s = 0; s < S; ++s) {
+            T g[D][D], gT[D];
+            heat_grad<D, T>(conn, grad, E, e, Tf + (int64_t)s * sstride, g, gT);
+            T gg = gT[0] * gT[0];
+#pragma unroll
+            for (int j = 1; j < D; ++j) gg = fma(gT[j], gT[j], gg);
+            W[(int64_t)s * E + e] = hv * gg;
+        }
+    }
+}
+
+constexpr int HT_SLICES = 64;   // fixed slices per (sample, part): a fixed summation order
+
+// stage 1, CTA (slice g, part k, sample s): the part's elements and nodes cut into HT_SLICES
+// equal slices; partial[s][k][g] = sum of the slice's W_e - f.T over the slice's nodes
+template <class T>
+__global__ void __launch_bounds__(HT_NT)
+k_heat_partials(int E, int N, int K, int64_t sstride, const int32_t* __restrict__ part_elem,
+                const int32_t* __restrict__ part_node, const T* __restrict__ W, const T* __restrict__ f,
+                const T* __restrict__ Tf, double* __restrict__ partial) {
+    __shared__ double s_red[HT_NT / 32];
+    const int g = blockIdx.x, kp = blockIdx.y, s = blockIdx.z;
+    const int e0 = part_elem ? part_elem[kp] : 0, e1 = part_elem ? part_elem[kp + 1] : E;
+    const int ce = (e1 - e0 + HT_SLICES - 1) / HT_SLICES;
+    const int a0 = min(e1, e0 + g * ce), a1 = min(e1, a0 + ce);
+    double acc = 0.0;
+    for (int e = a0 + threadIdx.x; e < a1; e += HT_NT) acc += (double)W[(int64_t)s * E + e];
+    if (f) {
+        const int n0 = part_node ? part_node[kp] : 0, n1 = part_node ? part_node[kp + 1] : N;
+        const int cn = (n1 - n0 + HT_SLICES - 1) / HT_SLICES;
+        const int b0 = min(n1, n0 + g * cn), b1 = min(n1, b0 + cn);
+        for (int n = b0 + threadIdx.x; n < b1; n += HT_NT) acc -= (double)f[n] * (double)Tf[(int64_t)s * sstride + n];
+    }
+    const double t = cta_sum<HT_NT>(acc, s_red);
+    if (threadIdx.x == 0) partial[((int64_t)s * K + kp) * HT_SLICES + g] = t;
+}
+
+// stage 2: totals[s][k] = sum of the part's slice partials in slice order
+template <class T>
+__global__ void __launch_bounds__(HT_NT)
+k_heat_totals(int SK, const double* __restrict__ partial, T* __restrict__ totals) {
+    const int i = blockIdx.x * HT_NT + threadIdx.x;
+    if (i >= SK) return;
+    double t = 0.0;
+    for (int g = 0; g < HT_SLICES; ++g) t += partial[(int64_t)i * HT_SLICES + g];
+    totals[i] = (T)t;
+}
+
+// fluxes: thread per node, entries in CSR order; the entry's geometry is loaded once for up to
+// HT_SC samples (each sample's sum still runs over the entries in ascending order)
+constexpr int HT_SC = 4;
+
+template <int D, class T>
+__global__ void __launch_bounds__(HT_NT)
+k_heat_flux(int N, int E, int S, int64_t sstride, const int32_t* __restrict__ csr_ptr, const int32_t* __restrict__ csr_ent,
+            const int32_t* __restrict__ conn, const T* __restrict__ grad, const T* __restrict__ vol,
+            const T* __restrict__ k, int64_t kstride, const T* __restrict__ Tf, T* __restrict__ r) {
+    constexpr int NV = D + 1;
+    for (int n = blockIdx.x * HT_NT + threadIdx.x; n < N; n += gridDim.x * HT_NT) {
+        const int k0 = __ldg(csr_ptr + n), k1 = __ldg(csr_ptr + n + 1);
+        for (int s0 = 0; s0 < S; s0 += HT_SC) {
+            const int nq = min(HT_SC, S - s0);
+            T acc[HT_SC];
+#pragma unroll
+            for (int q = 0; q < HT_SC; ++q) acc[q] = T(0);
+            for (int q = k0; q < k1; ++q) {
+                const int ent = __ldg(csr_ent + q);
+                const int e = ent / NV, a = ent - e * NV;
+                int c[NV];
+#pragma unroll
+                for (int b = 0; b < NV; ++b) c[b] = __ldg(conn + (int64_t)e * NV + b);
+                T g[D][D];
+#pragma unroll
+                for (int b = 0; b < D; ++b)
+#pragma unroll
+                    for (int j = 0; j < D; ++j) g[b][j] = __ldg(grad + (int64_t)(b * D + j) * E + e);
+                T ga[D];   // grad N_a, grad N_0 = -sum (compile-time register indices)
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    T sm = g[0][j];
+#pragma unroll
+                    for (int b = 1; b < D; ++b) sm += g[b][j];
+                    ga[j] = -sm;
+#pragma unroll
+                    for (int b = 0; b < D; ++b)
+                        if (a == b + 1) ga[j] = g[b][j];
+                }
+                const T kv = __ldg(k + (int64_t)e * kstride) * __ldg(vol + e);
+#pragma unroll
+                for (int sq = 0; sq < HT_SC; ++sq) {
+                    if (sq >= nq) break;
+                    const T* Ts = Tf + (int64_t)(s0 + sq) * sstride;
+                    const T t0 = __ldg(Ts + c[0]);
+                    T dt[D];
+#pragma unroll
+                    for (int b = 0; b < D; ++b) dt[b] = __ldg(Ts + c[b + 1]) - t0;
+                    T dg = T(0);
+#pragma unroll
+                    for (int j = 0; j < D; ++j) {
+                        T gTj = dt[0] * g[0][j];
+#pragma unroll
+                        for (int b = 1; b < D; ++b) gTj = fma(dt[b], g[b][j], gTj);
+                        dg = j == 0 ? gTj * ga[0] : fma(gTj, ga[j], dg);
+                    }
+                    acc[sq] = fma(kv, dg, acc[sq]);
+                }
+            }
+#pragma unroll
+            for (int sq = 0; sq < HT_SC; ++sq)
+                if (sq < nq) r[(int64_t)(s0 + sq) * sstride + n] = acc[sq];
+        }
+    }
+}
+
+size_t heat_ws_bytes(const pfem_mesh* m, int S) { return sizeof(double) * (size_t)S * m->n_parts * HT_SLICES; }
+
+template <int D, class T>
+pfem_status heat_impl(const pfem_mesh* m, const void* k, int64_t kstride, int S, const void* Tf, int64_t sstride,
+                      const void* f, void* W, void* totals, void* r, void* ws, cudaStream_t s) {
+    double* partial = (double*)ws;
+    const int E = m->n_elems, N = m->n_nodes;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (W) {
+        const int g = std::max(1, std::min(8 * nsm, (E + HT_NT - 1) / HT_NT));
+        k_heat_elem<D, T><<<g, HT_NT, 0, s>>>(E, N, S, sstride, m->conn, (const T*)m->grad, (const T*)m->vol,
+                                              (const T*)k, kstride, (const T*)Tf, (T*)W);
+        PFEM_LAUNCH_CHECK("k_heat_elem");
+        count_launch();
+    }
+    if (totals) {
+        const int K = m->n_parts;
+        k_heat_partials<T><<<dim3(HT_SLICES, K, S), HT_NT, 0, s>>>(E, N, K, sstride, m->part_elem, m->part_node,
+                                                                    (const T*)W, (const T*)f, (const T*)Tf, partial);
+        PFEM_LAUNCH_CHECK("k_heat_partials");
+        k_heat_totals<T><<<(S * K + HT_NT - 1) / HT_NT, HT_NT, 0, s>>>(S * K, partial, (T*)totals);
+        PFEM_LAUNCH_CHECK("k_heat_totals");
+        count_launch(2);
+    }
+    if (r) {
+        const int g = std::max(1, std::min(8 * nsm, (N + HT_NT - 1) / HT_NT));
+        k_heat_flux<D, T><<<g, HT_NT, 0, s>>>(N, E, S, sstride, m->csr_ptr, m->csr_ent, m->conn, (const T*)m->grad,
+                                              (const T*)m->vol, (const T*)k, kstride, (const T*)Tf, (T*)r);
+        PFEM_LAUNCH_CHECK("k_heat_flux");
+        count_launch();
+    }
+    return PFEM_OK;
+}
+
+pfem_status run_heat(const pfem_mesh* m, const void* k, int64_t kstride, int S, const void* Tf, int64_t sstride,
+                     const void* f, void* W, void* totals, void* r, void* ws, cudaStream_t s) {
+    if (m->dim == 2)
+        return m->dtype == PFEM_F32 ? heat_impl<2, float>(m, k, kstride, S, Tf, sstride, f, W, totals, r, ws, s)
+                                    : heat_impl<2, double>(m, k, kstride, S, Tf, sstride, f, W, totals, r, ws, s);
+    return m->dtype == PFEM_F32 ? heat_impl<3, float>(m, k, kstride, S, Tf, sstride, f, W, totals, r, ws, s)
+                                : heat_impl<3, double>(m, k, kstride, S, Tf, sstride, f, W, totals, r, ws, s);
+}
+
+}  // namespace pfem

@@ -566,3 +566,30 @@ def test_cg_edge_cases(orc):
     assert rep["status"] == -4 and not rep["converged"] and rep["iterations"] == 3
     xo, ro = oracle_problem(orc, p).cg(p.f_ext, p.mask, np.zeros_like(p.f_ext), tol=1e-12, max_iter=3)
     assert rel_l2(x.cpu().numpy(), xo) < 1e-10
+
+
+# ------------------------------------------------------------------ heat conduction (§8(f) row f4)
+@pytest.mark.parametrize("prob", SMALL, ids=lambda p: p.name)
+def test_heat_matches_oracle(orc, prob):
+    """pfem_heat (the paper's scalar example) vs the oracle: W_e, per-part totals with nodal
+    loads, and the CSR-ordered fluxes, on the small problems' meshes (one and two parts, T3 /
+    T4, fp32 / fp64), three temperature fields with per-element conductivity."""
+    import paper_2601_03086_b200 as pf
+    mesh, _, _ = gpu_problem(prob)
+    om = oracle_problem(orc, prob)
+    rng = np.random.default_rng(31)
+    T = rounded(np.sin(3 * prob.coords[:, 0])[None] + 0.1 * rng.standard_normal((3, prob.n_nodes)), prob.dtype)
+    k = rounded(np.exp(0.5 * rng.standard_normal(prob.n_elems)), prob.dtype)
+    f = rounded(0.01 * rng.standard_normal(prob.n_nodes), prob.dtype)
+    dt = {"f32": torch.float32, "f64": torch.float64}[prob.dtype]
+    W, tot, r = pf.heat(mesh, torch.as_tensor(k, dtype=dt, device="cuda"), torch.as_tensor(T, dtype=dt, device="cuda"),
+                        f=torch.as_tensor(f, dtype=dt, device="cuda"))
+    Wo, toto, ro = om.heat(T, k, f=f)
+    tol = TOL[prob.dtype]
+    assert rel_l2(W.cpu().numpy(), Wo) < tol
+    assert max_rel(tot.cpu().numpy(), toto) < (1e-10 if prob.dtype == "f64" else 1e-4)
+    assert rel_l2(r.cpu().numpy(), ro) < tol
+    # uniform conductivity (stride 0)
+    W1, _, r1 = pf.heat(mesh, torch.tensor([1.5], dtype=dt, device="cuda"), torch.as_tensor(T, dtype=dt, device="cuda"))
+    Wo1, _, ro1 = om.heat(T, [1.5])
+    assert rel_l2(r1.cpu().numpy(), ro1) < tol and rel_l2(W1.cpu().numpy(), Wo1) < tol
