@@ -593,6 +593,7 @@ k_assemble(const AsmParams<T> p) {
             for (int q = 0; q < ST; ++q) wacc[q] = T(0);
             for (int el = tid; el < ne; el += NT) {
                 const int e = p.perm ? seid[el] : e0 + el;   // input element id (W_e, flags)
+                T* const wrow = (HAS_PSI && p.W_e) ? p.W_e + (int64_t)s0 * p.E + e : nullptr;   // W_e[s0][e]
                 Geo<D, T> G_;
                 if (has_conn) {   // node ids: only the global gathers use them
                     if constexpr (D == 3) {
@@ -668,13 +669,18 @@ k_assemble(const AsmParams<T> p) {
                         first_inv = min(first_inv, e);
                     }
                     if (HAS_PSI) {
+                        // non-finite check once per pair: w - w is 0 for finite w, NaN otherwise
+                        if constexpr (L == 2) {
+                            const V z = psi - psi;
+                            if (!(z.v.x + z.v.y == 0.0f)) n_nonfin += (!isfinite(psi.v.x)) + (qq + 1 < nq && !isfinite(psi.v.y));
+                        }
 #pragma unroll
                         for (int k = 0; k < L; ++k) {
                             if (qq + k >= nq) break;
                             const T w = pfem::lane(psi, k);
-                            if (!isfinite(w)) ++n_nonfin;
+                            if (L == 1 && !isfinite(w)) ++n_nonfin;
                             wacc[qq + k] += w;
-                            if (p.W_e) p.W_e[(int64_t)(s + k) * p.E + e] = w;
+                            if (wrow) wrow[(int64_t)(qq + k) * p.E] = w;
                         }
                     }
                     if (HAS_FORCE) {
@@ -689,14 +695,16 @@ k_assemble(const AsmParams<T> p) {
                     }
                 }
             }
+            if (S > ST) {
 #pragma unroll
-            for (int q = 0; q < ST; ++q) wsum[q] += (double)wacc[q];   // per-thread, fixed order
+                for (int q = 0; q < ST; ++q) wsum[q] += (double)wacc[q];   // per-thread, fixed order
+            }
             if (HAS_PSI && S <= ST && !(p.dbg & 8)) {
                 // per-warp energy sums now, while other warps finish phase 1 (s_red is free:
                 // the previous block's warp 0 read it before this block's first barrier)
                 T wv[ST];
 #pragma unroll
-                for (int q = 0; q < ST; ++q) wv[q] = q < S ? (T)wsum[q] : T(0);
+                for (int q = 0; q < ST; ++q) wv[q] = q < S ? wacc[q] : T(0);
                 const T r = warp_multi_sum<T, ST>(wv, lane);
                 if ((lane & (32 / ST - 1)) == 0) s_red[warp][lane / (32 / ST)] = (double)r;
             }
@@ -736,11 +744,7 @@ k_assemble(const AsmParams<T> p) {
                         if constexpr (EPOS) {
                             for (int k = kb; k < k1; ++k) sacc<T, SD>(fbuf + (size_t)k * SD, accs);
                         } else if constexpr (HP == 1) {
-                            for (int k = kb; k < k1; ++k) {
-                                const int j = sle[k];
-                                const int el = j / NV, a = j - el * NV;
-                                sacc<T, SDH>(fbuf + ((size_t)a * EB + el) * SD, accs);
-                            }
+                            for (int k = kb; k < k1; ++k) sacc<T, SDH>(fbuf + (size_t)sle[k] * SD, accs);
                         } else {
                             // entries in pairs: both gathers in flight before the adds (the
                             // adds stay in ascending entry order)
@@ -748,10 +752,10 @@ k_assemble(const AsmParams<T> p) {
 #if PFEM_P2_UNROLL4
                             for (; k + 3 < k1; k += 4) {   // four entries' gathers in flight
                                 const int j0 = sle[k], j1 = sle[k + 1], j2 = sle[k + 2], j3 = sle[k + 3];
-                                const T* b0 = fbuf + ((size_t)(j0 & 3) * EB + (j0 >> 2)) * SD + qs;
-                                const T* b1 = fbuf + ((size_t)(j1 & 3) * EB + (j1 >> 2)) * SD + qs;
-                                const T* b2 = fbuf + ((size_t)(j2 & 3) * EB + (j2 >> 2)) * SD + qs;
-                                const T* b3 = fbuf + ((size_t)(j3 & 3) * EB + (j3 >> 2)) * SD + qs;
+                                const T* b0 = fbuf + (size_t)j0 * SD + qs;
+                                const T* b1 = fbuf + (size_t)j1 * SD + qs;
+                                const T* b2 = fbuf + (size_t)j2 * SD + qs;
+                                const T* b3 = fbuf + (size_t)j3 * SD + qs;
                                 float2 x0[D], x1[D], x2[D], x3[D];
 #pragma unroll
                                 for (int i = 0; i < D; ++i) {
@@ -771,8 +775,8 @@ k_assemble(const AsmParams<T> p) {
 #endif
                             for (; k + 1 < k1; k += 2) {
                                 const int j0 = sle[k], j1 = sle[k + 1];
-                                const T* b0 = fbuf + ((size_t)(j0 & 3) * EB + (j0 >> 2)) * SD + qs;
-                                const T* b1 = fbuf + ((size_t)(j1 & 3) * EB + (j1 >> 2)) * SD + qs;
+                                const T* b0 = fbuf + (size_t)j0 * SD + qs;   // (record loc_ent = slot)
+                                const T* b1 = fbuf + (size_t)j1 * SD + qs;
                                 float2 x0[D], x1[D];
 #pragma unroll
                                 for (int i = 0; i < D; ++i) {
@@ -788,7 +792,7 @@ k_assemble(const AsmParams<T> p) {
                             }
                             if (k < k1) {
                                 const int j0 = sle[k];
-                                const T* b0 = fbuf + ((size_t)(j0 & 3) * EB + (j0 >> 2)) * SD + qs;
+                                const T* b0 = fbuf + (size_t)j0 * SD + qs;
 #pragma unroll
                                 for (int i = 0; i < D; ++i) {
                                     const float2 x0 = *reinterpret_cast<const float2*>(b0 + i * ST);

@@ -236,12 +236,7 @@ k_assemble_direct(const AsmParams<T> p) {
                     for (int k = 0; k < SD; ++k) accs[k] = T(0);
                     const int k1 = first ? k1_0 : __ldg(soe + oi + 1);
                     for (int k = first ? kb_0 : __ldg(soe + oi); k < k1; ++k) {
-                        int slot = k;
-                        if (!EPOS) {
-                            const int j = le[k];
-                            const int el = j / NV, a = j - el * NV;
-                            slot = a * EB + el;
-                        }
+                        const int slot = EPOS ? k : (int)le[k];   // (record loc_ent = force-buffer slot)
                         sacc<T, SD>(fbuf + (size_t)slot * SD, accs);
                     }
                     if (word & (OCC_NONOWNER | OCC_EARLIER)) {

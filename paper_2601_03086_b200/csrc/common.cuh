@@ -49,7 +49,8 @@ constexpr int32_t OCC_EARLIER = 0x20000000;    // owner, and earlier blocks hold
 //   segment slot of a multi-block node's occurrence, -1 if the node is finished inside the
 //   block) | occ_perm [OCAP] uint16 (the block's occurrences ordered by descending entry count,
 //   ties by index: the staged kernel's phase-2 thread order, so each warp gathers occurrences
-//   of similar length) | loc_ent [(d+1) EB] uint16
+//   of similar length) | loc_ent [(d+1) EB] uint16 (each block-CSR entry's force-buffer slot
+//   a * EB + el)
 // The order lets every kernel form read one contiguous range: fp32 forms (force buffer in
 // entry order) [ent_pos, loc_ent), fp64 forms (loc_ent gather) [g, end), and the gathering
 // staged forms start at conn.

@@ -479,7 +479,14 @@ __global__ void k_pack_records(int E, const int32_t* __restrict__ blk_elem, cons
         roe[i] = (uint16_t)(i <= no ? occ_ent_ptr[o0 + i] - NV * e0 : NV * ne);
     uint16_t* rep = reinterpret_cast<uint16_t*>(r + L.ent_pos);
     for (int k = threadIdx.x; k < NV * L.eb; k += blockDim.x) {
-        rle[k] = k < NV * ne ? loc_ent[(int64_t)NV * e0 + k] : (uint16_t)0;
+        // the record keeps each entry's force-buffer slot a * EB + el (element-major buffer)
+        // rather than the plan's el * (d+1) + a, so phase 2 needs no division
+        if (k < NV * ne) {
+            const int j = loc_ent[(int64_t)NV * e0 + k];
+            rle[k] = (uint16_t)((j % NV) * L.eb + j / NV);
+        } else {
+            rle[k] = 0;
+        }
         if (k < NV * ne) rep[loc_ent[(int64_t)NV * e0 + k]] = (uint16_t)k;   // a permutation of [0, NV ne)
         else rep[k] = (uint16_t)k;
     }
