@@ -52,6 +52,16 @@ __device__ __forceinline__ void prefetch_record(const AsmParams<T>& p, int b) {
     if (p.mat.s1) l2_prefetch(p.mat.p1, E * sizeof(T), e0 * sizeof(T), ne * sizeof(T));
 }
 
+#ifndef PFEM_DIRECT_TMA
+#define PFEM_DIRECT_TMA 0   // fp32: the block's record copied to shared memory by one bulk copy (measurement switch)
+#endif
+// record read: shared-memory copy (plain load) or global (read-only path)
+template <bool SM, class X>
+__device__ __forceinline__ X rld(const X* q) {
+    if constexpr (SM) return *q;
+    else return __ldg(q);
+}
+
 #ifndef PFEM_DIRECT_SCALAR
 #define PFEM_DIRECT_SCALAR 0
 #endif
@@ -83,21 +93,39 @@ k_assemble_direct(const AsmParams<T> p) {
     const int S = p.S;
     const int EB = p.rec.eb;                                    // record / fbuf stride
     const size_t ust_sz = (size_t)p.rec.ocap * D * ST;
-    T* ust = reinterpret_cast<T*>(smem_raw);
+    constexpr bool TMA = PFEM_DIRECT_TMA && sizeof(T) == 4;
+    // TMA: smem_raw = [record bytes ent_pos .. loc_ent) | ust | fbuf
+    const uint32_t rb0 = p.rec.ent_pos, rbn = TMA ? ((p.rec.loc_ent - p.rec.ent_pos + 15u) & ~15u) : 0u;
+    T* ust = reinterpret_cast<T*>(smem_raw + rbn);
     constexpr bool EPOS = sizeof(T) == 4;
     uint16_t* le = reinterpret_cast<uint16_t*>(ust + NF * ust_sz);
-    T* fbuf = reinterpret_cast<T*>(smem_raw + ((NF * ust_sz * sizeof(T) + (EPOS ? 0 : 2 * (size_t)NV * EB) + 15) &
-                                               ~size_t(15)));
+    T* fbuf = reinterpret_cast<T*>(smem_raw + rbn + ((NF * ust_sz * sizeof(T) + (EPOS ? 0 : 2 * (size_t)NV * EB) + 15) &
+                                                     ~size_t(15)));
     const bool cgdot = OP == OP_TANGENT && p.cg != nullptr;
     if (p.cg && ld_relaxed_i(&p.cg->done)) return;
     const int b = blockIdx.x;
     if (p.lag > 0 && tid == 0 && b + p.lag < p.n_blocks) prefetch_record<T>(p, b + p.lag);
     const unsigned char* rg = p.recs + (size_t)b * p.rec.bytes;
+    __shared__ __align__(8) uint64_t s_rbar;
+    if constexpr (TMA) {
+        if (tid == 0) {
+            mbar_init(&s_rbar, 1);
+            mbar_fence_init();
+            mbar_expect_tx(&s_rbar, p.rec.loc_ent - rb0);
+            tma_bulk_g2s(smem_raw, rg + rb0, p.rec.loc_ent - rb0, &s_rbar);
+        }
+    }
+    // record bytes: from the shared copy (TMA) or from global memory
+    const unsigned char* rgb = TMA ? (const unsigned char*)smem_raw - rb0 : rg;
     const int e0 = __ldg(p.blk_elem + b), ne = __ldg(p.blk_elem + b + 1) - e0;
     const int no = __ldg(p.blk_occ + b + 1) - __ldg(p.blk_occ + b);
-    const int32_t* socc = reinterpret_cast<const int32_t*>(rg + p.rec.occ_node);
-    const uint16_t* soe = reinterpret_cast<const uint16_t*>(rg + p.rec.occ_ent);
-    const int32_t* sseg = reinterpret_cast<const int32_t*>(rg + p.rec.occ_seg);
+    if constexpr (TMA) {
+        __syncthreads();            // the mbarrier is initialised
+        mbar_wait(&s_rbar, 0);      // the record has landed
+    }
+    const int32_t* socc = reinterpret_cast<const int32_t*>(rgb + p.rec.occ_node);
+    const uint16_t* soe = reinterpret_cast<const uint16_t*>(rgb + p.rec.occ_ent);
+    const int32_t* sseg = reinterpret_cast<const int32_t*>(rgb + p.rec.occ_seg);
     if (!EPOS && HAS_FORCE) {   // block-local CSR entries -> shared (async, lands by the first barrier)
         const int nchunk = (2 * NV * ne + 15) / 16;
         for (int c = tid; c < nchunk; c += NT) cpn<16>(le + 8 * c, rg + p.rec.loc_ent + 16 * c);
@@ -105,10 +133,10 @@ k_assemble_direct(const AsmParams<T> p) {
     // this thread's first occurrence: phase-2 metadata loaded now, in flight during phase 1
     int w_0 = 0, kb_0 = 0, k1_0 = 0, sl_0 = -1;
     if ((HAS_FORCE || p.f_ext) && tid < no) {
-        w_0 = __ldg(socc + tid);
-        kb_0 = __ldg(soe + tid);
-        k1_0 = __ldg(soe + tid + 1);
-        sl_0 = __ldg(sseg + tid);
+        w_0 = rld<TMA>(socc + tid);
+        kb_0 = rld<TMA>(soe + tid);
+        k1_0 = rld<TMA>(soe + tid + 1);
+        sl_0 = rld<TMA>(sseg + tid);
     }
     int n_inv = 0, first_inv = INT32_MAX, n_nonfin = 0;
     double dot_acc = 0.0;
@@ -123,10 +151,10 @@ k_assemble_direct(const AsmParams<T> p) {
     for (int s0 = 0; s0 < S; s0 += ST) {
         const int nq = min(ST, S - s0);
         if (OP == OP_TANGENT) {
-            stage_fields<D, T, NT, ST, MASKED>(ust, rg, 0u, p.v, p, s0, nq, no);
-            if (NF == 2) stage_fields<D, T, NT, ST, false>(ust + ust_sz, rg, 0u, p.u, p, s0, nq, no);
+            stage_fields<D, T, NT, ST, MASKED>(ust, rgb, 0u, p.v, p, s0, nq, no);
+            if (NF == 2) stage_fields<D, T, NT, ST, false>(ust + ust_sz, rgb, 0u, p.u, p, s0, nq, no);
         } else {
-            stage_fields<D, T, NT, ST, false>(ust, rg, 0u, p.u, p, s0, nq, no);
+            stage_fields<D, T, NT, ST, false>(ust, rgb, 0u, p.u, p, s0, nq, no);
         }
         cp_commit();
         T wacc[ST];
@@ -140,32 +168,32 @@ k_assemble_direct(const AsmParams<T> p) {
         for (int el = tid; el < ne; el += NT) {
             // input element id (W_e, material, flags): identity order needs no load, and the
             // material load then does not wait on the id
-            const int e = PERM ? __ldg(reinterpret_cast<const int32_t*>(rg + p.rec.eid) + el) : e0 + el;
+            const int e = PERM ? rld<TMA>(reinterpret_cast<const int32_t*>(rgb + p.rec.eid) + el) : e0 + el;
             Geo<D, T> G;
             int lv[NV], ep[NV];   // vertex -> staged occurrence, vertex -> block-CSR entry
             if constexpr (D == 3) {
-                const uint2 c = __ldg(reinterpret_cast<const uint2*>(rg + p.rec.lconn) + el);
+                const uint2 c = rld<TMA>(reinterpret_cast<const uint2*>(rgb + p.rec.lconn) + el);
                 lv[0] = c.x & 0xffff; lv[1] = c.x >> 16; lv[2] = c.y & 0xffff; lv[3] = c.y >> 16;
                 if (EPOS) {
-                    const uint2 q = __ldg(reinterpret_cast<const uint2*>(rg + p.rec.ent_pos) + el);
+                    const uint2 q = rld<TMA>(reinterpret_cast<const uint2*>(rgb + p.rec.ent_pos) + el);
                     ep[0] = q.x & 0xffff; ep[1] = q.x >> 16; ep[2] = q.y & 0xffff; ep[3] = q.y >> 16;
                 }
             } else {
-                const uint16_t* lc = reinterpret_cast<const uint16_t*>(rg + p.rec.lconn) + el * NV;
-                const uint16_t* lp = reinterpret_cast<const uint16_t*>(rg + p.rec.ent_pos) + el * NV;
+                const uint16_t* lc = reinterpret_cast<const uint16_t*>(rgb + p.rec.lconn) + el * NV;
+                const uint16_t* lp = reinterpret_cast<const uint16_t*>(rgb + p.rec.ent_pos) + el * NV;
 #pragma unroll
                 for (int a = 0; a < NV; ++a) {
-                    lv[a] = __ldg(lc + a);
-                    if (EPOS) ep[a] = __ldg(lp + a);
+                    lv[a] = rld<TMA>(lc + a);
+                    if (EPOS) ep[a] = rld<TMA>(lp + a);
                 }
             }
             {
-                const T* sg = reinterpret_cast<const T*>(rg + p.rec.g);
+                const T* sg = reinterpret_cast<const T*>(rgb + p.rec.g);
 #pragma unroll
                 for (int a = 0; a < D; ++a)
 #pragma unroll
-                    for (int j = 0; j < D; ++j) G.g[a][j] = __ldg(sg + (a * D + j) * EB + el);
-                G.V = __ldg(reinterpret_cast<const T*>(rg + p.rec.vol) + el);
+                    for (int j = 0; j < D; ++j) G.g[a][j] = rld<TMA>(sg + (a * D + j) * EB + el);
+                G.V = rld<TMA>(reinterpret_cast<const T*>(rgb + p.rec.vol) + el);
                 const T m0 = __ldg(p.mat.p0 + (int64_t)e * p.mat.s0);
                 const T m1 = __ldg(p.mat.p1 + (int64_t)e * p.mat.s1);
                 lame_elem<T>(p.mat, lsc, m0, m1, G.mu, G.lam);
@@ -228,19 +256,19 @@ k_assemble_direct(const AsmParams<T> p) {
             // ---------------- phase 2: block-local CSR gather, thread per occurrence
             for (int oi = tid; oi < no; oi += NT) {
                 const bool first = oi == tid;
-                const int word = first ? w_0 : __ldg(socc + oi);
+                const int word = first ? w_0 : rld<TMA>(socc + oi);
                 const int node = word & OCC_NODE_MASK;
                 if (HAS_FORCE) {
                     T accs[SD];
 #pragma unroll
                     for (int k = 0; k < SD; ++k) accs[k] = T(0);
-                    const int k1 = first ? k1_0 : __ldg(soe + oi + 1);
-                    for (int k = first ? kb_0 : __ldg(soe + oi); k < k1; ++k) {
+                    const int k1 = first ? k1_0 : rld<TMA>(soe + oi + 1);
+                    for (int k = first ? kb_0 : rld<TMA>(soe + oi); k < k1; ++k) {
                         const int slot = EPOS ? k : (int)le[k];   // (record loc_ent = force-buffer slot)
                         sacc<T, SD>(fbuf + (size_t)slot * SD, accs);
                     }
                     if (word & (OCC_NONOWNER | OCC_EARLIER)) {
-                        const int slot = first ? sl_0 : __ldg(sseg + oi);
+                        const int slot = first ? sl_0 : rld<TMA>(sseg + oi);
 #pragma unroll
                         for (int q = 0; q < ST; ++q) {
                             if (q >= nq) break;

@@ -122,8 +122,9 @@ template <int D, int MODEL, class T, int OP, int ST, bool MASKED, int NT, bool P
 pfem_status launch_direct(AsmParams<T> p, cudaStream_t s) {
     constexpr bool HAS_FORCE = OP != OP_ENERGY;
     constexpr int NFd = (OP == OP_TANGENT && MODEL == MODEL_NH) ? 2 : 1;
-    const size_t smem = ((NFd * (size_t)p.rec.ocap * D * ST * sizeof(T) + (sizeof(T) == 4 ? 0 : 2 * (size_t)(D + 1) * p.rec.eb) +
-                          15) & ~size_t(15)) +
+    const size_t rbn = (PFEM_DIRECT_TMA && sizeof(T) == 4) ? ((p.rec.loc_ent - p.rec.ent_pos + 15u) & ~15u) : 0;
+    const size_t smem = rbn + ((NFd * (size_t)p.rec.ocap * D * ST * sizeof(T) + (sizeof(T) == 4 ? 0 : 2 * (size_t)(D + 1) * p.rec.eb) +
+                                15) & ~size_t(15)) +
                         (HAS_FORCE ? (size_t)ST * D * (D + 1) * p.rec.eb * sizeof(T) : 0);
     auto kd = k_assemble_direct<D, MODEL, T, OP, ST, MASKED, NT, PERM>;
     static size_t configured = 0;
