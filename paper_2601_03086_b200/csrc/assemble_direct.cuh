@@ -52,6 +52,9 @@ __device__ __forceinline__ void prefetch_record(const AsmParams<T>& p, int b) {
     if (p.mat.s1) l2_prefetch(p.mat.p1, E * sizeof(T), e0 * sizeof(T), ne * sizeof(T));
 }
 
+#ifndef PFEM_DIRECT_SMAT
+#define PFEM_DIRECT_SMAT 0   // element-wise materials copied into shared memory with the fields (measured slower: off)
+#endif
 #ifndef PFEM_DIRECT_TMA
 #define PFEM_DIRECT_TMA 0   // fp32: the block's record copied to shared memory by one bulk copy (measurement switch)
 #endif
@@ -101,6 +104,9 @@ k_assemble_direct(const AsmParams<T> p) {
     uint16_t* le = reinterpret_cast<uint16_t*>(ust + NF * ust_sz);
     T* fbuf = reinterpret_cast<T*>(smem_raw + rbn + ((NF * ust_sz * sizeof(T) + (EPOS ? 0 : 2 * (size_t)NV * EB) + 15) &
                                                      ~size_t(15)));
+    // element-wise materials [2][EB] after the force buffer
+    T* smat = fbuf + (HAS_FORCE ? (size_t)ST * D * NV * EB : 0);
+    const bool has_mat = (p.mat.s0 | p.mat.s1) != 0;
     const bool cgdot = OP == OP_TANGENT && p.cg != nullptr;
     if (p.cg && ld_relaxed_i(&p.cg->done)) return;
     const int b = blockIdx.x;
@@ -156,6 +162,15 @@ k_assemble_direct(const AsmParams<T> p) {
         } else {
             stage_fields<D, T, NT, ST, false>(ust, rgb, 0u, p.u, p, s0, nq, no);
         }
+        // element-wise materials of the block, copied into shared memory with the fields (one
+        // overlapped latency instead of one dependent gather per element and thread)
+        if (PFEM_DIRECT_SMAT && has_mat && s0 == 0) {
+            for (int el = tid; el < ne; el += NT) {
+                const int64_t e = PERM ? (int64_t)rld<TMA>(reinterpret_cast<const int32_t*>(rgb + p.rec.eid) + el) : e0 + el;
+                if (p.mat.s0) cpn<sizeof(T)>(smat + el, p.mat.p0 + e * p.mat.s0);
+                if (p.mat.s1) cpn<sizeof(T)>(smat + EB + el, p.mat.p1 + e * p.mat.s1);
+            }
+        }
         cp_commit();
         T wacc[ST];
 #pragma unroll
@@ -194,8 +209,8 @@ k_assemble_direct(const AsmParams<T> p) {
 #pragma unroll
                     for (int j = 0; j < D; ++j) G.g[a][j] = rld<TMA>(sg + (a * D + j) * EB + el);
                 G.V = rld<TMA>(reinterpret_cast<const T*>(rgb + p.rec.vol) + el);
-                const T m0 = __ldg(p.mat.p0 + (int64_t)e * p.mat.s0);
-                const T m1 = __ldg(p.mat.p1 + (int64_t)e * p.mat.s1);
+                const T m0 = (PFEM_DIRECT_SMAT && p.mat.s0) ? smat[el] : __ldg(p.mat.p0 + (int64_t)e * p.mat.s0);
+                const T m1 = (PFEM_DIRECT_SMAT && p.mat.s1) ? smat[EB + el] : __ldg(p.mat.p1 + (int64_t)e * p.mat.s1);
                 lame_elem<T>(p.mat, lsc, m0, m1, G.mu, G.lam);
                 G.mu *= G.V;
                 G.lam *= G.V;

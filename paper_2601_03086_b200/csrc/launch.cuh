@@ -125,7 +125,8 @@ pfem_status launch_direct(AsmParams<T> p, cudaStream_t s) {
     const size_t rbn = (PFEM_DIRECT_TMA && sizeof(T) == 4) ? ((p.rec.loc_ent - p.rec.ent_pos + 15u) & ~15u) : 0;
     const size_t smem = rbn + ((NFd * (size_t)p.rec.ocap * D * ST * sizeof(T) + (sizeof(T) == 4 ? 0 : 2 * (size_t)(D + 1) * p.rec.eb) +
                                 15) & ~size_t(15)) +
-                        (HAS_FORCE ? (size_t)ST * D * (D + 1) * p.rec.eb * sizeof(T) : 0);
+                        (HAS_FORCE ? (size_t)ST * D * (D + 1) * p.rec.eb * sizeof(T) : 0) +
+                        ((PFEM_DIRECT_SMAT && (p.mat.s0 | p.mat.s1)) ? 2 * (size_t)p.rec.eb * sizeof(T) : 0);
     auto kd = k_assemble_direct<D, MODEL, T, OP, ST, MASKED, NT, PERM>;
     static size_t configured = 0;
     static int pf_auto = 0;
