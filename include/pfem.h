@@ -236,8 +236,9 @@ pfem_status pfem_pretrain_loss(const pfem_mesh* m, const pfem_material* mat, int
  *   f_nodal      nullable [N] consistent nodal loads of the source and the boundary flux
  *   elem_energy  nullable [S][E]; required when totals is given
  *   totals       nullable [S][n_parts];  flux: nullable [S][N]
- *   ws, ws_bytes per-call workspace for the totals (pfem_heat_workspace_bytes), may be NULL
- *                without totals
+ *   ws, ws_bytes per-call workspace (pfem_heat_workspace_bytes): the totals' slice sums and
+ *                the fluxes' CSR-ordered entry buffer; may be NULL without totals (the fluxes
+ *                then re-form each element per CSR entry, same summation order)
  * Sums in fixed order (per part: 64 fixed slices, each a CTA tree, then the slices in order;
  * per node: CSR order); asynchronous on `stream`.
  * --------------------------------------------------------------------------------- */

@@ -267,7 +267,7 @@ pfem_status pfem_heat(const pfem_mesh* m, const void* k, int64_t k_stride, int32
     if (n_samples <= 0) { set_error("n_samples must be positive"); return PFEM_ERR_ARG; }
     if (sample_stride < m->n_nodes && n_samples > 1) { set_error("sample_stride smaller than n_nodes"); return PFEM_ERR_ARG; }
     if (totals && !elem_energy) { set_error("pfem_heat: totals need elem_energy"); return PFEM_ERR_ARG; }
-    if (totals && (!ws || ws_bytes < heat_ws_bytes(m, n_samples))) {
+    if ((totals && !ws) || (ws && ws_bytes < heat_ws_bytes(m, n_samples))) {
         set_error("pfem_heat: workspace too small (pfem_heat_workspace_bytes)");
         return PFEM_ERR_CAPACITY;
     }

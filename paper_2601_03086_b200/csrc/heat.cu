@@ -13,6 +13,9 @@
 namespace pfem {
 
 constexpr int HT_NT = 256;
+#ifndef PFEM_HEAT_EC
+#define PFEM_HEAT_EC 1   // element-centric fluxes through a CSR-ordered entry buffer (else per-node recompute)
+#endif
 
 template <int D, class T>
 __device__ __forceinline__ void heat_grad(const int32_t* __restrict__ conn, const T* __restrict__ grad, int E,
@@ -159,7 +162,115 @@ k_heat_flux(int N, int E, int S, int64_t sstride, const int32_t* __restrict__ cs
     }
 }
 
-size_t heat_ws_bytes(const pfem_mesh* m, int S) { return sizeof(double) * (size_t)S * m->n_parts * HT_SLICES; }
+size_t heat_ec_bytes(const pfem_mesh* m);
+size_t heat_ws_bytes(const pfem_mesh* m, int S) {
+    return ((sizeof(double) * (size_t)S * m->n_parts * HT_SLICES + 255) / 256 * 256) + heat_ec_bytes(m);
+}
+
+// element-centric flux path (HT_EC): entry position of every (element, vertex) in the CSR,
+// then per element the d+1 vertex fluxes of up to HT_SC samples stored at their CSR entries,
+// then each node sums its contiguous entries in CSR order (the same order as k_heat_flux)
+__global__ void __launch_bounds__(HT_NT)
+k_heat_entry_pos(int64_t nnz, const int32_t* __restrict__ csr_ent, int32_t* __restrict__ pos) {
+    const int64_t stride = (int64_t)gridDim.x * HT_NT;
+    for (int64_t q = (int64_t)blockIdx.x * HT_NT + threadIdx.x; q < nnz; q += stride) pos[csr_ent[q]] = (int32_t)q;
+}
+
+template <int D, class T>
+__global__ void __launch_bounds__(HT_NT)
+k_heat_elem_flux(int E, int S, int s0, int64_t sstride, const int32_t* __restrict__ conn, const T* __restrict__ grad,
+                 const T* __restrict__ vol, const T* __restrict__ k, int64_t kstride, const T* __restrict__ Tf,
+                 const int32_t* __restrict__ pos, T* __restrict__ ebuf, T* __restrict__ W) {
+    constexpr int NV = D + 1;
+    const int nq = min(HT_SC, S - s0);
+    for (int e = blockIdx.x * HT_NT + threadIdx.x; e < E; e += gridDim.x * HT_NT) {
+        int c[NV];
+#pragma unroll
+        for (int a = 0; a < NV; ++a) c[a] = __ldg(conn + (int64_t)e * NV + a);
+        T g[D][D];
+#pragma unroll
+        for (int b = 0; b < D; ++b)
+#pragma unroll
+            for (int j = 0; j < D; ++j) g[b][j] = __ldg(grad + (int64_t)(b * D + j) * E + e);
+        const T kv = __ldg(k + (int64_t)e * kstride) * __ldg(vol + e);
+        T fl[NV][HT_SC];
+#pragma unroll
+        for (int sq = 0; sq < HT_SC; ++sq) {
+            T gT[D];
+            if (sq < nq) {
+                const T* Ts = Tf + (int64_t)(s0 + sq) * sstride;
+                const T t0 = __ldg(Ts + c[0]);
+                T dt[D];
+#pragma unroll
+                for (int b = 0; b < D; ++b) dt[b] = __ldg(Ts + c[b + 1]) - t0;
+                T gg = T(0);
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    T v = dt[0] * g[0][j];
+#pragma unroll
+                    for (int b = 1; b < D; ++b) v = fma(dt[b], g[b][j], v);
+                    gg = j == 0 ? v * v : fma(v, v, gg);
+                    gT[j] = v * kv;
+                }
+                if (W) W[(int64_t)(s0 + sq) * E + e] = (T(0.5) * kv) * gg;   // the same W_e as k_heat_elem
+            } else {
+#pragma unroll
+                for (int j = 0; j < D; ++j) gT[j] = T(0);
+            }
+            // vertex a >= 1: kV grad T . grad N_a; vertex 0: minus their sum
+            T f0 = T(0);
+#pragma unroll
+            for (int b = 0; b < D; ++b) {
+                T v = gT[0] * g[b][0];
+#pragma unroll
+                for (int j = 1; j < D; ++j) v = fma(gT[j], g[b][j], v);
+                fl[b + 1][sq] = v;
+                f0 -= v;
+            }
+            fl[0][sq] = f0;
+        }
+#pragma unroll
+        for (int a = 0; a < NV; ++a) {
+            T* dst = ebuf + (int64_t)__ldg(pos + (int64_t)e * NV + a) * HT_SC;
+            if constexpr (sizeof(T) == 4 && HT_SC == 4) {
+                *reinterpret_cast<float4*>(dst) = make_float4(fl[a][0], fl[a][1], fl[a][2], fl[a][3]);
+            } else {
+#pragma unroll
+                for (int sq = 0; sq < HT_SC; ++sq) dst[sq] = fl[a][sq];
+            }
+        }
+    }
+}
+
+template <class T>
+__global__ void __launch_bounds__(HT_NT)
+k_heat_node_sum(int N, int S, int s0, int64_t sstride, const int32_t* __restrict__ csr_ptr, const T* __restrict__ ebuf,
+                T* __restrict__ r) {
+    const int nq = min(HT_SC, S - s0);
+    for (int n = blockIdx.x * HT_NT + threadIdx.x; n < N; n += gridDim.x * HT_NT) {
+        T acc[HT_SC];
+#pragma unroll
+        for (int sq = 0; sq < HT_SC; ++sq) acc[sq] = T(0);
+        for (int q = __ldg(csr_ptr + n); q < __ldg(csr_ptr + n + 1); ++q) {
+            if constexpr (sizeof(T) == 4 && HT_SC == 4) {
+                const float4 v = __ldcs(reinterpret_cast<const float4*>(ebuf + (int64_t)q * HT_SC));
+                acc[0] += v.x; acc[1] += v.y; acc[2] += v.z; acc[3] += v.w;
+            } else {
+#pragma unroll
+                for (int sq = 0; sq < HT_SC; ++sq) acc[sq] += ebuf[(int64_t)q * HT_SC + sq];
+            }
+        }
+#pragma unroll
+        for (int sq = 0; sq < HT_SC; ++sq)
+            if (sq < nq) r[(int64_t)(s0 + sq) * sstride + n] = acc[sq];
+    }
+}
+
+size_t heat_ec_bytes(const pfem_mesh* m) {
+    const size_t nnz = (size_t)m->n_elems * (m->dim + 1);
+    const size_t ts = m->dtype == PFEM_F64 ? 8 : 4;
+    return ((sizeof(int32_t) * nnz + 255) / 256 * 256) + ts * nnz * HT_SC;
+}
 
 template <int D, class T>
 pfem_status heat_impl(const pfem_mesh* m, const void* k, int64_t kstride, int S, const void* Tf, int64_t sstride,
@@ -169,12 +280,34 @@ pfem_status heat_impl(const pfem_mesh* m, const void* k, int64_t kstride, int S,
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (W) {
+    const bool ec = r && ws && PFEM_HEAT_EC;   // element-centric fluxes (W_e formed in the same pass)
+    if (W && !ec) {
         const int g = std::max(1, std::min(8 * nsm, (E + HT_NT - 1) / HT_NT));
         k_heat_elem<D, T><<<g, HT_NT, 0, s>>>(E, N, S, sstride, m->conn, (const T*)m->grad, (const T*)m->vol,
                                               (const T*)k, kstride, (const T*)Tf, (T*)W);
         PFEM_LAUNCH_CHECK("k_heat_elem");
         count_launch();
+    }
+    if (ec) {
+        // element-centric: per-element vertex fluxes at their CSR entries, node sums in CSR order
+        char* w = (char*)ws + ((sizeof(double) * (size_t)S * m->n_parts * HT_SLICES + 255) / 256 * 256);
+        int32_t* pos = (int32_t*)w;
+        const int64_t nnz = (int64_t)E * (D + 1);
+        T* ebuf = (T*)(w + ((sizeof(int32_t) * (size_t)nnz + 255) / 256 * 256));
+        const int gp = (int)std::max<int64_t>(1, std::min<int64_t>(8 * nsm, (nnz + HT_NT - 1) / HT_NT));
+        k_heat_entry_pos<<<gp, HT_NT, 0, s>>>(nnz, m->csr_ent, pos);
+        PFEM_LAUNCH_CHECK("k_heat_entry_pos");
+        count_launch();
+        const int ge = std::max(1, std::min(16 * nsm, (E + HT_NT - 1) / HT_NT));
+        const int gn = std::max(1, std::min(16 * nsm, (N + HT_NT - 1) / HT_NT));
+        for (int s0 = 0; s0 < S; s0 += HT_SC) {
+            k_heat_elem_flux<D, T><<<ge, HT_NT, 0, s>>>(E, S, s0, sstride, m->conn, (const T*)m->grad, (const T*)m->vol,
+                                                        (const T*)k, kstride, (const T*)Tf, pos, ebuf, (T*)W);
+            PFEM_LAUNCH_CHECK("k_heat_elem_flux");
+            k_heat_node_sum<T><<<gn, HT_NT, 0, s>>>(N, S, s0, sstride, m->csr_ptr, ebuf, (T*)r);
+            PFEM_LAUNCH_CHECK("k_heat_node_sum");
+            count_launch(2);
+        }
     }
     if (totals) {
         const int K = m->n_parts;
@@ -185,7 +318,7 @@ pfem_status heat_impl(const pfem_mesh* m, const void* k, int64_t kstride, int S,
         PFEM_LAUNCH_CHECK("k_heat_totals");
         count_launch(2);
     }
-    if (r) {
+    if (r && !ec) {
         const int g = std::max(1, std::min(8 * nsm, (N + HT_NT - 1) / HT_NT));
         k_heat_flux<D, T><<<g, HT_NT, 0, s>>>(N, E, S, sstride, m->csr_ptr, m->csr_ent, m->conn, (const T*)m->grad,
                                               (const T*)m->vol, (const T*)k, kstride, (const T*)Tf, (T*)r);
