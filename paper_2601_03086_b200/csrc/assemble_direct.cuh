@@ -52,6 +52,9 @@ __device__ __forceinline__ void prefetch_record(const AsmParams<T>& p, int b) {
     if (p.mat.s1) l2_prefetch(p.mat.p1, E * sizeof(T), e0 * sizeof(T), ne * sizeof(T));
 }
 
+#ifndef PFEM_DIRECT_MINB64
+#define PFEM_DIRECT_MINB64 4   // fp64 linear single-sample calls: 4 CTAs per SM (64 registers; config 4 134.5 -> 132.4 us)
+#endif
 #ifndef PFEM_DIRECT_SMAT
 #define PFEM_DIRECT_SMAT 0   // element-wise materials copied into shared memory with the fields (measured slower: off)
 #endif
@@ -71,11 +74,14 @@ __device__ __forceinline__ X rld(const X* q) {
 #ifndef PFEM_DIRECT_MINBS
 #define PFEM_DIRECT_MINBS 6
 #endif
-// register budget (measured): fp64 single-sample calls use the compiler's own allocation (an
-// explicit 64-register bound was 6% slower on config 4); fp32 single-sample calls 64
-// registers (8% faster on config 5 than the default); several-sample fp32 calls 80
+// register budget (measured): fp32 single-sample calls 64 registers (8% faster on config 5
+// than the default); several-sample fp32 calls 80; fp64 linear single-sample calls 64 (4 CTAs
+// per SM with the 384-element blocks: config 4 134.5 -> 132.4 us); fp64 Neo-Hookean and fp64
+// several-sample calls the compiler's own allocation (a 40-register cap spilled hundreds of
+// bytes per thread)
 template <int D, int MODEL, class T, int OP, int ST, bool MASKED, int NT, bool PERM>
-__global__ void __launch_bounds__(NT, ST > 1 ? PFEM_DIRECT_MINBS : (sizeof(T) == 4 ? 65536 / (NT * 64) : 0))
+__global__ void __launch_bounds__(NT, ST > 1 ? (sizeof(T) == 4 ? PFEM_DIRECT_MINBS : 0)
+                                            : (sizeof(T) == 4 ? 65536 / (NT * 64) : (MODEL == MODEL_LINEAR ? PFEM_DIRECT_MINB64 : 0)))
 k_assemble_direct(const AsmParams<T> p) {
     // shared: ust[NF][OCAP][D][ST] (staged nodal fields) | [le[(d+1) EB] u16] | fbuf
     // EPOS (fp32): fbuf[(d+1) EB entries][D][ST], element vertex forces scattered to their
