@@ -57,6 +57,7 @@ __device__ __forceinline__ bool vec_last_block2(VecRed* vr, double v, double v2,
 }
 
 __device__ __forceinline__ double vec_final_part2(VecRed* vr, double* s_red) {
+    __threadfence();   // after the arrival that made this CTA the last one (as vec_final)
     double v = 0.0;
     for (int i0 = threadIdx.x; i0 < (int)gridDim.x; i0 += 8 * VEC_NT) {
         double w[8];
