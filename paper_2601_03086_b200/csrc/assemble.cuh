@@ -513,7 +513,11 @@ k_assemble(const AsmParams<T> p) {
     __shared__ double s_red[NT / 32][2 * ST + 1];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int S = p.S;
-    const bool pref = S <= ST;          // nodal fields staged in shared memory (else direct gathers)
+    // work items: (block, sample chunk of ST samples), chunk-major, so S > ST calls spread over
+    // all CTAs; every item stages its chunk's nodal fields in shared memory
+    constexpr bool pref = true;
+    const int nb = p.n_blocks;
+    const int NI = nb * ((S + ST - 1) / ST);
     const bool cgdot = OP == OP_TANGENT && p.cg != nullptr;
     if (p.cg && ld_relaxed_i(&p.cg->done)) return;     // converged CG: the whole grid exits
 
@@ -534,31 +538,30 @@ k_assemble(const AsmParams<T> p) {
     uint32_t par0 = 0u, par1 = 0u;   // mbarrier phase of each record buffer (registers, no arrays)
     // prologue: record of the first block, then its fields
     const bool has_mat = (p.mat.s0 | p.mat.s1) != 0;
-    if (t < p.n_blocks) {
-        stage_block<D, T, NT>(stage0, mstage, &s_bar[0], p, t);
-        if (pref || has_mat) {
-            mbar_wait(&s_bar[0], 0);
-            if (pref) {
-                const int no0 = __ldg(p.blk_occ + t + 1) - __ldg(p.blk_occ + t);
-                stage_fields<D, T, NT, ST, MASKED>(ustage, stage0, p.rec_base, staged_src, p, 0, S, no0);
-                if (NF == 2) stage_fields<D, T, NT, ST, false>(ustage + ust1, stage0, p.rec_base, p.u, p, 0, S, no0);
-            }
-            if (has_mat) stage_material<T, NT>(mstage, stage0, p.rec_base, p, t);
-        }
+    if (t < NI) {
+        const int bt = t % nb, s0t = (t / nb) * ST;
+        stage_block<D, T, NT>(stage0, mstage, &s_bar[0], p, bt);
+        mbar_wait(&s_bar[0], 0);
+        const int no0 = __ldg(p.blk_occ + bt + 1) - __ldg(p.blk_occ + bt);
+        stage_fields<D, T, NT, ST, MASKED>(ustage, stage0, p.rec_base, staged_src, p, s0t, min(ST, S - s0t), no0);
+        if (NF == 2) stage_fields<D, T, NT, ST, false>(ustage + ust1, stage0, p.rec_base, p.u, p, s0t, min(ST, S - s0t), no0);
+        if (has_mat) stage_material<T, NT>(mstage, stage0, p.rec_base, p, bt);
         cp_commit();
     }
-    for (int it = 0; t < p.n_blocks; ++it, t += G) {
+    for (int it = 0; t < NI; ++it, t += G) {
         const int cur = it & 1;
         const int tn = t + G;
-        const int b = t;
-        // prefetch the next block's record (its fields follow after phase 1)
+        const int b = t % nb, bn = tn % nb;
+        const int s0 = (t / nb) * ST;          // this item's sample chunk
+        const int nq = min(ST, S - s0);
+        // prefetch the next item's record (its fields follow after phase 1)
         unsigned char* const sg_cur = cur ? stage1 : stage0;
         unsigned char* const sg_nxt = cur ? stage0 : stage1;
-        if (tn < p.n_blocks) stage_block<D, T, NT>(sg_nxt, mstage + 2 * EB * (cur ^ 1), &s_bar[cur ^ 1], p, tn);
+        if (tn < NI) stage_block<D, T, NT>(sg_nxt, mstage + 2 * EB * (cur ^ 1), &s_bar[cur ^ 1], p, bn);
         else cp_commit();
-        if (PFEM_STAGED_L2PF && tid == 32 && tn + G < p.n_blocks) {
+        if (PFEM_STAGED_L2PF && tid == 32 && tn + G < NI) {
             // the record after next into L2, so next iteration's bulk copy is an L2 hit
-            const size_t rb = p.rec.bytes, off = (size_t)(tn + G) * rb + p.rec_base;
+            const size_t rb = p.rec.bytes, off = (size_t)((tn + G) % nb) * rb + p.rec_base;
             const uintptr_t a0 = (uintptr_t)(p.recs + off), a1 = (uintptr_t)(p.recs + off + (p.rec_end - p.rec_base));
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((unsigned)(a1 - a0)) : "memory");
         }
@@ -582,11 +585,10 @@ k_assemble(const AsmParams<T> p) {
         cp_wait<1>();                          // this thread's material + field copies of block b
         bar_main(NT);                          // everyone's field copies have landed
         double dot_acc = 0.0;
-        double wsum[ST], fsum[ST];
+        double fsum[ST];
 #pragma unroll
-        for (int q = 0; q < ST; ++q) wsum[q] = fsum[q] = 0.0;
-        for (int s0 = 0; s0 < S; s0 += ST) {
-            const int nq = min(ST, S - s0);
+        for (int q = 0; q < ST; ++q) fsum[q] = 0.0;
+        {
             // ---------------- phase 1: elements
             T wacc[ST];
 #pragma unroll
@@ -695,16 +697,12 @@ k_assemble(const AsmParams<T> p) {
                     }
                 }
             }
-            if (S > ST) {
-#pragma unroll
-                for (int q = 0; q < ST; ++q) wsum[q] += (double)wacc[q];   // per-thread, fixed order
-            }
-            if (HAS_PSI && S <= ST && !(p.dbg & 8)) {
+            if (HAS_PSI && !(p.dbg & 8)) {
                 // per-warp energy sums now, while other warps finish phase 1 (s_red is free:
-                // the previous block's warp 0 read it before this block's first barrier)
+                // the previous item's warp 0 read it before this item's first barrier)
                 T wv[ST];
 #pragma unroll
-                for (int q = 0; q < ST; ++q) wv[q] = q < S ? wacc[q] : T(0);
+                for (int q = 0; q < ST; ++q) wv[q] = q < nq ? wacc[q] : T(0);
                 const T r = warp_multi_sum<T, ST>(wv, lane);
                 if ((lane & (32 / ST - 1)) == 0) s_red[warp][lane / (32 / ST)] = (double)r;
             }
@@ -712,17 +710,16 @@ k_assemble(const AsmParams<T> p) {
             // are done (the barrier before phase 2); its record has had phase 1 to land, and
             // the copies have phase 2 to complete
             const bool do_p2 = (HAS_FORCE || p.f_ext) && !(p.dbg & 2);
-            if (do_p2 || (pref && s0 + ST >= S)) bar_main(NT);
-            if (s0 + ST >= S) {
-                if ((pref || has_mat) && tn < p.n_blocks) {
+            bar_main(NT);   // every thread's phase-1 reads of the field buffer are done
+            {
+                if (tn < NI) {
                     mbar_wait(&s_bar[cur ^ 1], cur ? par0 : par1);
-                    if (pref) {
-                        const int non = __ldg(p.blk_occ + tn + 1) - __ldg(p.blk_occ + tn);
-                        stage_fields<D, T, NT, ST, MASKED>(ustage, sg_nxt, p.rec_base, staged_src, p, 0, S, non);
-                        if (NF == 2) stage_fields<D, T, NT, ST, false>(ustage + ust1, sg_nxt, p.rec_base, p.u, p, 0, S, non);
-                    }
+                    const int non = __ldg(p.blk_occ + bn + 1) - __ldg(p.blk_occ + bn);
+                    const int s0n = (tn / nb) * ST, nqn = min(ST, S - s0n);
+                    stage_fields<D, T, NT, ST, MASKED>(ustage, sg_nxt, p.rec_base, staged_src, p, s0n, nqn, non);
+                    if (NF == 2) stage_fields<D, T, NT, ST, false>(ustage + ust1, sg_nxt, p.rec_base, p.u, p, s0n, nqn, non);
                     if (has_mat)
-                        stage_material<T, NT>(mstage + 2 * EB * (cur ^ 1), sg_nxt, p.rec_base, p, tn);
+                        stage_material<T, NT>(mstage + 2 * EB * (cur ^ 1), sg_nxt, p.rec_base, p, bn);
                 }
                 cp_commit();
             }
@@ -846,33 +843,13 @@ k_assemble(const AsmParams<T> p) {
                     }
                 }
             }
-            if (HAS_PSI && S > ST) {
-                // several sample chunks: flush this chunk's per-sample sums directly
-                bar_main(NT);
-#pragma unroll
-                for (int q = 0; q < ST; ++q) {
-                    double a = warp_sum(q < nq ? wsum[q] : 0.0), f2 = warp_sum(q < nq ? fsum[q] : 0.0);
-                    if (lane == 0) { s_red[warp][q] = a; s_red[warp][ST + q] = f2; }
-                    wsum[q] = fsum[q] = 0.0;
-                }
-                bar_main(NT);
-                if (tid < 2 * nq) {
-                    const int q = tid % nq, kind = tid / nq;
-                    double r = 0.0;
-                    for (int w = 0; w < NT / 32; ++w) r += s_red[w][kind * ST + q];
-                    p.blk_sum[(int64_t)(kind * S + s0 + q) * p.n_blocks + b] = r;
-                }
-                bar_main(NT);
-            } else if (HAS_FORCE && s0 + ST < S) {
-                bar_main(NT);   // fbuf is reused by the next chunk
-            }
         }
-        // ---------------- per-block sums (single-chunk case) and CG dot
-        if (((HAS_PSI && S <= ST) || cgdot) && !(p.dbg & 8)) {
-            if (HAS_PSI && S <= ST) {   // (the energy sums went to s_red after phase 1)
+        // ---------------- per-item sums (the item's samples) and CG dot
+        if ((HAS_PSI || cgdot) && !(p.dbg & 8)) {
+            if (HAS_PSI) {   // (the energy sums went to s_red after phase 1)
 #pragma unroll
                 for (int q = 0; q < ST; ++q) {
-                    if (q >= S) break;
+                    if (q >= nq) break;
                     const double f2 = p.f_ext ? warp_sum(fsum[q]) : 0.0;
                     if (lane == 0) s_red[warp][ST + q] = f2;
                 }
@@ -883,12 +860,12 @@ k_assemble(const AsmParams<T> p) {
             }
         }
         bar_main(NT);   // phase 2 done (fbuf free), s_red complete
-        if (((HAS_PSI && S <= ST) || cgdot) && !(p.dbg & 8) && warp == 0) {
-            if (HAS_PSI && S <= ST && lane < 2 * S) {
-                const int q = lane % S, kind = lane / S;
+        if ((HAS_PSI || cgdot) && !(p.dbg & 8) && warp == 0) {
+            if (HAS_PSI && lane < 2 * nq) {
+                const int q = lane % nq, kind = lane / nq;
                 double r = 0.0;
                 for (int w = 0; w < NT / 32; ++w) r += s_red[w][kind * ST + q];
-                p.blk_sum[(int64_t)(kind * S + q) * p.n_blocks + b] = r;
+                p.blk_sum[(int64_t)(kind * S + s0 + q) * p.n_blocks + b] = r;
             }
             if (cgdot && lane == 31) {
                 double r = 0.0;

@@ -171,7 +171,7 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
         // the staged copy (RecLayout order) skips conn when the fields are staged and the NH
         // state u is not gathered; fp32 (force buffer in entry order) reads ent_pos and not
         // loc_ent, fp64 (loc_ent gather) the reverse
-        const bool need_conn = p.S > ST;   // (the NH tangent state is staged with the fields)
+        const bool need_conn = false;   // every work item stages its fields (and the NH state u)
         constexpr bool EPOS = sizeof(T) == 4 && PFEM_STAGED_EPOS;
         p.rec_base = need_conn ? p.rec.conn : (EPOS ? p.rec.ent_pos : p.rec.g);
         p.rec_end = EPOS ? p.rec.loc_ent : p.rec.bytes;
@@ -194,7 +194,8 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
             }
             resident = per_sm * nsm;
         }
-        const int grid = std::max(1, std::min(resident, p.n_blocks));
+        const int items = p.n_blocks * ((p.S + ST - 1) / ST);   // (block, sample chunk) work items
+        const int grid = std::max(1, std::min(resident, items));
         kern<<<grid, NT, smem, s>>>(p);
         PFEM_LAUNCH_CHECK("k_assemble");
     }
