@@ -501,7 +501,7 @@ k_assemble(const AsmParams<T> p) {
     const T* staged_src = (OP == OP_TANGENT) ? p.v : p.u;
     // shared layout: rec[2] | mat[2][2][EB] | ust[2][OCAP][D][ST] | fbuf[NV][EB][D][ST]
     const uint32_t srb = p.rec_end - p.rec_base;     // staged bytes of a record
-    const bool has_conn = p.rec_base <= p.rec.conn;   // conn is staged (gathers, NH tangent state)
+    constexpr bool has_conn = false;   // every item stages its fields: no global gathers need node ids
     unsigned char* const stage0 = smem_raw;
     unsigned char* const stage1 = smem_raw + srb;
     T* mstage = reinterpret_cast<T*>(smem_raw + 2 * (size_t)srb);

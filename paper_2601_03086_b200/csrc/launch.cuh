@@ -168,12 +168,11 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
                                       : launch_direct<D, MODEL, T, OP, ST, MASKED, direct_nt<T>(), false>(p, s);
         if (st != PFEM_OK) return st;
     } else {
-        // the staged copy (RecLayout order) skips conn when the fields are staged and the NH
-        // state u is not gathered; fp32 (force buffer in entry order) reads ent_pos and not
-        // loc_ent, fp64 (loc_ent gather) the reverse
-        const bool need_conn = false;   // every work item stages its fields (and the NH state u)
+        // the staged copy (RecLayout order) skips conn: every work item stages its fields (and
+        // the NH state u); fp32 with the force buffer in entry order would read ent_pos and not
+        // loc_ent, the element-major buffer reads loc_ent
         constexpr bool EPOS = sizeof(T) == 4 && PFEM_STAGED_EPOS;
-        p.rec_base = need_conn ? p.rec.conn : (EPOS ? p.rec.ent_pos : p.rec.g);
+        p.rec_base = EPOS ? p.rec.ent_pos : p.rec.g;
         p.rec_end = EPOS ? p.rec.loc_ent : p.rec.bytes;
         const size_t smem = 2 * (size_t)(p.rec_end - p.rec_base) + 4 * EB * sizeof(T) +
                             (size_t)NF * p.rec.ocap * D * ST * sizeof(T) +
