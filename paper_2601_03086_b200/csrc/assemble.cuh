@@ -51,6 +51,9 @@
 #ifndef PFEM_STAGED_EPOS
 #define PFEM_STAGED_EPOS 0
 #endif
+#ifndef PFEM_HP2_2D
+#define PFEM_HP2_2D 1         // two phase-2 threads per occurrence for T3 as well
+#endif
 #ifndef PFEM_STAGED_HP2
 #define PFEM_STAGED_HP2 1
 #endif
@@ -495,7 +498,7 @@ k_assemble(const AsmParams<T> p) {
     // block-CSR entry (ent_pos), so an occurrence's entries are contiguous in phase 2.
     // !EPOS (fp64): fbuf[NV][EB][D][ST] in element order, gathered through loc_ent.
     constexpr bool EPOS = sizeof(T) == 4 && PFEM_STAGED_EPOS;
-    constexpr int HP = (sizeof(T) == 4 && ST == 4 && D == 3 && !EPOS && PFEM_STAGED_HP2) ? 2 : 1;   // phase-2 threads per occurrence
+    constexpr int HP = (sizeof(T) == 4 && ST == 4 && (D == 3 || PFEM_HP2_2D) && !EPOS && PFEM_STAGED_HP2) ? 2 : 1;   // phase-2 threads per occurrence
     constexpr int STH = ST / HP;
     constexpr int SDH = D * STH;
     const T* staged_src = (OP == OP_TANGENT) ? p.v : p.u;
