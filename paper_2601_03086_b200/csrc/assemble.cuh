@@ -51,6 +51,9 @@
 #ifndef PFEM_STAGED_EPOS
 #define PFEM_STAGED_EPOS 0
 #endif
+#ifndef PFEM_DBG
+#define PFEM_DBG 0            // compile the PFEM_DEBUG ablation switches into the staged kernel (tools)
+#endif
 #ifndef PFEM_HP2_2D
 #define PFEM_HP2_2D 1         // two phase-2 threads per occurrence for T3 as well
 #endif
@@ -521,7 +524,7 @@ k_assemble(const AsmParams<T> p) {
     constexpr bool pref = true;
     const int nb = p.n_blocks;
     const int NI = nb * ((S + ST - 1) / ST);
-    const bool cgdot = OP == OP_TANGENT && p.cg != nullptr;
+    constexpr bool cgdot = false;   // CG products are single-sample calls: the direct form
     if (p.cg && ld_relaxed_i(&p.cg->done)) return;     // converged CG: the whole grid exits
 
     if (tid == 0) {
@@ -644,7 +647,7 @@ k_assemble(const AsmParams<T> p) {
                 }
 #pragma unroll
                 for (int qq = 0; qq < ST; qq += L) {
-                    if (qq >= nq || (p.dbg & 1)) break;
+                    if (qq >= nq || (PFEM_DBG && (p.dbg & 1))) break;
                     const int s = s0 + qq;
                     const int64_t lstride = (L > 1 && qq + 1 >= nq) ? 0 : p.sstride;
                     V x[NV][D], H[D][D], P[D][D], psi = V(T(0));
@@ -700,7 +703,7 @@ k_assemble(const AsmParams<T> p) {
                     }
                 }
             }
-            if (HAS_PSI && !(p.dbg & 8)) {
+            if (HAS_PSI && !(PFEM_DBG && (p.dbg & 8))) {
                 // per-warp energy sums now, while other warps finish phase 1 (s_red is free:
                 // the previous item's warp 0 read it before this item's first barrier)
                 T wv[ST];
@@ -712,7 +715,7 @@ k_assemble(const AsmParams<T> p) {
             // the next block's fields, into the same buffer once every thread's phase-1 reads
             // are done (the barrier before phase 2); its record has had phase 1 to land, and
             // the copies have phase 2 to complete
-            const bool do_p2 = (HAS_FORCE || p.f_ext) && !(p.dbg & 2);
+            const bool do_p2 = (HAS_FORCE || p.f_ext) && !(PFEM_DBG && (p.dbg & 2));
             bar_main(NT);   // every thread's phase-1 reads of the field buffer are done
             {
                 if (tn < NI) {
@@ -848,7 +851,7 @@ k_assemble(const AsmParams<T> p) {
             }
         }
         // ---------------- per-item sums (the item's samples) and CG dot
-        if ((HAS_PSI || cgdot) && !(p.dbg & 8)) {
+        if ((HAS_PSI || cgdot) && !(PFEM_DBG && (p.dbg & 8))) {
             if (HAS_PSI) {   // (the energy sums went to s_red after phase 1)
 #pragma unroll
                 for (int q = 0; q < ST; ++q) {
@@ -863,7 +866,7 @@ k_assemble(const AsmParams<T> p) {
             }
         }
         bar_main(NT);   // phase 2 done (fbuf free), s_red complete
-        if ((HAS_PSI || cgdot) && !(p.dbg & 8) && warp == 0) {
+        if ((HAS_PSI || cgdot) && !(PFEM_DBG && (p.dbg & 8)) && warp == 0) {
             if (HAS_PSI && lane < 2 * nq) {
                 const int q = lane % nq, kind = lane / nq;
                 double r = 0.0;

@@ -162,7 +162,8 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
     // PFEM_VARIANT=0/1 forces staged/direct (measurement switch).
     // Blocks larger than the staged kernel's compile-time capacity always take the direct form.
     // (the staged form reads the record with its compile-time stride EB)
-    const bool direct = p.eb_max > EB || p.rec.eb != EB || (variant >= 0 ? variant == 1 : p.S == 1);
+    // (CG products, p.cg set, always take the direct form: the staged kernel has no fused p.q)
+    const bool direct = p.eb_max > EB || p.rec.eb != EB || p.cg != nullptr || (variant >= 0 ? variant == 1 : p.S == 1);
     if (direct) {
         const pfem_status st = p.perm ? launch_direct<D, MODEL, T, OP, ST, MASKED, direct_nt<T>(), true>(p, s)
                                       : launch_direct<D, MODEL, T, OP, ST, MASKED, direct_nt<T>(), false>(p, s);

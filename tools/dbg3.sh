@@ -1,5 +1,6 @@
 #!/bin/bash
-# config-3 E+R (and K.v) kernel time under PFEM_DEBUG ablation switches
+# config-3 E+R (and K.v) kernel time under PFEM_DEBUG ablation switches; the kernel-side switches
+# need a build with them compiled in: python tools/ab_build.py dbg PFEM_DBG=1, then PFEM_LIB=libpfem_dbg.so
 cd "$(dirname "$0")/.." || exit 1
 for d in 0 32 33 34 40 35 43 59; do
   for op in er kv; do
