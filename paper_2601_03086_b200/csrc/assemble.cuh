@@ -902,16 +902,27 @@ k_node_finish(const AsmParams<T> p, int op_psi, int n_items) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int S = p.S;
     const bool cgdot = p.cg != nullptr;
+    // the first item's plan metadata (not written by kernel A) loads before the wait, so its
+    // latency overlaps kernel A's tail
+    const int nsc = (S + ST - 1) / ST;
+    const int item0 = blockIdx.x * NTB + tid;
+    int node0 = 0, k00 = 0, k10 = 0;
+    if (item0 < n_items) {
+        const int f = item0 / nsc;
+        node0 = __ldg(p.fix_node + f);
+        k00 = __ldg(p.fix_src_ptr + f);
+        k10 = __ldg(p.fix_src_ptr + f + 1);
+    }
     asm volatile("griddepcontrol.wait;" ::: "memory");    // kernel A complete and visible
     if (p.cg && ld_relaxed_i(&p.cg->done)) return;
     double dot_acc = 0.0;
     // ---------------- multi-block nodes: item = (fix entry, sample chunk)
-    const int nsc = (S + ST - 1) / ST;
-    for (int item = blockIdx.x * NTB + tid; item < n_items; item += gridDim.x * NTB) {
+    for (int item = item0; item < n_items; item += gridDim.x * NTB) {
         const int f = item / nsc, s0 = (item - f * nsc) * ST;
         const int nq = min(ST, S - s0);
-        const int node = __ldg(p.fix_node + f);
-        const int k0 = __ldg(p.fix_src_ptr + f), k1 = __ldg(p.fix_src_ptr + f + 1);
+        const bool first = item == item0;
+        const int node = first ? node0 : __ldg(p.fix_node + f);
+        const int k0 = first ? k00 : __ldg(p.fix_src_ptr + f), k1 = first ? k10 : __ldg(p.fix_src_ptr + f + 1);
         // the node's segments are contiguous: seg[k][s][d], k in [k0, k1) (ascending block)
         T acc[SD];
         ld_seg_vec<T, SD>(p.partial + ((int64_t)k0 * S + s0) * D, acc, nq * D);
