@@ -900,7 +900,7 @@ k_node_finish(const AsmParams<T> p, int op_psi, int n_items) {
     __shared__ int s_last;
     constexpr int SD = ST * D;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int S = p.S;
+    const int S = ST == 1 ? 1 : p.S;   // single-sample instantiations serve S = 1 only (dispatch_st)
     const bool cgdot = p.cg != nullptr;
     // the first item's plan metadata (not written by kernel A) loads before the wait, so its
     // latency overlaps kernel A's tail

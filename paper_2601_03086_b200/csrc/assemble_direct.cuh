@@ -99,7 +99,9 @@ k_assemble_direct(const AsmParams<T> p) {
     using V = std::conditional_t<(sizeof(T) == 4 && ST % 2 == 0 && !PFEM_DIRECT_SCALAR), F2, T>;
     constexpr int L = VTraits<V>::L;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int S = p.S;
+    // single-sample instantiations serve S = 1 only (dispatch_st); folding it into the fp64 code
+    // measured faster (config 4 132.4 -> 130.5 us), into the fp32 code slower (config 5 71 -> 73)
+    const int S = (ST == 1 && sizeof(T) == 8) ? 1 : p.S;
     const int EB = p.rec.eb;                                    // record / fbuf stride
     const size_t ust_sz = (size_t)p.rec.ocap * D * ST;
     constexpr bool TMA = PFEM_DIRECT_TMA && sizeof(T) == 4;
