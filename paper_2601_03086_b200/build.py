@@ -52,6 +52,8 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False, 
         return LIB
     os.makedirs(bdir, exist_ok=True)
     extra = (["-Xptxas", "-v"] if ptxas_info else []) + [f"-D{d}" for d in defines]
+    if tag and os.environ.get("PFEM_NVCC_EXTRA"):   # A/B builds only: extra nvcc flags
+        extra += os.environ["PFEM_NVCC_EXTRA"].split()
 
     def compile_one(src):
         obj = os.path.join(bdir, os.path.basename(src) + ".o")
