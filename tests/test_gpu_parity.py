@@ -593,3 +593,23 @@ def test_heat_matches_oracle(orc, prob):
     W1, _, r1 = pf.heat(mesh, torch.tensor([1.5], dtype=dt, device="cuda"), torch.as_tensor(T, dtype=dt, device="cuda"))
     Wo1, _, ro1 = om.heat(T, [1.5])
     assert rel_l2(r1.cpu().numpy(), ro1) < tol and rel_l2(W1.cpu().numpy(), Wo1) < tol
+
+
+def test_staged_items_multi_part_ragged_samples(orc):
+    """The staged form's (block, sample chunk) items on a two-part mesh with a ragged last chunk
+    (S = 6 fp32: chunks of 4 + 2; S = 5 fp64: 2 + 2 + 1): W_e, per-(sample, part) totals with
+    nodal loads, the residual and K.v match the oracle."""
+    rng = np.random.default_rng(41)
+    ca, ta = square_t3(31, 19)
+    cb, tb = square_t3(13, 37)
+    coords = np.concatenate([ca, cb + 3.0])
+    conn = np.concatenate([ta, tb + len(ca)]).astype(np.int32)
+    pe = np.array([0, len(ta), len(conn)], np.int32)
+    pn = np.array([0, len(ca), len(coords)], np.int32)
+    for S, dt in ((6, "f32"), (5, "f64")):
+        u = np.stack([0.05 * fourier_field(coords, rng) for _ in range(S)])
+        p = Problem(f"two-parts-S{S}-{dt}", 2, coords, conn, "neohookean", "lame", rng.uniform(0.3, 1.0, len(conn)),
+                    rng.uniform(0.3, 1.0, len(conn)), u, dt, part_elem=pe, part_node=pn)
+        f = rng.standard_normal(coords.shape) * 1e-2
+        check_energy(orc, p, "csr", f_ext=f)
+        check_tangent(orc, p, "csr")
