@@ -450,6 +450,47 @@ def run_extras(torch, pf, dev, peak):
                                    "note": "timed back-to-back on one copy (partly L2-resident)"}
     del m5, outs
     torch.cuda.empty_cache()
+    # ---------------- configs 1 and 2 (BASELINE configs[0], configs[1]): latency of the tiny
+    # case; config 2 fused E+R over 32 fields in fp32 and fp64 (3 rotating copies > L2)
+    from pfem_gen import config1, config2
+    p1 = config1()
+    m1 = pf.Mesh(torch.as_tensor(p1.coords, device=dev), torch.as_tensor(p1.conn, device=dev), dtype=torch.float64)
+    mat1 = pf.Material("linear", "young_poisson", torch.as_tensor(p1.p0, device=dev), torch.as_tensor(p1.p1, device=dev))
+    u1 = torch.as_tensor(p1.u, device=dev)
+    out1 = (torch.empty((1, 1), dtype=torch.float64, device=dev), torch.empty((1, p1.n_elems), dtype=torch.float64, device=dev),
+            torch.empty_like(u1))
+    for _ in range(5):
+        pf.energy(m1, mat1, u1, elem_energy=True, residual=True, out=out1)
+    t1 = time_events(torch, lambda: pf.energy(m1, mat1, u1, elem_energy=True, residual=True, out=out1), 200)
+    ex["config1_energy_residual"] = {"E": p1.n_elems, "us": t1 * 1e3, "note": "latency: one E+R call on 450 T3 (fp64)"}
+    for dt_name, tdt, sz in (("f32", torch.float32, 4), ("f64", torch.float64, 8)):
+        p2 = config2(dtype=dt_name)
+        E2, N2, S2 = p2.n_elems, p2.n_nodes, p2.u.shape[0]
+        cps = []
+        for c in range(3):
+            m2 = pf.Mesh(torch.as_tensor(p2.coords, device=dev), torch.as_tensor(p2.conn, device=dev), dtype=tdt)
+            mat2 = pf.Material("linear", "young_poisson", torch.as_tensor(p2.p0, dtype=tdt, device=dev),
+                               torch.as_tensor(p2.p1, dtype=tdt, device=dev))
+            u2 = torch.as_tensor(p2.u, dtype=tdt, device=dev)
+            cps.append((m2, mat2, u2, (torch.empty((S2, 1), dtype=tdt, device=dev),
+                                       torch.empty((S2, E2), dtype=tdt, device=dev), torch.empty_like(u2))))
+        for i in range(6):
+            m2, mat2, u2, o2 = cps[i % 3]
+            pf.energy(m2, mat2, u2, elem_energy=True, residual=True, out=o2)
+        i2 = [0]
+
+        def c2_call():
+            m2, mat2, u2, o2 = cps[i2[0] % 3]
+            pf.energy(m2, mat2, u2, elem_energy=True, residual=True, out=o2)
+            i2[0] += 1
+        t2 = time_events(torch, c2_call, 60)
+        B2 = bytes_energy_residual(E2, N2, 2, S2, sz, True, 1)
+        ex[f"config2_energy_residual_{dt_name}"] = {"E": E2, "S": S2, "us": t2 * 1e3, "algorithmic_bytes": B2,
+                                                    "GBps": B2 / (t2 * 1e-3) / 1e9, "frac": B2 / (t2 * 1e-3) / 1e9 / peak,
+                                                    "element_samples_per_s": E2 * S2 / (t2 * 1e-3),
+                                                    "l2": "3 rotating copies"}
+        del cps
+    torch.cuda.empty_cache()
     # ---------------- §8(f) f4: steady heat conduction on the config-3 mesh (4 fields, fp32)
     from pfem_gen import config3
     p3 = config3()
@@ -468,7 +509,15 @@ def run_extras(torch, pf, dev, peak):
         ih[0] += 1
     th = time_events(torch, heat_call, 30)
     B_h = E3 * (16 + 9 * 4 + 4 + 4) + 4 * (N3 * 4 * 2 + E3 * 4 + 4) + N3 * 4
-    ex["heat_config3_mesh"] = {"E": E3, "S": 4, "us": th * 1e3, "algorithmic_bytes": B_h,
+    ih[0] = 0
+
+    def heat_otf_call():
+        pf.heat(m3, k3, T3s[ih[0] % 3], f=f3, geometry_on_the_fly=True)
+        ih[0] += 1
+    heat_otf_call()
+    th_otf = time_events(torch, heat_otf_call, 30)
+    ex["heat_config3_mesh"] = {"E": E3, "S": 4, "us": th * 1e3, "us_geometry_on_the_fly": th_otf * 1e3,
+                               "algorithmic_bytes": B_h,
                                "GBps": B_h / (th * 1e-3) / 1e9, "frac": B_h / (th * 1e-3) / 1e9 / peak,
                                "element_samples_per_s": E3 * 4 / (th * 1e-3),
                                "kernels": "k_heat_elem + k_heat_totals + k_heat_flux (CSR gather, element gradient re-formed per entry)"}

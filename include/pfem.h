@@ -242,10 +242,15 @@ pfem_status pfem_pretrain_loss(const pfem_mesh* m, const pfem_material* mat, int
  * Sums in fixed order (per part: 64 fixed slices, each a CTA tree, then the slices in order;
  * per node: CSR order); asynchronous on `stream`.
  * --------------------------------------------------------------------------------- */
+/* options: PFEM_HEAT_GEOMETRY_ON_THE_FLY forms grad N_a and V_e in fp64 from the mesh
+ * coordinates inside the element pass (with a workspace and fluxes requested) instead of
+ * reading the prepared gradients and volumes (SURVEY §8(f) row f4 variant) */
+#define PFEM_HEAT_GEOMETRY_ON_THE_FLY 1
 size_t pfem_heat_workspace_bytes(const pfem_mesh* m, int32_t n_samples);
 pfem_status pfem_heat(const pfem_mesh* m, const void* k, int64_t k_stride, int32_t n_samples,
                       const void* T, int64_t sample_stride, const void* f_nodal, void* elem_energy,
-                      void* totals, void* flux, void* ws, size_t ws_bytes, void* stream);
+                      void* totals, void* flux, int32_t options, void* ws, size_t ws_bytes,
+                      void* stream);
 
 /* Internal force only (no energy arithmetic), see pfem_energy. */
 pfem_status pfem_residual(const pfem_mesh* m, const pfem_material* mat, int32_t n_samples,

@@ -88,7 +88,8 @@ SIGNATURES = {
                                      C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "pfem_heat_workspace_bytes": (C.c_size_t, [C.POINTER(pfem_mesh), C.c_int32]),
     "pfem_heat": (C.c_int, [C.POINTER(pfem_mesh), C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64,
-                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_size_t,
+                            C.c_void_p]),
     "pfem_tangent_diag": (C.c_int, [C.POINTER(pfem_mesh), C.POINTER(pfem_material), C.c_void_p, C.c_void_p,
                                     C.c_void_p, C.c_void_p]),
     "pfem_pcg": (C.c_int, [C.POINTER(pfem_mesh), C.POINTER(pfem_material), C.c_void_p, C.c_void_p, C.c_void_p,

@@ -233,7 +233,8 @@ def pretrain_loss(mesh: Mesh, mat: Material, H: torch.Tensor, phi=None, f_ext=No
     return loss, totals, grad, (u if phi is not None else H)
 
 
-def heat(mesh: Mesh, k: torch.Tensor, T: torch.Tensor, f=None, elem_energy=True, totals=True, flux=True):
+def heat(mesh: Mesh, k: torch.Tensor, T: torch.Tensor, f=None, elem_energy=True, totals=True, flux=True,
+         geometry_on_the_fly: bool = False):
     """pfem_heat: steady heat conduction on the prepared mesh.  T: [S, N] (or [N]); k: per element
     or numel 1.  Returns (W_e [S, E] or None, totals [S, K] or None, flux [S, N] or None)."""
     _require_cuda(T, k)
@@ -249,7 +250,8 @@ def heat(mesh: Mesh, k: torch.Tensor, T: torch.Tensor, f=None, elem_energy=True,
         ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=dev)
         mesh._ws[("heat", S)] = ws
     L.check(L.load().pfem_heat(mesh.ref(), _ptr(k), 0 if k.numel() == 1 else 1, S, _ptr(T), T.shape[1], _ptr(f),
-                               _ptr(W), _ptr(tot), _ptr(r), _ptr(ws), ws.numel(), _stream()))
+                               _ptr(W), _ptr(tot), _ptr(r), 1 if geometry_on_the_fly else 0, _ptr(ws), ws.numel(),
+                               _stream()))
     return W, tot, r
 
 

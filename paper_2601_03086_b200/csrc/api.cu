@@ -36,7 +36,7 @@ pfem_status run_cg(const pfem_mesh* m, const pfem_material* mat, const void* u_s
 pfem_status run_tangent_diag(const pfem_mesh* m, const pfem_material* mat, const void* u, const uint8_t* mask,
                              int invert, void* out, cudaStream_t s);
 pfem_status run_heat(const pfem_mesh* m, const void* k, int64_t kstride, int S, const void* Tf, int64_t sstride,
-                     const void* f, void* W, void* totals, void* r, void* ws, cudaStream_t s);
+                     const void* f, void* W, void* totals, void* r, void* ws, int otf, cudaStream_t s);
 size_t heat_ws_bytes(const pfem_mesh* m, int S);
 pfem_status run_pretrain_stage(const pfem_mesh* m, int S, int64_t sstride, const void* H, const void* phi, void* u,
                                int stage, const void* f_ext, void* grad, const void* totals, double* loss,
@@ -259,7 +259,7 @@ size_t pfem_heat_workspace_bytes(const pfem_mesh* m, int32_t n_samples) {
 
 pfem_status pfem_heat(const pfem_mesh* m, const void* k, int64_t k_stride, int32_t n_samples, const void* T,
                       int64_t sample_stride, const void* f_nodal, void* elem_energy, void* totals, void* flux,
-                      void* ws, size_t ws_bytes, void* stream) {
+                      int32_t options, void* ws, size_t ws_bytes, void* stream) {
     pfem_status st = check_mesh(m, false);
     if (st) return st;
     if (!k || !T) { set_error("pfem_heat: k and T are required"); return PFEM_ERR_ARG; }
@@ -272,8 +272,10 @@ pfem_status pfem_heat(const pfem_mesh* m, const void* k, int64_t k_stride, int32
         return PFEM_ERR_CAPACITY;
     }
     if (flux && (!m->csr_ptr || !m->csr_ent)) { set_error("pfem_heat: mesh CSR missing (prepare first)"); return PFEM_ERR_ARG; }
+    if (options & ~PFEM_HEAT_GEOMETRY_ON_THE_FLY) { set_error("pfem_heat: unknown options"); return PFEM_ERR_ARG; }
+    if ((options & PFEM_HEAT_GEOMETRY_ON_THE_FLY) && !m->coords) { set_error("pfem_heat: on-the-fly geometry needs coords"); return PFEM_ERR_ARG; }
     return run_heat(m, k, k_stride, n_samples, T, sample_stride, f_nodal, elem_energy, totals, flux, ws,
-                    (cudaStream_t)stream);
+                    (options & PFEM_HEAT_GEOMETRY_ON_THE_FLY) ? 1 : 0, (cudaStream_t)stream);
 }
 
 pfem_status pfem_residual(const pfem_mesh* m, const pfem_material* mat, int32_t n_samples, const void* u,

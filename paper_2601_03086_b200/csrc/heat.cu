@@ -176,11 +176,44 @@ k_heat_entry_pos(int64_t nnz, const int32_t* __restrict__ csr_ent, int32_t* __re
     for (int64_t q = (int64_t)blockIdx.x * HT_NT + threadIdx.x; q < nnz; q += stride) pos[csr_ent[q]] = (int32_t)q;
 }
 
+// on-the-fly geometry (SURVEY §8(f) row f4 variant): grad N_a (rows of J^-1, J = [X_1 - X_0 | ..])
+// and V = |det J| / d! formed in fp64 from the vertex coordinates (App. B), instead
+// of reading the prepared gradients and volumes: fewer bytes per element, more arithmetic
 template <int D, class T>
+__device__ __forceinline__ void geometry_of(const double* __restrict__ X, const int (&c)[D + 1], T g[D][D], T& V) {
+    double J[D][D];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int a = 0; a < D; ++a) J[i][a] = __ldg(X + (int64_t)c[a + 1] * D + i) - __ldg(X + (int64_t)c[0] * D + i);
+    if constexpr (D == 2) {
+        const double det = J[0][0] * J[1][1] - J[0][1] * J[1][0], r = 1.0 / det;
+        g[0][0] = (T)(J[1][1] * r);  g[0][1] = (T)(-J[0][1] * r);
+        g[1][0] = (T)(-J[1][0] * r); g[1][1] = (T)(J[0][0] * r);
+        V = (T)(fabs(det) * 0.5);
+    } else {
+        double cof[3][3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const int i1 = (i + 1) % 3, i2 = (i + 2) % 3, j1 = (j + 1) % 3, j2 = (j + 2) % 3;
+                cof[i][j] = J[i1][j1] * J[i2][j2] - J[i1][j2] * J[i2][j1];
+            }
+        const double det = J[0][0] * cof[0][0] + J[0][1] * cof[0][1] + J[0][2] * cof[0][2], r = 1.0 / det;
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) g[a][j] = (T)(cof[j][a] * r);   // (J^-1)[a][j] = cof[j][a] / det
+        V = (T)(fabs(det) / 6.0);
+    }
+}
+
+template <int D, class T, bool OTF>
 __global__ void __launch_bounds__(HT_NT)
 k_heat_elem_flux(int E, int S, int s0, int64_t sstride, const int32_t* __restrict__ conn, const T* __restrict__ grad,
-                 const T* __restrict__ vol, const T* __restrict__ k, int64_t kstride, const T* __restrict__ Tf,
-                 const int32_t* __restrict__ pos, T* __restrict__ ebuf, T* __restrict__ W) {
+                 const T* __restrict__ vol, const double* __restrict__ X, const T* __restrict__ k, int64_t kstride,
+                 const T* __restrict__ Tf, const int32_t* __restrict__ pos, T* __restrict__ ebuf, T* __restrict__ W) {
     constexpr int NV = D + 1;
     const int nq = min(HT_SC, S - s0);
     for (int e = blockIdx.x * HT_NT + threadIdx.x; e < E; e += gridDim.x * HT_NT) {
@@ -188,11 +221,17 @@ k_heat_elem_flux(int E, int S, int s0, int64_t sstride, const int32_t* __restric
 #pragma unroll
         for (int a = 0; a < NV; ++a) c[a] = __ldg(conn + (int64_t)e * NV + a);
         T g[D][D];
+        T Ve;
+        if constexpr (OTF) {
+            geometry_of<D, T>(X, c, g, Ve);
+        } else {
 #pragma unroll
-        for (int b = 0; b < D; ++b)
+            for (int b = 0; b < D; ++b)
 #pragma unroll
-            for (int j = 0; j < D; ++j) g[b][j] = __ldg(grad + (int64_t)(b * D + j) * E + e);
-        const T kv = __ldg(k + (int64_t)e * kstride) * __ldg(vol + e);
+                for (int j = 0; j < D; ++j) g[b][j] = __ldg(grad + (int64_t)(b * D + j) * E + e);
+            Ve = __ldg(vol + e);
+        }
+        const T kv = __ldg(k + (int64_t)e * kstride) * Ve;
         T fl[NV][HT_SC];
 #pragma unroll
         for (int sq = 0; sq < HT_SC; ++sq) {
@@ -274,7 +313,7 @@ size_t heat_ec_bytes(const pfem_mesh* m) {
 
 template <int D, class T>
 pfem_status heat_impl(const pfem_mesh* m, const void* k, int64_t kstride, int S, const void* Tf, int64_t sstride,
-                      const void* f, void* W, void* totals, void* r, void* ws, cudaStream_t s) {
+                      const void* f, void* W, void* totals, void* r, void* ws, int otf, cudaStream_t s) {
     double* partial = (double*)ws;
     const int E = m->n_elems, N = m->n_nodes;
     int dev = 0, nsm = 148;
@@ -301,8 +340,14 @@ pfem_status heat_impl(const pfem_mesh* m, const void* k, int64_t kstride, int S,
         const int ge = std::max(1, std::min(16 * nsm, (E + HT_NT - 1) / HT_NT));
         const int gn = std::max(1, std::min(16 * nsm, (N + HT_NT - 1) / HT_NT));
         for (int s0 = 0; s0 < S; s0 += HT_SC) {
-            k_heat_elem_flux<D, T><<<ge, HT_NT, 0, s>>>(E, S, s0, sstride, m->conn, (const T*)m->grad, (const T*)m->vol,
-                                                        (const T*)k, kstride, (const T*)Tf, pos, ebuf, (T*)W);
+            if (otf)
+                k_heat_elem_flux<D, T, true><<<ge, HT_NT, 0, s>>>(E, S, s0, sstride, m->conn, (const T*)m->grad,
+                                                                  (const T*)m->vol, m->coords, (const T*)k, kstride,
+                                                                  (const T*)Tf, pos, ebuf, (T*)W);
+            else
+                k_heat_elem_flux<D, T, false><<<ge, HT_NT, 0, s>>>(E, S, s0, sstride, m->conn, (const T*)m->grad,
+                                                                   (const T*)m->vol, m->coords, (const T*)k, kstride,
+                                                                   (const T*)Tf, pos, ebuf, (T*)W);
             PFEM_LAUNCH_CHECK("k_heat_elem_flux");
             k_heat_node_sum<T><<<gn, HT_NT, 0, s>>>(N, S, s0, sstride, m->csr_ptr, ebuf, (T*)r);
             PFEM_LAUNCH_CHECK("k_heat_node_sum");
@@ -329,12 +374,12 @@ pfem_status heat_impl(const pfem_mesh* m, const void* k, int64_t kstride, int S,
 }
 
 pfem_status run_heat(const pfem_mesh* m, const void* k, int64_t kstride, int S, const void* Tf, int64_t sstride,
-                     const void* f, void* W, void* totals, void* r, void* ws, cudaStream_t s) {
+                     const void* f, void* W, void* totals, void* r, void* ws, int otf, cudaStream_t s) {
     if (m->dim == 2)
-        return m->dtype == PFEM_F32 ? heat_impl<2, float>(m, k, kstride, S, Tf, sstride, f, W, totals, r, ws, s)
-                                    : heat_impl<2, double>(m, k, kstride, S, Tf, sstride, f, W, totals, r, ws, s);
-    return m->dtype == PFEM_F32 ? heat_impl<3, float>(m, k, kstride, S, Tf, sstride, f, W, totals, r, ws, s)
-                                : heat_impl<3, double>(m, k, kstride, S, Tf, sstride, f, W, totals, r, ws, s);
+        return m->dtype == PFEM_F32 ? heat_impl<2, float>(m, k, kstride, S, Tf, sstride, f, W, totals, r, ws, otf, s)
+                                    : heat_impl<2, double>(m, k, kstride, S, Tf, sstride, f, W, totals, r, ws, otf, s);
+    return m->dtype == PFEM_F32 ? heat_impl<3, float>(m, k, kstride, S, Tf, sstride, f, W, totals, r, ws, otf, s)
+                                : heat_impl<3, double>(m, k, kstride, S, Tf, sstride, f, W, totals, r, ws, otf, s);
 }
 
 }  // namespace pfem

@@ -589,6 +589,11 @@ def test_heat_matches_oracle(orc, prob):
     assert rel_l2(W.cpu().numpy(), Wo) < tol
     assert max_rel(tot.cpu().numpy(), toto) < (1e-10 if prob.dtype == "f64" else 1e-4)
     assert rel_l2(r.cpu().numpy(), ro) < tol
+    # geometry formed on the fly from the coordinates (f4 variant): same results within the bar
+    W2, tot2, r2 = pf.heat(mesh, torch.as_tensor(k, dtype=dt, device="cuda"), torch.as_tensor(T, dtype=dt, device="cuda"),
+                           f=torch.as_tensor(f, dtype=dt, device="cuda"), geometry_on_the_fly=True)
+    assert rel_l2(W2.cpu().numpy(), Wo) < tol and rel_l2(r2.cpu().numpy(), ro) < tol
+    assert max_rel(tot2.cpu().numpy(), toto) < (1e-10 if prob.dtype == "f64" else 1e-4)
     # uniform conductivity (stride 0)
     W1, _, r1 = pf.heat(mesh, torch.tensor([1.5], dtype=dt, device="cuda"), torch.as_tensor(T, dtype=dt, device="cuda"))
     Wo1, _, ro1 = om.heat(T, [1.5])
