@@ -484,7 +484,9 @@ __device__ __forceinline__ void stage_fields(T* ust, const unsigned char* rec, u
     }
 }
 
-template <int D, int MODEL, class T, int OP, int ST, bool MASKED, int EB, int NT>
+// FEXT: the call passes f_ext (Pi = W - f.u; the pretraining epilogue); without it the f.u
+// code is compiled out
+template <int D, int MODEL, class T, int OP, int ST, bool MASKED, int EB, int NT, bool FEXT>
 __global__ void __launch_bounds__(NT, PFEM_STAGED_MINB)
 k_assemble(const AsmParams<T> p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -715,7 +717,7 @@ k_assemble(const AsmParams<T> p) {
             // the next block's fields, into the same buffer once every thread's phase-1 reads
             // are done (the barrier before phase 2); its record has had phase 1 to land, and
             // the copies have phase 2 to complete
-            const bool do_p2 = (HAS_FORCE || p.f_ext) && !(PFEM_DBG && (p.dbg & 2));
+            const bool do_p2 = (HAS_FORCE || FEXT) && !(PFEM_DBG && (p.dbg & 2));
             bar_main(NT);   // every thread's phase-1 reads of the field buffer are done
             {
                 if (tn < NI) {
@@ -835,7 +837,7 @@ k_assemble(const AsmParams<T> p) {
                             }
                         }
                     }
-                    if (HAS_PSI && p.f_ext && !(word & OCC_NONOWNER)) {
+                    if (HAS_PSI && FEXT && !(word & OCC_NONOWNER)) {
 #pragma unroll
                         for (int q = 0; q < ST; ++q) {   // (compile-time q: fsum stays in registers)
                             if (q < qs || q >= qs + STH || q >= nq) continue;
@@ -856,7 +858,7 @@ k_assemble(const AsmParams<T> p) {
 #pragma unroll
                 for (int q = 0; q < ST; ++q) {
                     if (q >= nq) break;
-                    const double f2 = p.f_ext ? warp_sum(fsum[q]) : 0.0;
+                    const double f2 = FEXT ? warp_sum(fsum[q]) : 0.0;
                     if (lane == 0) s_red[warp][ST + q] = f2;
                 }
             }

@@ -178,9 +178,12 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
         const size_t smem = 2 * (size_t)(p.rec_end - p.rec_base) + 4 * EB * sizeof(T) +
                             (size_t)NF * p.rec.ocap * D * ST * sizeof(T) +
                             (HAS_FORCE ? (size_t)ST * D * (D + 1) * EB * sizeof(T) : 0);
-        auto kern = k_assemble<D, MODEL, T, OP, ST, MASKED, EB, NT>;
-        static int resident = 0;   // per instantiation: co-resident CTAs (persistent grid)
-        static size_t configured = 0;
+        const int fx = (HAS_PSI && p.f_ext) ? 1 : 0;
+        auto kern = fx ? k_assemble<D, MODEL, T, OP, ST, MASKED, EB, NT, HAS_PSI> : k_assemble<D, MODEL, T, OP, ST, MASKED, EB, NT, false>;
+        static int resident_[2] = {0, 0};   // per instantiation: co-resident CTAs (persistent grid)
+        static size_t configured_[2] = {0, 0};
+        int& resident = resident_[fx];
+        size_t& configured = configured_[fx];
         if (resident == 0 || smem > configured) {
             PFEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             configured = smem;
