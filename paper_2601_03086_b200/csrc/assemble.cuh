@@ -51,6 +51,9 @@
 #ifndef PFEM_STAGED_EPOS
 #define PFEM_STAGED_EPOS 0
 #endif
+#ifndef PFEM_F0_DERIVED
+#define PFEM_F0_DERIVED 0     // vertex-0 forces formed in phase 2 (a quarter less force buffer)
+#endif
 #ifndef PFEM_DBG
 #define PFEM_DBG 0            // compile the PFEM_DEBUG ablation switches into the staged kernel (tools)
 #endif
@@ -457,6 +460,31 @@ __device__ __forceinline__ void sacc_reg(const T (&b)[SD], T (&acc)[SD]) {
     }
 }
 
+// one entry's two-sample force vector from a force buffer without vertex-0 rows (F0D): slot
+// j = a * EB + el; vertex 0 is ((-f1) - f2) - f3 (the order forces() forms it in)
+template <int D, class T, int ST>
+__device__ __forceinline__ void entry_f0d(const T* fbuf, int j, int EB, int SD, int qs, float2 (&x)[D]) {
+    if (j >= EB) {
+        const T* b = fbuf + (size_t)(j - EB) * SD + qs;
+#pragma unroll
+        for (int i = 0; i < D; ++i) x[i] = *reinterpret_cast<const float2*>(b + i * ST);
+    } else {
+        const T* b1 = fbuf + (size_t)j * SD + qs;
+        const size_t step = (size_t)EB * SD;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            const float2 q1 = *reinterpret_cast<const float2*>(b1 + i * ST);
+            F2 s = -F2(q1.x, q1.y);
+#pragma unroll
+            for (int a = 1; a < D; ++a) {
+                const float2 q = *reinterpret_cast<const float2*>(b1 + a * step + i * ST);
+                s = s - F2(q.x, q.y);
+            }
+            x[i] = s.v;
+        }
+    }
+}
+
 template <int D, class T, int NT, int ST, bool MASKED>
 __device__ __forceinline__ void stage_fields(T* ust, const unsigned char* rec, uint32_t base, const T* src,
                                              const AsmParams<T>& p, int s0, int nq, int no) {
@@ -505,6 +533,9 @@ k_assemble(const AsmParams<T> p) {
     constexpr bool EPOS = sizeof(T) == 4 && PFEM_STAGED_EPOS;
     constexpr int HP = (sizeof(T) == 4 && ST == 4 && (D == 3 || PFEM_HP2_2D) && !EPOS && PFEM_STAGED_HP2) ? 2 : 1;   // phase-2 threads per occurrence
     constexpr int STH = ST / HP;
+    // F0D: vertex 0's forces are not stored; phase 2 forms them as ((-f1) - f2) - f3, the same
+    // operations phase 1 used (a quarter less force buffer)
+    constexpr bool F0D = PFEM_F0_DERIVED && HP == 2;
     constexpr int SDH = D * STH;
     const T* staged_src = (OP == OP_TANGENT) ? p.v : p.u;
     // shared layout: rec[2] | mat[2][2][EB] | ust[2][OCAP][D][ST] | fbuf[NV][EB][D][ST]
@@ -513,7 +544,7 @@ k_assemble(const AsmParams<T> p) {
     unsigned char* const stage0 = smem_raw;
     unsigned char* const stage1 = smem_raw + srb;
     T* mstage = reinterpret_cast<T*>(smem_raw + 2 * (size_t)srb);
-    T* ustage = mstage + 4 * EB;
+    T* ustage = mstage + (((p.mat.s0 | p.mat.s1) != 0) ? 4 * EB : 0);   // material stage only if element-wise
     const size_t ust1 = (size_t)p.rec.ocap * D * ST;   // one staged field
     const size_t ust_sz = (size_t)NF * ust1;
     T* fbuf = ustage + ust_sz;
@@ -700,7 +731,8 @@ k_assemble(const AsmParams<T> p) {
                         for (int a = 0; a < NV; ++a)
 #pragma unroll
                             for (int i = 0; i < D; ++i)
-                                *reinterpret_cast<V*>(fbuf + ((size_t)(EPOS ? ep[a] : a * EB + el) * D + i) * ST + qq) = f[a][i];
+                                if (!F0D || a > 0)
+                                    *reinterpret_cast<V*>(fbuf + ((size_t)(EPOS ? ep[a] : (a - (F0D ? 1 : 0)) * EB + el) * D + i) * ST + qq) = f[a][i];
                         if (!HAS_PSI && !isfinite(pfem::lane(f[0][0], 0))) ++n_nonfin;
                     }
                 }
@@ -780,13 +812,18 @@ k_assemble(const AsmParams<T> p) {
 #endif
                             for (; k + 1 < k1; k += 2) {
                                 const int j0 = sle[k], j1 = sle[k + 1];
-                                const T* b0 = fbuf + (size_t)j0 * SD + qs;   // (record loc_ent = slot)
-                                const T* b1 = fbuf + (size_t)j1 * SD + qs;
                                 float2 x0[D], x1[D];
+                                if constexpr (F0D) {
+                                    entry_f0d<D, T, ST>(fbuf, j0, EB, SD, qs, x0);
+                                    entry_f0d<D, T, ST>(fbuf, j1, EB, SD, qs, x1);
+                                } else {
+                                    const T* b0 = fbuf + (size_t)j0 * SD + qs;   // (record loc_ent = slot)
+                                    const T* b1 = fbuf + (size_t)j1 * SD + qs;
 #pragma unroll
-                                for (int i = 0; i < D; ++i) {
-                                    x0[i] = *reinterpret_cast<const float2*>(b0 + i * ST);
-                                    x1[i] = *reinterpret_cast<const float2*>(b1 + i * ST);
+                                    for (int i = 0; i < D; ++i) {
+                                        x0[i] = *reinterpret_cast<const float2*>(b0 + i * ST);
+                                        x1[i] = *reinterpret_cast<const float2*>(b1 + i * ST);
+                                    }
                                 }
 #pragma unroll
                                 for (int i = 0; i < D; ++i) {
@@ -797,12 +834,18 @@ k_assemble(const AsmParams<T> p) {
                             }
                             if (k < k1) {
                                 const int j0 = sle[k];
-                                const T* b0 = fbuf + (size_t)j0 * SD + qs;
+                                float2 x0[D];
+                                if constexpr (F0D) {
+                                    entry_f0d<D, T, ST>(fbuf, j0, EB, SD, qs, x0);
+                                } else {
+                                    const T* b0 = fbuf + (size_t)j0 * SD + qs;
+#pragma unroll
+                                    for (int i = 0; i < D; ++i) x0[i] = *reinterpret_cast<const float2*>(b0 + i * ST);
+                                }
 #pragma unroll
                                 for (int i = 0; i < D; ++i) {
-                                    const float2 x0 = *reinterpret_cast<const float2*>(b0 + i * ST);
                                     F2 a0(accs[2 * i], accs[2 * i + 1]);
-                                    a0 = a0 + F2(x0.x, x0.y);
+                                    a0 = a0 + F2(x0[i].x, x0[i].y);
                                     accs[2 * i] = a0.v.x; accs[2 * i + 1] = a0.v.y;
                                 }
                             }

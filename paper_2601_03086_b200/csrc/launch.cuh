@@ -175,9 +175,12 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
         constexpr bool EPOS = sizeof(T) == 4 && PFEM_STAGED_EPOS;
         p.rec_base = EPOS ? p.rec.ent_pos : p.rec.g;
         p.rec_end = EPOS ? p.rec.loc_ent : p.rec.bytes;
-        const size_t smem = 2 * (size_t)(p.rec_end - p.rec_base) + 4 * EB * sizeof(T) +
+        constexpr bool F0D = PFEM_F0_DERIVED && sizeof(T) == 4 && ST == 4 && (D == 3 || PFEM_HP2_2D) && !EPOS &&
+                             PFEM_STAGED_HP2;   // (the kernel's HP == 2 condition)
+        const size_t smem = 2 * (size_t)(p.rec_end - p.rec_base) +
+                            (((p.mat.s0 | p.mat.s1) != 0) ? 4 * EB * sizeof(T) : 0) +
                             (size_t)NF * p.rec.ocap * D * ST * sizeof(T) +
-                            (HAS_FORCE ? (size_t)ST * D * (D + 1) * EB * sizeof(T) : 0);
+                            (HAS_FORCE ? (size_t)ST * D * (D + 1 - (F0D ? 1 : 0)) * EB * sizeof(T) : 0);
         const int fx = (HAS_PSI && p.f_ext) ? 1 : 0;
         auto kern = fx ? k_assemble<D, MODEL, T, OP, ST, MASKED, EB, NT, HAS_PSI> : k_assemble<D, MODEL, T, OP, ST, MASKED, EB, NT, false>;
         static int resident_[2] = {0, 0};   // per instantiation: co-resident CTAs (persistent grid)
