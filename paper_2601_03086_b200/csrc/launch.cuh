@@ -112,11 +112,14 @@ AsmParams<T> make_params(const Call& c) {
     return p;
 }
 
+#ifndef PFEM_DIRECT_NT64
+#define PFEM_DIRECT_NT64 256
+#endif
 #ifndef PFEM_DIRECT_NT32
 #define PFEM_DIRECT_NT32 128
 #endif
 template <class T>
-constexpr int direct_nt() { return sizeof(T) == 4 ? PFEM_DIRECT_NT32 : 256; }   // direct kernel threads per CTA (measured)
+constexpr int direct_nt() { return sizeof(T) == 4 ? PFEM_DIRECT_NT32 : PFEM_DIRECT_NT64; }   // direct kernel threads per CTA (measured)
 
 template <int D, int MODEL, class T, int OP, int ST, bool MASKED, int NT, bool PERM>
 pfem_status launch_direct(AsmParams<T> p, cudaStream_t s) {
