@@ -14,6 +14,9 @@
  *                  linear: f = int B^T sigma dV (virtual power)
  *   tangent        K = int G0^T S G0 + B0^T C^SE B0 dV0                 (App. B); linear: B^T D B
  *   CG             K U = F, stop on ||K U - F|| / ||F|| < tol            (App. B), warm start U0
+ *   Jacobi PCG     M = diag of the textbook element tangents, textbook PCG (§5.5; reading R27)
+ *   heat           W = 1/2 k |grad T|^2 V, flux = dW/dT                  (Eq. poisson, energy form P:249-284)
+ *   (the Newton iteration and the pretraining loss are compositions of these in oracle.py)
  *
  * Everything in float64, plain loops, IEEE RN, built with -O2 -ffp-contract=off.
  * Element-local work may run in an OpenMP parallel loop writing per-element
