@@ -156,7 +156,8 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
     constexpr int EB = EbOf<D>::value;
     constexpr int NT = PFEM_STAGED_NT;
     constexpr int NF = (OP == OP_TANGENT && MODEL == MODEL_NH) ? 2 : 1;   // staged fields (single buffer)
-    static const int dbg = getenv("PFEM_DEBUG") ? atoi(getenv("PFEM_DEBUG")) : 0;
+    // PFEM_DEBUG ablation switches (incomplete results) exist only in PFEM_DBG=1 builds
+    static const int dbg = (PFEM_DBG && getenv("PFEM_DEBUG")) ? atoi(getenv("PFEM_DEBUG")) : 0;
     static const int variant = getenv("PFEM_VARIANT") ? atoi(getenv("PFEM_VARIANT")) : -1;
     p.dbg = dbg;
     // kernel A form: direct (one CTA per block, small shared memory) for single-sample calls,

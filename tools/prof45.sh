@@ -1,5 +1,6 @@
 #!/bin/bash
-# kernel-A-alone times (PFEM_DEBUG=32) for configs 4 K.v and 5 E+R, plus ncu full captures of both
+# kernel-A-alone times (PFEM_DEBUG=32; needs a PFEM_DBG=1 build: python tools/ab_build.py dbg PFEM_DBG=1,
+# then PFEM_LIB=libpfem_dbg.so) for configs 4 K.v and 5 E+R, plus ncu full captures of both
 cd "$(dirname "$0")/.." || exit 1
 TAG=${1:-x}
 for a in "--config 4 --op kv" "--config 5 --op er"; do
