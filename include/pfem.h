@@ -238,7 +238,10 @@ pfem_status pfem_pretrain_loss(const pfem_mesh* m, const pfem_material* mat, int
  *   totals       nullable [S][n_parts];  flux: nullable [S][N]
  *   ws, ws_bytes per-call workspace (pfem_heat_workspace_bytes): the totals' slice sums and
  *                the fluxes' CSR-ordered entry buffer; may be NULL without totals (the fluxes
- *                then re-form each element per CSR entry, same summation order)
+ *                then re-form each element per CSR entry, same summation order).  The
+ *                workspace caches the CSR entry positions of the prepared mesh it was last
+ *                used with (keyed by the plan; recomputed when the mesh changes); it must be
+ *                ZERO-FILLED before its first use
  * Sums in fixed order (per part: 64 fixed slices, each a CTA tree, then the slices in order;
  * per node: CSR order); asynchronous on `stream`.
  * --------------------------------------------------------------------------------- */

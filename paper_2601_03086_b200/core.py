@@ -247,7 +247,7 @@ def heat(mesh: Mesh, k: torch.Tensor, T: torch.Tensor, f=None, elem_energy=True,
     nb = L.load().pfem_heat_workspace_bytes(mesh.ref(), S)
     ws = mesh._ws.get(("heat", S))
     if ws is None:
-        ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=dev)
+        ws = torch.zeros(max(nb, 1), dtype=torch.uint8, device=dev)   # zero-filled before first use
         mesh._ws[("heat", S)] = ws
     L.check(L.load().pfem_heat(mesh.ref(), _ptr(k), 0 if k.numel() == 1 else 1, S, _ptr(T), T.shape[1], _ptr(f),
                                _ptr(W), _ptr(tot), _ptr(r), 1 if geometry_on_the_fly else 0, _ptr(ws), ws.numel(),

@@ -82,6 +82,7 @@ inline RecLayout rec_layout(int D, size_t tsize, int eb, int ocap, bool with_eid
 }
 
 struct Plan {
+    uint64_t serial = 0;              // unique per prepared plan in this process (workspace caches key on it)
     int32_t dim = 0, n_nodes = 0, n_elems = 0, n_parts = 0;
     int32_t n_blocks = 0, n_occ = 0, eb_max = 0;
     int32_t* blk_elem = nullptr;      // [n_blocks+1] in plan positions (see elem_perm)

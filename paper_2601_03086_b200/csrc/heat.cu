@@ -171,7 +171,9 @@ size_t heat_ws_bytes(const pfem_mesh* m, int S) {
 // then per element the d+1 vertex fluxes of up to HT_SC samples stored at their CSR entries,
 // then each node sums its contiguous entries in CSR order (the same order as k_heat_flux)
 __global__ void __launch_bounds__(HT_NT)
-k_heat_entry_pos(int64_t nnz, const int32_t* __restrict__ csr_ent, int32_t* __restrict__ pos) {
+k_heat_entry_pos(int64_t nnz, const int32_t* __restrict__ csr_ent, int32_t* __restrict__ pos,
+                 const unsigned long long* __restrict__ stamp, unsigned long long key) {
+    if (stamp[0] == key) return;   // this workspace already holds the positions of this plan
     const int64_t stride = (int64_t)gridDim.x * HT_NT;
     for (int64_t q = (int64_t)blockIdx.x * HT_NT + threadIdx.x; q < nnz; q += stride) pos[csr_ent[q]] = (int32_t)q;
 }
@@ -284,8 +286,9 @@ k_heat_elem_flux(int E, int S, int s0, int64_t sstride, const int32_t* __restric
 template <class T>
 __global__ void __launch_bounds__(HT_NT)
 k_heat_node_sum(int N, int S, int s0, int64_t sstride, const int32_t* __restrict__ csr_ptr, const T* __restrict__ ebuf,
-                T* __restrict__ r) {
+                T* __restrict__ r, unsigned long long* __restrict__ stamp, unsigned long long key) {
     const int nq = min(HT_SC, S - s0);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *stamp = key;   // positions complete (previous kernel)
     for (int n = blockIdx.x * HT_NT + threadIdx.x; n < N; n += gridDim.x * HT_NT) {
         T acc[HT_SC];
 #pragma unroll
@@ -308,7 +311,7 @@ k_heat_node_sum(int N, int S, int s0, int64_t sstride, const int32_t* __restrict
 size_t heat_ec_bytes(const pfem_mesh* m) {
     const size_t nnz = (size_t)m->n_elems * (m->dim + 1);
     const size_t ts = m->dtype == PFEM_F64 ? 8 : 4;
-    return ((sizeof(int32_t) * nnz + 255) / 256 * 256) + ts * nnz * HT_SC;
+    return 256 + ((sizeof(int32_t) * nnz + 255) / 256 * 256) + ts * nnz * HT_SC;   // stamp | pos | entries
 }
 
 template <int D, class T>
@@ -330,11 +333,19 @@ pfem_status heat_impl(const pfem_mesh* m, const void* k, int64_t kstride, int S,
     if (ec) {
         // element-centric: per-element vertex fluxes at their CSR entries, node sums in CSR order
         char* w = (char*)ws + ((sizeof(double) * (size_t)S * m->n_parts * HT_SLICES + 255) / 256 * 256);
+        // the CSR entry positions depend only on the mesh: computed once per (workspace, plan)
+        unsigned long long* stamp = (unsigned long long*)w;
+        // (never 0, so a zero-filled workspace always computes them; splitmix64 of the serial)
+        unsigned long long key = reinterpret_cast<const Plan*>(m->plan)->serial + 0x9E3779B97F4A7C15ull;
+        key = (key ^ (key >> 30)) * 0xBF58476D1CE4E5B9ull;
+        key = (key ^ (key >> 27)) * 0x94D049BB133111EBull;
+        key = (key ^ (key >> 31)) | 1ull;
+        w += 256;
         int32_t* pos = (int32_t*)w;
         const int64_t nnz = (int64_t)E * (D + 1);
         T* ebuf = (T*)(w + ((sizeof(int32_t) * (size_t)nnz + 255) / 256 * 256));
         const int gp = (int)std::max<int64_t>(1, std::min<int64_t>(8 * nsm, (nnz + HT_NT - 1) / HT_NT));
-        k_heat_entry_pos<<<gp, HT_NT, 0, s>>>(nnz, m->csr_ent, pos);
+        k_heat_entry_pos<<<gp, HT_NT, 0, s>>>(nnz, m->csr_ent, pos, stamp, key);
         PFEM_LAUNCH_CHECK("k_heat_entry_pos");
         count_launch();
         const int ge = std::max(1, std::min(16 * nsm, (E + HT_NT - 1) / HT_NT));
@@ -349,7 +360,7 @@ pfem_status heat_impl(const pfem_mesh* m, const void* k, int64_t kstride, int S,
                                                                    (const T*)m->vol, m->coords, (const T*)k, kstride,
                                                                    (const T*)Tf, pos, ebuf, (T*)W);
             PFEM_LAUNCH_CHECK("k_heat_elem_flux");
-            k_heat_node_sum<T><<<gn, HT_NT, 0, s>>>(N, S, s0, sstride, m->csr_ptr, ebuf, (T*)r);
+            k_heat_node_sum<T><<<gn, HT_NT, 0, s>>>(N, S, s0, sstride, m->csr_ptr, ebuf, (T*)r, stamp, key);
             PFEM_LAUNCH_CHECK("k_heat_node_sum");
             count_launch(2);
         }

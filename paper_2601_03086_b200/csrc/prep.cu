@@ -5,6 +5,7 @@
 //      + colour-sorted element list (stable radix sort on the colour key)
 //   plan: element blocks, block-local CSR (smem bitonic sort of (node, entry) keys),
 //      node occurrences with ownership / earlier-partial kinds, node-major occurrence list.
+#include <atomic>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -702,6 +703,8 @@ pfem_status prepare_impl(pfem_mesh* m, cudaStream_t s) {
     const int nch = (int)chunk_blk.size() - 1;
 
     Plan* P = new Plan();
+    static std::atomic<uint64_t> plan_serial{0};
+    P->serial = ++plan_serial;
     P->dim = D; P->n_nodes = N; P->n_elems = E; P->n_parts = K;
     P->n_blocks = nb; P->eb_max = eb_max; P->n_chunks = nch;
     // first allocation: everything whose size is known now
