@@ -112,6 +112,9 @@ AsmParams<T> make_params(const Call& c) {
     return p;
 }
 
+#ifndef PFEM_NTB
+#define PFEM_NTB 256
+#endif
 #ifndef PFEM_DIRECT_NT64
 #define PFEM_DIRECT_NT64 256
 #endif
@@ -210,7 +213,7 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
         PFEM_LAUNCH_CHECK("k_assemble");
     }
     // kernel B: finish multi-block nodes + reductions (programmatic dependent launch)
-    constexpr int NTB = 256;
+    constexpr int NTB = PFEM_NTB;   // kernel B threads per CTA
     const int nsc = (p.S + ST - 1) / ST;
     const int n_items = HAS_FORCE ? P_nfix(p) * nsc : 0;
     int gridb = std::max({1, (n_items + NTB - 1) / NTB, 0});
