@@ -618,3 +618,28 @@ def test_staged_items_multi_part_ragged_samples(orc):
         f = rng.standard_normal(coords.shape) * 1e-2
         check_energy(orc, p, "csr", f_ext=f)
         check_tangent(orc, p, "csr")
+
+
+def test_inversion_flags_staged_items():
+    """Inversion counts through the staged (block, sample chunk) items: S = 7 fp32 fields on a
+    small T4 block, two of them inverting element 0 (J <= 0): n_inverted counts every
+    (element, sample) with J <= 0, first_inverted is element 0, and the non-inverted samples'
+    energies stay finite."""
+    import paper_2601_03086_b200 as pf
+    coords, conn = kuhn_cube(4)
+    S = 7
+    u = np.zeros((S,) + coords.shape)
+    c0 = conn[0]
+    for s in (2, 5):   # flatten element 0 through its vertex 1 (beyond the opposite face)
+        d = coords[c0[1]] - coords[c0[0]]
+        u[s, c0[1]] = -2.0 * d
+    p = Problem("inv-staged", 3, coords, conn, "neohookean", "lame", np.array([0.4]), np.array([0.6]), u, "f32")
+    mesh, mat, ut = gpu_problem(p)
+    flags = torch.zeros(4, dtype=torch.int32, device="cuda")
+    tot, W, r = pf.energy(mesh, mat, ut, elem_energy=True, residual=True, flags=flags)
+    torch.cuda.synchronize()
+    f = flags.cpu().numpy()
+    Wn = W.cpu().numpy()
+    bad = ~np.isfinite(Wn)
+    assert f[0] == int(bad.sum()) and f[0] >= 2 and f[1] == 0
+    assert np.all(np.isfinite(Wn[[0, 1, 3, 4, 6]]))
