@@ -240,9 +240,10 @@ def run_gpu(args):
     u_h = ss[0]["u"].cpu().pin_memory()
     v_h = ss[0]["v"].cpu().pin_memory()
     outs_h = [(torch.empty(ss[0]["outs"][0].shape, dtype=torch.float32).pin_memory(),
+               torch.empty(ss[0]["outs"][1].shape, dtype=torch.float32).pin_memory(),
                torch.empty(ss[0]["u"].shape, dtype=torch.float32).pin_memory(),
                torch.empty(ss[0]["u"].shape, dtype=torch.float32).pin_memory()) for _ in range(2)]
-    tot_h, r_h, kv_h = outs_h[0]
+    tot_h, w_h, r_h, kv_h = outs_h[0]
     Ke = max(5, min(50, K // 10))
     cur = torch.cuda.current_stream()
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
@@ -267,8 +268,9 @@ def run_gpu(args):
         ev_used[i].record(cur)
         with torch.cuda.stream(s_out):
             s_out.wait_event(ev_used[i])
-            th, rh, kh = outs_h[i]
+            th, wh, rh, kh = outs_h[i]
             th.copy_(sti["outs"][0], non_blocking=True)
+            wh.copy_(sti["outs"][1], non_blocking=True)
             rh.copy_(sti["outs"][2], non_blocking=True)
             kh.copy_(sti["Kv"], non_blocking=True)
             ev_back[i].record(s_out)
@@ -295,7 +297,8 @@ def run_gpu(args):
         e2e_ms = float(t.item())
     e2e = {"value": world * E * S / (e2e_ms * 1e-3), "unit": UNIT,
            "h2d_bytes_per_step": int(u_h.numel() * 4 + v_h.numel() * 4),
-           "d2h_bytes_per_step": int(tot_h.numel() * 4 + r_h.numel() * 4 + kv_h.numel() * 4),
+           "d2h_bytes_per_step": int((tot_h.numel() + w_h.numel() + r_h.numel() + kv_h.numel()) * 4),
+           "d2h_tensors": "totals [S,1], W_e [S,E], residual [S,N,3], K(u)v [S,N,3]",
            "ms_per_step": e2e_ms, "overlap": "H2D / compute / D2H on 3 streams, 2 buffer sets"}
 
     extras = {}
@@ -304,6 +307,17 @@ def run_gpu(args):
         torch.cuda.empty_cache()
         extras = run_extras(torch, pf, dev, peak)
         extras["config3_prepare_s"] = prep_s
+    # every kernel the north star grades (>= 60% of the HBM roofline on the >= 1M-element
+    # configs), in the line itself so the driver's parse keeps them
+    graded = {"config3_energy_residual": {"us": roofline["avg_launch_us"], "frac": roofline["frac"],
+                                          "algorithmic_bytes": B_er},
+              "config3_Kv": {"us": roofline["tangent"]["avg_launch_us"], "frac": roofline["tangent"]["frac"],
+                             "algorithmic_bytes": B_tg}}
+    for k in ("config4_Kv", "config5_energy_residual"):
+        if k in extras:
+            graded[k] = {"us": extras[k]["us"], "frac": extras[k]["frac"],
+                         "algorithmic_bytes": extras[k]["algorithmic_bytes"]}
+    roofline["graded"] = graded
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -417,20 +431,31 @@ def run_extras(torch, pf, dev, peak):
     p5 = config5()
     E5, N5 = p5.n_elems, p5.n_nodes
     pe, pn = p5.parts()
-    m5 = pf.Mesh(torch.as_tensor(p5.coords, device=dev), torch.as_tensor(p5.conn, device=dev), dtype=torch.float32,
-                 part_elem=pe, part_node=pn)
-    mat5 = pf.Material("neohookean", "lame", torch.as_tensor(p5.p0, dtype=torch.float32, device=dev),
-                       torch.as_tensor(p5.p1, dtype=torch.float32, device=dev))
-    u5 = torch.as_tensor(p5.u, dtype=torch.float32, device=dev)
-    outs = (torch.empty((1, 64), dtype=torch.float32, device=dev), torch.empty((1, E5), dtype=torch.float32, device=dev),
-            torch.empty_like(u5))
-    for _ in range(5):
-        pf.energy(m5, mat5, u5, elem_energy=True, residual=True, out=outs)
-    t5 = time_events(torch, lambda: pf.energy(m5, mat5, u5, elem_energy=True, residual=True, out=outs), 50)
+    c5 = []
+    for _ in range(N_COPIES):   # rotating copies (~0.4 GB): every call reads HBM, not L2 (§8(d4))
+        m5 = pf.Mesh(torch.as_tensor(p5.coords, device=dev), torch.as_tensor(p5.conn, device=dev),
+                     dtype=torch.float32, part_elem=pe, part_node=pn)
+        mat5 = pf.Material("neohookean", "lame", torch.as_tensor(p5.p0, dtype=torch.float32, device=dev),
+                           torch.as_tensor(p5.p1, dtype=torch.float32, device=dev))
+        u5 = torch.as_tensor(p5.u, dtype=torch.float32, device=dev)
+        outs = (torch.empty((1, 64), dtype=torch.float32, device=dev),
+                torch.empty((1, E5), dtype=torch.float32, device=dev), torch.empty_like(u5))
+        c5.append((m5, mat5, u5, outs))
+    i5 = [0]
+
+    def c5_call():
+        m5_, mat5_, u5_, o5_ = c5[i5[0] % N_COPIES]
+        pf.energy(m5_, mat5_, u5_, elem_energy=True, residual=True, out=o5_)
+        i5[0] += 1
+    for _ in range(6):
+        c5_call()
+    t5 = time_events(torch, c5_call, 60)
     B5 = bytes_energy_residual(E5, N5, 2, 1, 4, mat_per_elem=2, K=64)
     ex["config5_energy_residual"] = {"E": E5, "us": t5 * 1e3, "algorithmic_bytes": B5,
                                      "GBps": B5 / (t5 * 1e-3) / 1e9, "frac": B5 / (t5 * 1e-3) / 1e9 / peak,
-                                     "note": "timed back-to-back on one copy: partly L2-resident (upper bound)"}
+                                     "elements_per_s": E5 / (t5 * 1e-3),
+                                     "l2": f"{N_COPIES} rotating copies (inputs > L2)"}
+    m5, mat5, u5, outs = c5[0]
     # §8(f) f2: the pretraining loss of the 64-sample batch through the hard-BC ansatz
     # u = phi (.) H, phi = distance to each plate's left edge / plate width (R28)
     phi5 = np.empty((N5, 2))
@@ -448,7 +473,7 @@ def run_extras(torch, pf, dev, peak):
                                    "loss": float(pl_out[0]),
                                    "launches": "ansatz + fused energy/residual with the gradient epilogue in its writes and the loss in kernel B's last CTA",
                                    "note": "timed back-to-back on one copy (partly L2-resident)"}
-    del m5, outs
+    del m5, outs, c5
     torch.cuda.empty_cache()
     # ---------------- configs 1 and 2 (BASELINE configs[0], configs[1]): latency of the tiny
     # case; config 2 fused E+R over 32 fields in fp32 and fp64 (3 rotating copies > L2)
@@ -583,12 +608,37 @@ def cpu_baseline(prob, samples=1):
     oms.tangent(v, u=u)
     dt1 = time.perf_counter() - t0
     oracle.set_threads(0)
+    cg = cpu_cg_config4(oracle)
     return {"value": prob.n_elems * samples / dt, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
+            "cg_config4": cg,
             "sample": f"config 3, {samples} of {prob.n_samples} fields, full mesh ({prob.n_elems} tets): "
                       f"energy + residual + tangent, fp64, {dt:.1f} s",
             "single_thread": {"value": sub.n_elems * samples / dt1, "unit": UNIT, "cores": 1,
                               "sample": f"leading {sub.n_elems} tets of config 3, 1 field, {dt1:.1f} s"},
             "cpu_model": cpu_model()}
+
+
+def cpu_cg_config4(oracle, n_timed=20):
+    """The oracle CG on config 4: 20 iterations timed on all host cores, the
+    time to tolerance extrapolated with the oracle's own iteration counts to 1e-8 (zero and
+    warm start, tests/golden/config4_cg.json, written by an oracle-only script)."""
+    from pfem_gen import config4
+    p4 = config4()
+    om = oracle.prepare_problem(p4)
+    t0 = time.perf_counter()
+    _, rep = om.cg(p4.f_ext, p4.mask, np.zeros_like(p4.f_ext), tol=1e-30, max_iter=n_timed, history=False)
+    dt = time.perf_counter() - t0
+    per_it = dt / (n_timed + 3)   # + r0, the lifted rhs and the final true-residual products
+    out = {"timed_iterations": n_timed, "seconds": dt, "seconds_per_iteration": per_it, "cores": cpu_cores(),
+           "method": "extrapolated from 20 timed iterations x the oracle's iteration count"}
+    gp = os.path.join(ROOT, "tests", "golden", "config4_cg.json")
+    if os.path.exists(gp):
+        with open(gp) as fh:
+            g = json.load(fh)
+        for start in ("zero", "warm"):
+            k = g[start]["runs"]["0"]["iterations"]
+            out[start] = {"iterations": k, "time_to_tol_s": k * per_it}
+    return out
 
 
 def gpu_info(torch):
@@ -674,6 +724,19 @@ def main():
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # --gpus N without a launcher: start N ranks ourselves (one process per GPU, torchrun,
+        # rendezvous on 127.0.0.1) and return rank 0's exit status
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
+    if args.gpus != world:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args)
         return

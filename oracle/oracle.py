@@ -34,9 +34,11 @@ class OracleError(RuntimeError):
 def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (-O2 -ffp-contract=off: no FMA contraction, plain)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = f"{_LIB}.{os.getpid()}.tmp"
         cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-shared",
-               "-fPIC", "-std=c11", "-o", _LIB, _SRC, "-lm"]
+               "-fPIC", "-std=c11", "-o", tmp, _SRC, "-lm"]
         subprocess.check_call(cmd)
+        os.replace(tmp, _LIB)   # atomic: a process that has the old library mapped keeps it
     return _LIB
 
 
@@ -75,6 +77,21 @@ I64 = C.c_int64
 def set_threads(n: int = 0):
     """OpenMP threads of the oracle (0 = all); results do not depend on it."""
     lib().oracle_set_threads(C.c_int(n))
+
+
+def set_tangent_form(form: int = 0):
+    """Association of the element tangent product: 0 = B^T (D (B v)), 1 = formed K_e then K_e v."""
+    lib().oracle_set_tangent_form(C.c_int(form))
+
+
+def dot(a, b, order: int = 0) -> float:
+    """The CG dot product of the oracle under order 0 (ascending), 1 (descending), 2 (pairwise),
+    3 (1024-blocked) or 4 (Kahan) — reading R18's orders."""
+    a = _f64(a).ravel()
+    b = _f64(b).ravel()
+    f = lib().oracle_dot
+    f.restype = C.c_double
+    return float(f(C.c_int(order), I64(len(a)), _p(a), _p(b)))
 
 
 def lame(kind: str, p0, p1, n: int):
@@ -295,8 +312,10 @@ class Mesh:
         _check(st, "tangent_diag")
         return d.reshape(self.n_nodes, self.dim)
 
-    def pcg(self, f, mask, x0, tol=1e-8, max_iter=50000, u_state=None, precond=1, history=True):
-        """Jacobi-preconditioned CG (reading R27), same stop test as cg(); precond=0 is plain CG."""
+    def pcg(self, f, mask, x0, tol=1e-8, max_iter=50000, u_state=None, precond=1, history=True, dot_order=0):
+        """Jacobi-preconditioned CG (reading R27), same stop test as cg(); precond=0 is plain CG.
+        dot_order as in cg() (reading R18)."""
+        lib().oracle_set_dot_order(C.c_int(dot_order))
         x = _f64(x0).copy().reshape(-1)
         f = _f64(f).reshape(-1)
         m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8).reshape(-1)
@@ -310,12 +329,30 @@ class Mesh:
         rep = {"status": st, "iterations": it.value, "converged": st == OK, "rel_res0": r0.value,
                "rel_res_final": rf.value, "true_rel_res_final": tr.value,
                "history": None if hist is None else hist[: it.value + 1].copy()}
+        lib().oracle_set_dot_order(C.c_int(0))
         return x.reshape(np.shape(x0)), rep
 
-    def cg_spread(self, f, mask, x0, tol=1e-8, max_iter=50000, u_state=None):
-        """Iteration counts of the oracle CG under the five dot-product orders (R18)."""
-        return [self.cg(f, mask, x0, tol, max_iter, u_state, history=False, dot_order=o)[1]["iterations"]
-                for o in (0, 1, 2, 3, 4)]
+    def pcg_spread(self, f, mask, x0, tol=1e-8, max_iter=50000, u_state=None, forms=(0, 1)):
+        """Iteration counts of the oracle Jacobi PCG under the five dot-product orders and both
+        tangent associations (R18)."""
+        out = []
+        for form in forms:
+            set_tangent_form(form)
+            out += [self.pcg(f, mask, x0, tol, max_iter, u_state, history=False, dot_order=o)[1]["iterations"]
+                    for o in (0, 1, 2, 3, 4)]
+        set_tangent_form(0)
+        return out
+
+    def cg_spread(self, f, mask, x0, tol=1e-8, max_iter=50000, u_state=None, forms=(0, 1)):
+        """Iteration counts of the oracle CG under the five dot-product orders and both
+        associations of the element tangent product (reading R18: valid re-orderings)."""
+        out = []
+        for form in forms:
+            set_tangent_form(form)
+            out += [self.cg(f, mask, x0, tol, max_iter, u_state, history=False, dot_order=o)[1]["iterations"]
+                    for o in (0, 1, 2, 3, 4)]
+        set_tangent_form(0)
+        return out
 
 
 def prepare(coords, conn, model: str, param_kind: str, p0, p1, part_elem=None, part_node=None) -> Mesh:

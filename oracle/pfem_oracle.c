@@ -302,7 +302,15 @@ static int nh_state(int dim, double F[3][3], double mu, double lam, double S[3][
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j) Fd[i][j] = F[i][j];
     double J = dim == 2 ? (Fd[0][0] * Fd[1][1] - Fd[0][1] * Fd[1][0]) : det3(Fd);
-    if (!(J > 0.0)) return OR_ERR_INVERTED;
+    if (!(J > 0.0)) {
+        /* inverted element (reading R3): every output is NaN, never left uninitialised */
+        for (int I = 0; I < 3; ++I)
+            for (int Jx = 0; Jx < 3; ++Jx) S[I][Jx] = Ci[I][Jx] = NAN;
+        *J_out = J;
+        *lnJ_out = NAN;
+        *psi_out = NAN;
+        return OR_ERR_INVERTED;
+    }
     double lnJ = log(J);
     double I1 = 0.0;
     for (int i = 0; i < dim; ++i) I1 += C[i][i];
@@ -450,30 +458,25 @@ int oracle_residual(int dim, int64_t n_nodes, int64_t n_elems, const int32_t* co
 /* Element tangent matrix K_e (ne x ne, row/col index a*d + i):          */
 /*  linear: V B^T D B;  NH: V (G0^T S G0 + B0^T C^SE B0)  */
 /* ------------------------------------------------------------------ */
-static int elem_tangent(int dim, int model, double g[4][3], double V, double mu, double lam,
-                        const int32_t* c, const double* us, double K[12][12]) {
-    const int nv = dim + 1, ne = nv * dim;
-    memset(K, 0, sizeof(double) * 144);
+/* The factors of the element tangent: strain-displacement matrix B (linear: Voigt B; NH: B0(F)),
+ * material matrix D (linear: Voigt D; NH: C^SE in Voigt form) and, for NH, the second
+ * Piola-Kirchhoff stress S of the geometric term (zero for linear).  Returns the status of the
+ * NH state (OR_ERR_INVERTED for J <= 0, all factors NaN). */
+static int tangent_factors(int dim, int model, double g[4][3], double mu, double lam, const int32_t* c,
+                           const double* us, double B[6][12], double D[6][6], double S[3][3], int* nvo_out) {
+    const int nv = dim + 1;
     if (model == OR_LINEAR) {
-        double B[6][12], D[6][6];
-        int nvo = voigt_B(dim, g, B);
+        *nvo_out = voigt_B(dim, g, B);
         voigt_D(dim, mu, lam, D);
-        for (int p = 0; p < ne; ++p)
-            for (int q = 0; q < ne; ++q) {
-                double acc = 0.0;
-                for (int x = 0; x < nvo; ++x)
-                    for (int y = 0; y < nvo; ++y) acc += B[x][p] * D[x][y] * B[y][q];
-                K[p][q] = V * acc;
-            }
+        memset(S, 0, sizeof(double) * 9);
         return OR_OK;
     }
-    double F[3][3], S[3][3], Ci[3][3], J, lnJ, psi;
+    double F[3][3], Ci[3][3], J, lnJ, psi;
     elem_F(dim, c, us, g, F);
     int st = nh_state(dim, F, mu, lam, S, Ci, &J, &lnJ, &psi);
     const int nvo = dim == 2 ? 3 : 6;
     const int (*VI)[2] = dim == 2 ? VI2 : VI3;
     /* C^SE in Voigt form (engineering shear for strains) */
-    double D[6][6];
     for (int x = 0; x < nvo; ++x)
         for (int y = 0; y < nvo; ++y) {
             int I = VI[x][0], Jx = VI[x][1], K2 = VI[y][0], L = VI[y][1];
@@ -481,24 +484,35 @@ static int elem_tangent(int dim, int model, double g[4][3], double V, double mu,
         }
     /* B0: delta E (Voigt, engineering shear) = B0 delta u;
      * dE_KL = 1/2 (F_iK dN_a/dX_L + F_iL dN_a/dX_K) du_ia, shear rows doubled. */
-    double B0[6][12];
-    memset(B0, 0, sizeof(B0));
+    memset(B, 0, sizeof(double) * 6 * 12);
     for (int x = 0; x < nvo; ++x) {
         int Kk = VI[x][0], L = VI[x][1];
         for (int a = 0; a < nv; ++a)
             for (int i = 0; i < dim; ++i) {
                 double v = (Kk == L) ? F[i][Kk] * g[a][L]
                                      : F[i][Kk] * g[a][L] + F[i][L] * g[a][Kk];
-                B0[x][a * dim + i] = v;
+                B[x][a * dim + i] = v;
             }
     }
+    *nvo_out = nvo;
+    return st;
+}
+
+static int elem_tangent(int dim, int model, double g[4][3], double V, double mu, double lam,
+                        const int32_t* c, const double* us, double K[12][12]) {
+    const int nv = dim + 1, ne = nv * dim;
+    double B[6][12], D[6][6], S[3][3];
+    int nvo = 0;
+    int st = tangent_factors(dim, model, g, mu, lam, c, us, B, D, S, &nvo);
+    memset(K, 0, sizeof(double) * 144);
     for (int p = 0; p < ne; ++p)
         for (int q = 0; q < ne; ++q) {
             double acc = 0.0;
             for (int x = 0; x < nvo; ++x)
-                for (int y = 0; y < nvo; ++y) acc += B0[x][p] * D[x][y] * B0[y][q];
+                for (int y = 0; y < nvo; ++y) acc += B[x][p] * D[x][y] * B[y][q];
             K[p][q] = V * acc;
         }
+    if (model == OR_LINEAR) return st;
     /* geometric: K_geo[(a,i),(b,j)] = delta_ij grad N_a . S . grad N_b */
     for (int a = 0; a < nv; ++a)
         for (int b = 0; b < nv; ++b) {
@@ -509,6 +523,47 @@ static int elem_tangent(int dim, int model, double g[4][3], double V, double mu,
         }
     return st;
 }
+
+/* K_e v_e without forming K_e: the same product V (B^T D B + G0^T S G0) v_e evaluated right to
+ * left, B^T (D (B v_e)) (reading R30: the association order of the matrix chain) */
+static int elem_tangent_apply(int dim, int model, double g[4][3], double V, double mu, double lam,
+                              const int32_t* c, const double* us, const double* ve, double* out) {
+    const int nv = dim + 1, ne = nv * dim;
+    double B[6][12], D[6][6], S[3][3], eps[6], sig[6];
+    int nvo = 0;
+    int st = tangent_factors(dim, model, g, mu, lam, c, us, B, D, S, &nvo);
+    for (int x = 0; x < nvo; ++x) {
+        double acc = 0.0;
+        for (int q = 0; q < ne; ++q) acc += B[x][q] * ve[q];
+        eps[x] = acc;
+    }
+    for (int x = 0; x < nvo; ++x) {
+        double acc = 0.0;
+        for (int y = 0; y < nvo; ++y) acc += D[x][y] * eps[y];
+        sig[x] = acc;
+    }
+    for (int p = 0; p < ne; ++p) {
+        double acc = 0.0;
+        for (int x = 0; x < nvo; ++x) acc += B[x][p] * sig[x];
+        out[p] = V * acc;
+    }
+    if (model == OR_LINEAR) return st;
+    /* geometric: (K_geo v)_(a,i) = sum_b (grad N_a . S . grad N_b) v_(b,i) */
+    for (int a = 0; a < nv; ++a)
+        for (int b = 0; b < nv; ++b) {
+            double gsg = 0.0;
+            for (int k = 0; k < dim; ++k)
+                for (int l = 0; l < dim; ++l) gsg += g[a][k] * S[k][l] * g[b][l];
+            for (int i = 0; i < dim; ++i) out[a * dim + i] += V * gsg * ve[b * dim + i];
+        }
+    return st;
+}
+
+/* association of the element product: 0 = B^T (D (B v_e)) (default), 1 = (B^T D B) v_e with the
+ * element matrix formed first.  Form 1 exists only to widen the oracle's own CG iteration-count
+ * spread over valid orderings of the same sums (reading R18). */
+static int g_tangent_form = 0;
+void oracle_set_tangent_form(int form) { g_tangent_form = form; }
 
 /* ------------------------------------------------------------------ */
 /* Matrix-free tangent apply with optional Dirichlet mask (reading R9):  */
@@ -529,22 +584,30 @@ int oracle_tangent(int dim, int64_t n_nodes, int64_t n_elems, const int32_t* con
         double* out = Kv + (int64_t)s * n_nodes * dim;
 #pragma omp parallel for schedule(static)
         for (int64_t e = 0; e < n_elems; ++e) {
-            double g[4][3], K[12][12], ve[12];
+            double g[4][3], ve[12];
             elem_grads(dim, grad, e, g);
             const int32_t* c = conn + e * nv;
-            if (elem_tangent(dim, model, g, vol[e], mu[e], lam[e], c, us, K) != OR_OK) {
-#pragma omp critical
-                { if (first_bad < 0 || e < first_bad) first_bad = e; }
-            }
             for (int a = 0; a < nv; ++a)
                 for (int i = 0; i < dim; ++i) {
                     int64_t dof = (int64_t)c[a] * dim + i;
                     ve[a * dim + i] = (mask && mask[dof]) ? 0.0 : vs[dof];
                 }
-            for (int p = 0; p < ne; ++p) {
-                double acc = 0.0;
-                for (int q = 0; q < ne; ++q) acc += K[p][q] * ve[q];
-                fe[e * ne + p] = acc;
+            int est;
+            if (g_tangent_form == 1) {
+                /* formed element matrix, then K_e v_e (the other association of the same chain) */
+                double K[12][12];
+                est = elem_tangent(dim, model, g, vol[e], mu[e], lam[e], c, us, K);
+                for (int p = 0; p < ne; ++p) {
+                    double acc = 0.0;
+                    for (int q = 0; q < ne; ++q) acc += K[p][q] * ve[q];
+                    fe[e * ne + p] = acc;
+                }
+            } else {
+                est = elem_tangent_apply(dim, model, g, vol[e], mu[e], lam[e], c, us, ve, fe + e * ne);
+            }
+            if (est != OR_OK) {
+#pragma omp critical
+                { if (first_bad < 0 || e < first_bad) first_bad = e; }
             }
         }
         for (int64_t k = 0; k < n_nodes * dim; ++k) out[k] = 0.0;
@@ -614,6 +677,16 @@ static double dot(int64_t n, const double* a, const double* b) {
 }
 
 void oracle_set_dot_order(int order) { g_dot_order = order; }
+
+/* one dot product under a given order (exported so the orders can be pinned against an exact
+ * dot product: tests/test_oracle_pins.py) */
+double oracle_dot(int order, int64_t n, const double* a, const double* b) {
+    const int saved = g_dot_order;
+    g_dot_order = order;
+    const double s = dot(n, a, b);
+    g_dot_order = saved;
+    return s;
+}
 
 int oracle_cg(int dim, int64_t n_nodes, int64_t n_elems, const int32_t* conn, const double* grad,
               const double* vol, int model, const double* mu, const double* lam,

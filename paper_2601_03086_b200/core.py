@@ -238,6 +238,18 @@ def heat(mesh: Mesh, k: torch.Tensor, T: torch.Tensor, f=None, elem_energy=True,
     """pfem_heat: steady heat conduction on the prepared mesh.  T: [S, N] (or [N]); k: per element
     or numel 1.  Returns (W_e [S, E] or None, totals [S, K] or None, flux [S, N] or None)."""
     _require_cuda(T, k)
+    if T.dtype != mesh.dtype or k.dtype != mesh.dtype or (f is not None and f.dtype != mesh.dtype):
+        raise TypeError(f"heat: T, k and f must have the mesh dtype {mesh.dtype}")
+    if k.numel() not in (1, mesh.n_elems):
+        raise ValueError(f"heat: k must have 1 or n_elems = {mesh.n_elems} entries, got {k.numel()}")
+    if T.numel() % mesh.n_nodes != 0:
+        raise ValueError("heat: T must be [S, n_nodes] or [n_nodes]")
+    if f is not None:
+        if f.numel() != mesh.n_nodes:
+            raise ValueError(f"heat: f must have n_nodes = {mesh.n_nodes} entries")
+        _require_cuda(f)
+        f = f.contiguous()
+    k = k.contiguous()
     T = T.reshape(-1, mesh.n_nodes).contiguous()
     S = T.shape[0]
     dev = T.device

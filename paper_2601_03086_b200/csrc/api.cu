@@ -253,14 +253,14 @@ pfem_status pfem_pretrain_loss(const pfem_mesh* m, const pfem_material* mat, int
 }
 
 size_t pfem_heat_workspace_bytes(const pfem_mesh* m, int32_t n_samples) {
-    if (check_mesh(m, false) != PFEM_OK || n_samples <= 0) return 0;
+    if (check_mesh(m, true) != PFEM_OK || n_samples <= 0) return 0;
     return heat_ws_bytes(m, n_samples);
 }
 
 pfem_status pfem_heat(const pfem_mesh* m, const void* k, int64_t k_stride, int32_t n_samples, const void* T,
                       int64_t sample_stride, const void* f_nodal, void* elem_energy, void* totals, void* flux,
                       int32_t options, void* ws, size_t ws_bytes, void* stream) {
-    pfem_status st = check_mesh(m, false);
+    pfem_status st = check_mesh(m, true);   // runs on the prepared mesh (the flux path reads the plan)
     if (st) return st;
     if (!k || !T) { set_error("pfem_heat: k and T are required"); return PFEM_ERR_ARG; }
     if (k_stride < 0) { set_error("pfem_heat: negative k_stride"); return PFEM_ERR_ARG; }

@@ -134,10 +134,7 @@ struct AsmParams {
     const unsigned char* recs;
     // workspace
     Counters* ctr;
-    int32_t* flag;         // [n_blocks]
     double* blk_sum;       // [2S+2][n_blocks]: W_s, f.u_s, dot(main), dot(fix-up)
-    int32_t* fix_flag;     // [n_blocks] fix-up of block done (CG dot)
-    int32_t* chunk_flag;   // [n_chunks] chunk reduced
     double* chunk_sum;     // [2S+1][n_chunks]
     int32_t* part_cnt;     // [K] reduced chunks per part (0 at rest)
     T* partial;            // [n_occ][S][D]

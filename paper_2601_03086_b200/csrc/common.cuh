@@ -125,8 +125,10 @@ struct Plan {
 };
 
 // ------------------------------------------------------------------ workspace layout
-// [ Counters | blk_flag[n_blocks] | fix_flag[n_blocks] | blk_sum[2S+2][n_blocks] (double) | chunk_flag[n_chunks] |
-//   chunk_sum[2S+1][n_chunks] (double) | partial[n_occ][S][d] (T) | colour-mode W [S][E] (T) ]
+// [ Counters | part_cnt[n_parts] | blk_sum[2S+2][n_blocks] (double) | chunk_sum[2S+1][n_chunks] (double) |
+//   partial[n_seg][S][d] (T) | colour-mode W [S][E] (T) ]
+// The zero-at-rest counters (Counters, part_cnt) sit at offsets that depend only on the plan, so
+// one workspace sized for the largest sample count may serve calls with any S.
 struct Counters {
     int32_t ticket;
     int32_t done;
@@ -140,7 +142,7 @@ struct Counters {
 };
 
 struct WsLayout {
-    size_t counters, flags, fix_flags, blk_sum, chunk_flags, chunk_sum, partial, wtmp, part_cnt, total;
+    size_t counters, part_cnt, blk_sum, chunk_sum, partial, wtmp, total;
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -149,14 +151,11 @@ inline WsLayout ws_layout(const Plan& p, int S, size_t tsize) {
     WsLayout L;
     size_t o = 0;
     L.counters = o; o += align_up(sizeof(Counters), 256);
-    L.flags = o;    o += align_up(sizeof(int32_t) * (size_t)(p.n_blocks + 1), 256);
-    L.fix_flags = o; o += align_up(sizeof(int32_t) * (size_t)(p.n_blocks + 1), 256);
+    L.part_cnt = o; o += align_up(sizeof(int32_t) * (size_t)(p.n_parts + 1), 256);   // reduced chunks per part
     L.blk_sum = o;  o += align_up(sizeof(double) * (2 * (size_t)S + 2) * (p.n_blocks + 1), 256);
-    L.chunk_flags = o; o += align_up(sizeof(int32_t) * (size_t)(p.n_chunks + 1), 256);
     L.chunk_sum = o;  o += align_up(sizeof(double) * (2 * (size_t)S + 1) * (p.n_chunks + 1), 256);
     L.partial = o;  o += align_up(tsize * (size_t)S * std::max(p.n_seg, 1) * p.dim, 256);
     L.wtmp = o;     o += align_up(tsize * (size_t)S * p.n_elems, 256);
-    L.part_cnt = o; o += align_up(sizeof(int32_t) * (size_t)(p.n_parts + 1), 256);   // reduced chunks per part
     L.total = o;
     return L;
 }

@@ -163,8 +163,10 @@ k_heat_flux(int N, int E, int S, int64_t sstride, const int32_t* __restrict__ cs
 }
 
 size_t heat_ec_bytes(const pfem_mesh* m);
+// workspace: [ stamp | pos | entry buffer ] at offset 0 (their offsets depend only on the mesh,
+// so one workspace may serve calls with different sample counts) | slice partials [S][K][slices]
 size_t heat_ws_bytes(const pfem_mesh* m, int S) {
-    return ((sizeof(double) * (size_t)S * m->n_parts * HT_SLICES + 255) / 256 * 256) + heat_ec_bytes(m);
+    return heat_ec_bytes(m) + ((sizeof(double) * (size_t)S * m->n_parts * HT_SLICES + 255) / 256 * 256);
 }
 
 // element-centric flux path (HT_EC): entry position of every (element, vertex) in the CSR,
@@ -317,7 +319,7 @@ size_t heat_ec_bytes(const pfem_mesh* m) {
 template <int D, class T>
 pfem_status heat_impl(const pfem_mesh* m, const void* k, int64_t kstride, int S, const void* Tf, int64_t sstride,
                       const void* f, void* W, void* totals, void* r, void* ws, int otf, cudaStream_t s) {
-    double* partial = (double*)ws;
+    double* partial = ws ? (double*)((char*)ws + heat_ec_bytes(m)) : nullptr;
     const int E = m->n_elems, N = m->n_nodes;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
@@ -332,7 +334,7 @@ pfem_status heat_impl(const pfem_mesh* m, const void* k, int64_t kstride, int S,
     }
     if (ec) {
         // element-centric: per-element vertex fluxes at their CSR entries, node sums in CSR order
-        char* w = (char*)ws + ((sizeof(double) * (size_t)S * m->n_parts * HT_SLICES + 255) / 256 * 256);
+        char* w = (char*)ws;   // fixed offset 0, independent of S
         // the CSR entry positions depend only on the mesh: computed once per (workspace, plan)
         unsigned long long* stamp = (unsigned long long*)w;
         // (never 0, so a zero-filled workspace always computes them; splitmix64 of the serial)

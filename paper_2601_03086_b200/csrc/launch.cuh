@@ -95,10 +95,7 @@ AsmParams<T> make_params(const Call& c) {
     const WsLayout L = ws_layout(P, c.S, sizeof(T));
     char* w = (char*)c.ws;
     p.ctr = (Counters*)(w + L.counters);
-    p.flag = (int32_t*)(w + L.flags);
     p.blk_sum = (double*)(w + L.blk_sum);
-    p.fix_flag = (int32_t*)(w + L.fix_flags);
-    p.chunk_flag = (int32_t*)(w + L.chunk_flags);
     p.chunk_sum = (double*)(w + L.chunk_sum);
     p.partial = (T*)(w + L.partial);
     p.part_cnt = (int32_t*)(w + L.part_cnt);

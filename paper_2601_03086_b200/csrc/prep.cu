@@ -153,7 +153,8 @@ __global__ void k_colour_greedy(int nv, int E, const int32_t* __restrict__ conn,
                     k = -1;
                 }
                 if (!blocked) {
-                    int c = (~used0) ? __ffsll((long long)~used0) - 1 : 64 + __ffsll((long long)~used1) - 1;
+                    // both masks full (all 128 colours taken below e): overflow, never a reused colour
+                    int c = (~used0) ? __ffsll((long long)~used0) - 1 : ((~used1) ? 64 + __ffsll((long long)~used1) - 1 : 128);
                     if (c >= max_colours || c < 0) {
                         atomicMin(overflow, e);
                         c = max_colours - 1;       // keep going; prepare reports CAPACITY

@@ -49,3 +49,32 @@ def oracle_problem(orc, prob, dtype=None):
     pe, pn = prob.parts()
     return orc.prepare(prob.coords, prob.conn, prob.model, prob.param_kind, rounded(prob.p0, dtype),
                        rounded(prob.p1, dtype), pe, pn)
+
+
+PER_ENTRY = 100.0   # reading R31: per-entry bar = PER_ENTRY * rel-L2 bar, scale-relative
+
+
+def assert_field(a, b, dtype, what=""):
+    """Parity of one output array (reading R13 / R31): the whole-array rel-L2 bar of the north
+    star, and next to it a per-entry bar |a_i - b_i| <= 100 tol (|b_i| + rms(b)), so that a
+    single wrong element or node cannot hide inside a small global norm."""
+    a = np.asarray(a, np.float64).ravel()
+    b = np.asarray(b, np.float64).ravel()
+    tol = TOL[dtype]
+    e = rel_l2(a, b)
+    assert e < tol, (what, "rel-L2", e)
+    rms = float(np.sqrt(np.mean(b * b))) if b.size else 0.0
+    worst = float(np.max(np.abs(a - b) / (np.abs(b) + rms + 1e-300))) if b.size else 0.0
+    assert worst < PER_ENTRY * tol, (what, "per-entry", worst)
+    return e, worst
+
+
+def assert_totals(t, ref, scale, dtype, what="totals"):
+    """Per-(sample, part) totals (reading R32): |t - ref| <= tol * scale entry by entry, where
+    scale = |W| + |f.u| is the sum of the magnitudes of the two terms of Pi = W - f.u (no
+    f_ext: scale = |W|), so the cancellation in W - f.u is not charged to the kernel."""
+    t = np.asarray(t, np.float64)
+    ref = np.asarray(ref, np.float64)
+    scale = np.asarray(scale, np.float64)
+    err = np.abs(t - ref) / np.maximum(scale, 1e-300)
+    assert float(np.max(err)) < TOL[dtype], (what, float(np.max(err)))

@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 import torch
 
-from helpers import TOL, gpu_problem, max_rel, oracle_problem, rel_l2, rounded
+from helpers import TOL, assert_field, assert_totals, gpu_problem, max_rel, oracle_problem, rel_l2, rounded
 from pfem_gen import (config1, config2, config3, config4, config5, fourier_field, kuhn_cube, plate_with_holes,
                       square_t3)
 from pfem_gen.configs import Problem
@@ -52,8 +52,16 @@ SMALL = list(small_problems())
 
 
 # ------------------------------------------------------------------ prep
-@pytest.mark.parametrize("prob", SMALL + [config1()], ids=lambda p: p.name)
+FULL = {2: lambda: config2(dtype="f32"), "2d": lambda: config2(dtype="f64"), 3: config3, 4: config4, 5: config5}
+
+
+@pytest.mark.parametrize("prob", SMALL + [config1()] + [pytest.param(k, id=f"config{k}-full") for k in FULL])
 def test_prepare_bitexact(orc, prob):
+    """Preparation is bit-exact against the oracle (north star): the CSR (ptr, ent), the greedy
+    colouring, the colour-sorted element list and its offsets; geometry within rounding.  Every
+    BASELINE config at full size (configs 2 fp32 / fp64, 3, 4, 5) plus the small meshes."""
+    if not isinstance(prob, Problem):
+        prob = FULL[prob]()
     mesh, _, _ = gpu_problem(prob)
     ptr, ent = orc.csr(prob.conn, prob.n_nodes)
     assert np.array_equal(mesh.csr_ptr.cpu().numpy(), ptr)
@@ -128,11 +136,10 @@ def test_element_order_energy_residual_tangent(orc, prob, order):
     kv = pf.tangent_apply(mesh, mat, torch.as_tensor(v, dtype=u.dtype, device="cuda"),
                           u=u if prob.model == "neohookean" else None)
     torch.cuda.synchronize()
-    tol = TOL[prob.dtype]
-    assert rel_l2(W.cpu().numpy(), W_ref) < tol
-    assert max_rel(tot.cpu().numpy(), tot_ref) < (tol if prob.dtype == "f64" else 1e-5)
-    assert rel_l2(r.cpu().numpy(), r_ref) < tol
-    assert rel_l2(kv.cpu().numpy(), kv_ref) < tol
+    assert_field(W.cpu().numpy(), W_ref, prob.dtype, "W_e")
+    assert_totals(tot.cpu().numpy(), tot_ref, np.abs(tot_ref), prob.dtype)
+    assert_field(r.cpu().numpy(), r_ref, prob.dtype, "residual")
+    assert_field(kv.cpu().numpy(), kv_ref, prob.dtype, "Kv")
 
 
 # ------------------------------------------------------------------ energy / residual
@@ -142,15 +149,17 @@ def check_energy(orc, prob, mode, block_elems=0, f_ext=None):
     ur = rounded(prob.u, prob.dtype)
     fe = None if f_ext is None else rounded(f_ext, prob.dtype)
     W_ref, tot_ref = om.energy(ur, f_ext=fe)
+    _, w_ref = om.energy(ur, want_elem=False) if fe is not None else (None, tot_ref)
     r_ref = om.residual(ur)
     import paper_2601_03086_b200 as pf
     ft = None if fe is None else torch.as_tensor(fe, dtype=u.dtype, device="cuda")
     tot, W, r = pf.energy(mesh, mat, u, f_ext=ft, elem_energy=True, residual=True, mode=mode)
     torch.cuda.synchronize()
     tol = TOL[prob.dtype]
-    assert rel_l2(W.cpu().numpy(), W_ref) < tol, rel_l2(W.cpu().numpy(), W_ref)
-    assert max_rel(tot.cpu().numpy(), tot_ref) < (tol if prob.dtype == "f64" else 1e-5)
-    assert rel_l2(r.cpu().numpy(), r_ref) < tol, rel_l2(r.cpu().numpy(), r_ref)
+    assert_field(W.cpu().numpy(), W_ref, prob.dtype, "W_e")
+    # Pi = W - f.u: scale |W| + |f.u| (reading R32)
+    assert_totals(tot.cpu().numpy(), tot_ref, np.abs(w_ref) + np.abs(w_ref - tot_ref), prob.dtype)
+    assert_field(r.cpu().numpy(), r_ref, prob.dtype, "residual")
     r2 = pf.residual(mesh, mat, u, mode=mode)
     torch.cuda.synchronize()
     assert torch.equal(r2, r) or rel_l2(r2.cpu().numpy(), r_ref) < tol
@@ -197,8 +206,7 @@ def check_tangent(orc, prob, mode, mask=None, seed=9, block_elems=0):
     mt = None if mask is None else torch.as_tensor(mask, dtype=torch.uint8, device="cuda")
     Kv = pf.tangent_apply(mesh, mat, vt, u=u if prob.model == "neohookean" else None, mask=mt, mode=mode)
     torch.cuda.synchronize()
-    err = rel_l2(Kv.cpu().numpy(), ref)
-    assert err < TOL[prob.dtype], err
+    assert_field(Kv.cpu().numpy(), ref, prob.dtype, "Kv")
 
 
 @pytest.mark.parametrize("mode", ["csr", "colour"])
@@ -335,6 +343,46 @@ def test_cg_config4_scaled(orc, n):
             assert rel_l2(x.cpu().numpy(), xo) < 1e-6
 
 
+def _golden_config4():
+    import json
+    import os
+    g = os.path.join(os.path.dirname(__file__), "golden")
+    with open(os.path.join(g, "config4_cg.json")) as fh:
+        gold = json.load(fh)
+    ustar = np.load(os.path.join(g, "config4_ustar_f32.npz"))["ustar"].astype(np.float64)
+    return gold, ustar
+
+
+@pytest.mark.parametrize("start", ["zero", "warm"])
+def test_cg_config4_full_vs_oracle_golden(start):
+    """Config 4 at full size (80^3 nodes, 2,958,234 tets, tol 1e-8): the
+    GPU CG iteration count against the oracle's, stored by tests/golden/make_config4_cg.py (which
+    calls only oracle/): |dk| <= 1 vs dot order 0, or inside the oracle's own spread over three
+    dot orders +-1 (reading R18); the first 50 residual-history entries within 1e-6 relative; the
+    true residual below the tolerance.  The warm start x0 = u* + 0.01 rms(u*) xi is rebuilt from
+    the stored oracle u* (float32) with the same seed on both sides."""
+    import paper_2601_03086_b200 as pf
+    from pfem_gen import warm_start
+    gold, ustar = _golden_config4()
+    p = config4()
+    mesh, mat, _ = gpu_problem(p)
+    x0 = np.zeros_like(p.f_ext) if start == "zero" else warm_start(ustar.reshape(p.f_ext.shape), p.mask, seed=4004)
+    f = torch.as_tensor(p.f_ext, device="cuda")
+    mask = torch.as_tensor(p.mask, device="cuda")
+    x, rep = pf.cg(mesh, mat, f, torch.as_tensor(x0, device="cuda"), mask=mask, tol=gold["tol"])
+    g = gold[start]
+    r0 = g["runs"]["0"]
+    assert rep["converged"]
+    k = rep["iterations"]
+    lo, hi = g["spread"]
+    assert abs(k - r0["iterations"]) <= 1 or lo - 1 <= k <= hi + 1, (k, r0["iterations"], g["spread"])
+    h = rep["history"][:50]
+    ho = np.asarray(r0["history50"])
+    assert np.max(np.abs(h - ho[: len(h)]) / ho[: len(h)]) < 1e-6
+    assert rep["true_rel_res_final"] < gold["tol"]
+    assert abs(rep["rel_res0"] - r0["rel_res0"]) <= 1e-9 * r0["rel_res0"]
+
+
 # ------------------------------------------------------------------ Newton (§8(f) row f1)
 @pytest.mark.parametrize("order", ["input", "locality"])
 def test_newton_matches_oracle(orc, order):
@@ -449,10 +497,8 @@ def test_pcg_config4_scaled(orc, n):
             x, rep = pf.cg(mesh, mat, f, torch.as_tensor(x0, device="cuda"), mask=mask, tol=1e-8, mode=mode,
                            precond="jacobi")
             assert rep["converged"]
-            assert abs(rep["iterations"] - ro["iterations"]) <= 2, (rep["iterations"], ro["iterations"])
-            h, ho = rep["history"], ro["history"]
-            m = min(50, len(h), len(ho))
-            assert np.max(np.abs(h[:m] - ho[:m]) / ho[:m]) < 1e-6
+            # reading R18 with the oracle PCG's own spread over the five dot orders
+            assert_cg_count(rep, ro, om.pcg_spread(p.f_ext, p.mask, x0, tol=1e-8))
             assert rep["true_rel_res_final"] < 2e-8
             assert rel_l2(x.cpu().numpy(), xo) < 1e-6
     # precond "none" through pfem_pcg is pfem_cg
@@ -476,7 +522,8 @@ def test_pcg_neohookean_state(orc):
     x, rep = pf.cg(mesh, mat, f, torch.zeros_like(f), mask=mask, tol=1e-10, u_state=torch.as_tensor(us, device="cuda"),
                    precond="jacobi")
     xo, ro = om.pcg(p.f_ext, p.mask, np.zeros_like(p.f_ext), tol=1e-10, u_state=us)
-    assert rep["converged"] and ro["converged"] and abs(rep["iterations"] - ro["iterations"]) <= 2
+    assert rep["converged"] and ro["converged"]
+    assert_cg_count(rep, ro, om.pcg_spread(p.f_ext, p.mask, np.zeros_like(p.f_ext), tol=1e-10, u_state=us))
     assert rel_l2(x.cpu().numpy(), xo) < 1e-8
 
 
@@ -497,15 +544,17 @@ def test_pretrain_loss_matches_oracle(orc, prob, with_phi):
     fr, phr = rounded(f, prob.dtype), None if phi is None else rounded(phi, prob.dtype)
     dt = H.dtype
     lo, Po, go, uo = om.pretrain_loss(rounded(prob.u, prob.dtype), phr, fr)
+    _, Wo = om.energy(uo, want_elem=False)
+    scale = np.abs(Wo) + np.abs(Wo - Po)                      # |W| + |f.u| (reading R32)
     tol = TOL[prob.dtype]
     for mode in ("csr", "colour"):   # CSR: epilogue fused into the assembly writes; COLOUR: own pass
         loss, tot, grad, u = pf.pretrain_loss(mesh, mat, H, mode=mode,
                                               phi=None if phi is None else torch.as_tensor(phr, dtype=dt, device="cuda"),
                                               f_ext=torch.as_tensor(fr, dtype=dt, device="cuda"))
-        assert rel_l2(u.cpu().numpy(), uo) < tol
-        assert max_rel(tot.cpu().numpy(), Po) < (1e-10 if prob.dtype == "f64" else 1e-4)
-        assert abs(float(loss) - lo) <= (1e-10 if prob.dtype == "f64" else 1e-4) * abs(lo)
-        assert rel_l2(grad.cpu().numpy(), go) < tol
+        assert_field(u.cpu().numpy(), uo, prob.dtype, "u")
+        assert_totals(tot.cpu().numpy(), Po, scale, prob.dtype, "Pi")
+        assert abs(float(loss) - lo) <= tol * float(scale.mean())   # loss = mean of Pi
+        assert_field(grad.cpu().numpy(), go, prob.dtype, "dloss/dH")
 
 
 # ------------------------------------------------------------------ large blocks (direct form)
@@ -585,15 +634,18 @@ def test_heat_matches_oracle(orc, prob):
     W, tot, r = pf.heat(mesh, torch.as_tensor(k, dtype=dt, device="cuda"), torch.as_tensor(T, dtype=dt, device="cuda"),
                         f=torch.as_tensor(f, dtype=dt, device="cuda"))
     Wo, toto, ro = om.heat(T, k, f=f)
+    _, wo, _ = om.heat(T, k)
+    scale = np.abs(wo) + np.abs(wo - toto)                    # |W| + |f.T| (reading R32)
     tol = TOL[prob.dtype]
-    assert rel_l2(W.cpu().numpy(), Wo) < tol
-    assert max_rel(tot.cpu().numpy(), toto) < (1e-10 if prob.dtype == "f64" else 1e-4)
-    assert rel_l2(r.cpu().numpy(), ro) < tol
+    assert_field(W.cpu().numpy(), Wo, prob.dtype, "W_e")
+    assert_totals(tot.cpu().numpy(), toto, scale, prob.dtype)
+    assert_field(r.cpu().numpy(), ro, prob.dtype, "flux")
     # geometry formed on the fly from the coordinates (f4 variant): same results within the bar
     W2, tot2, r2 = pf.heat(mesh, torch.as_tensor(k, dtype=dt, device="cuda"), torch.as_tensor(T, dtype=dt, device="cuda"),
                            f=torch.as_tensor(f, dtype=dt, device="cuda"), geometry_on_the_fly=True)
-    assert rel_l2(W2.cpu().numpy(), Wo) < tol and rel_l2(r2.cpu().numpy(), ro) < tol
-    assert max_rel(tot2.cpu().numpy(), toto) < (1e-10 if prob.dtype == "f64" else 1e-4)
+    assert_field(W2.cpu().numpy(), Wo, prob.dtype, "W_e otf")
+    assert_field(r2.cpu().numpy(), ro, prob.dtype, "flux otf")
+    assert_totals(tot2.cpu().numpy(), toto, scale, prob.dtype)
     # uniform conductivity (stride 0)
     W1, _, r1 = pf.heat(mesh, torch.tensor([1.5], dtype=dt, device="cuda"), torch.as_tensor(T, dtype=dt, device="cuda"))
     Wo1, _, ro1 = om.heat(T, [1.5])

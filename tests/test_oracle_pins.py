@@ -501,6 +501,31 @@ def test_cg_history_and_breakdown_conventions(orc):
     assert h[-1] < 1e-6 and np.all(h[:-1] >= 1e-6)
 
 
+@pytest.mark.parametrize("order", [0, 1, 2, 3, 4])
+def test_dot_orders_pinned_to_exact_dot(orc, order):
+    """The five CG dot-product orders of reading R18 (ascending, descending, pairwise,
+    1024-blocked, Kahan) are sums of the same n products (P:1021-1036 CG).  Pinned against an
+    exact dot: (i) small-integer vectors, where every partial sum is an integer below 2^53 and so
+    every order must give the exact value bit for bit (a dropped, repeated or misindexed term
+    fails); (ii) random floats against math.fsum of the rounded products, within the
+    order-independent bound n eps sum|a_i b_i| (Kahan: 2 eps sum|a_i b_i|)."""
+    import math
+    rng = np.random.default_rng(1800 + order)
+    for n in (1, 2, 7, 8, 9, 1023, 1024, 1025, 5000):
+        a = rng.integers(-1000, 1001, n).astype(np.float64)
+        b = rng.integers(-1000, 1001, n).astype(np.float64)
+        exact = int(np.dot(a.astype(np.int64), b.astype(np.int64)))
+        assert orc.dot(a, b, order) == float(exact), (order, n)
+    eps = np.finfo(np.float64).eps
+    for n in (3, 1000, 4099, 100000):
+        a = rng.standard_normal(n) * np.exp(rng.uniform(-5, 5, n))
+        b = rng.standard_normal(n)
+        prods = a * b
+        ref = math.fsum(prods.tolist())
+        bound = (2.0 if order == 4 else n) * eps * float(np.sum(np.abs(prods)))
+        assert abs(orc.dot(a, b, order) - ref) <= bound, (order, n)
+
+
 # ---------------------------------------------------------------- Newton (§8(f) row f1)
 def _potential(m, u, f):
     """Pi(U) = W(U) - f.U (App. B / P:164, the energy the residual differentiates)."""
