@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define PFEM_ABI_VERSION 4
+#define PFEM_ABI_VERSION 5
 
 typedef enum {
     PFEM_OK = 0,
@@ -86,6 +86,15 @@ typedef enum {
     PFEM_ORDER_AUTO = 2            /* whichever of the two gives fewer (block, node) occurrences  */
 } pfem_elem_order;
 
+/* Element geometry of the CSR-mode element kernels (SURVEY §8(f) row f4 variant). */
+typedef enum {
+    PFEM_GEOMETRY_STORED = 0,      /* read grad / vol prepared by pfem_mesh_prepare                 */
+    PFEM_GEOMETRY_ON_THE_FLY = 1   /* form grad N_a and V_e in fp64 from `coords` inside the element
+                                      pass (same formula as prepare; fewer HBM bytes, more ALU).
+                                      Applies to PFEM_ASSEMBLE_CSR energy / residual / tangent and
+                                      the solvers built on them; COLOUR mode reads grad / vol      */
+} pfem_geometry;
+
 typedef struct pfem_plan pfem_plan;   /* opaque, library-owned device data */
 
 /* Mesh descriptor.  Inputs are set by the caller; pfem_mesh_prepare fills the outputs. */
@@ -99,6 +108,7 @@ typedef struct {
     int32_t elem_order;            /* assembly element order (pfem_elem_order): the plan may visit
                                       elements in a locality order; results are unchanged up to
                                       rounding and are reported in input element order           */
+    int32_t geometry;              /* pfem_geometry; may change between calls (coords must stay valid) */
     const double* coords;          /* [n_nodes][dim], float64 always                             */
     const int32_t* conn;           /* [n_elems][dim+1], node ids in [0, n_nodes)                 */
     const int32_t* part_elem;      /* [n_parts+1] element offsets (device), NULL if n_parts == 1 */

@@ -34,12 +34,15 @@ def _require_cuda(*ts):
             raise ValueError("libpfem takes CUDA tensors only (no CPU fallback)")
 
 
+GEOMETRY = {"stored": 0, "on_the_fly": 1}
+
+
 class Mesh:
     """A prepared mesh (pfem_mesh_prepare): geometry, CSR, colouring and assembly plan."""
 
     def __init__(self, coords: torch.Tensor, conn: torch.Tensor, dtype=torch.float64, part_elem=None,
                  part_node=None, block_elems: int = 0, max_colours: int = 128, stream=None,
-                 elem_order: str = "auto"):
+                 elem_order: str = "auto", geometry: str = "stored"):
         lib = L.load()
         _require_cuda(coords, conn)
         dev = coords.device
@@ -70,6 +73,7 @@ class Mesh:
         m.dtype = _DT[dtype]
         m.block_elems = block_elems
         m.elem_order = {"input": 0, "locality": 1, "auto": 2}[elem_order]
+        m.geometry = GEOMETRY[geometry]
         m.coords, m.conn = self.coords.data_ptr(), self.conn.data_ptr()
         m.part_elem = self.part_elem.data_ptr() if self.part_elem is not None else None
         m.part_node = self.part_node.data_ptr() if self.part_node is not None else None
@@ -83,6 +87,15 @@ class Mesh:
         self._ws = {}
 
     # ------------------------------------------------------------------ info
+    @property
+    def geometry(self) -> str:
+        """"stored" (prepared grad / vol) or "on_the_fly" (formed from coords in the element pass)."""
+        return {v: k for k, v in GEOMETRY.items()}[self._m.geometry]
+
+    @geometry.setter
+    def geometry(self, g: str):
+        self._m.geometry = GEOMETRY[g]
+
     @property
     def n_colours(self):
         return self._m.n_colours

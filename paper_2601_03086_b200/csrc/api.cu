@@ -90,6 +90,14 @@ static pfem_status common_checks(const pfem_mesh* m, const pfem_material* mat, i
         return PFEM_ERR_ARG;
     }
     if (mode != PFEM_ASSEMBLE_CSR && mode != PFEM_ASSEMBLE_COLOUR) { set_error("bad assembly mode"); return PFEM_ERR_ARG; }
+    if (m->geometry != PFEM_GEOMETRY_STORED && m->geometry != PFEM_GEOMETRY_ON_THE_FLY) {
+        set_error("bad geometry option");
+        return PFEM_ERR_ARG;
+    }
+    if (m->geometry == PFEM_GEOMETRY_ON_THE_FLY && !m->coords) {
+        set_error("on-the-fly geometry needs coords");
+        return PFEM_ERR_ARG;
+    }
     if (!ws) { set_error("workspace is NULL"); return PFEM_ERR_ARG; }
     const Plan* P = reinterpret_cast<const Plan*>(m->plan);
     if (ws_bytes < ws_layout(*P, S, m->dtype == PFEM_F64 ? 8 : 4).total) {
@@ -131,6 +139,7 @@ pfem_status pfem_mesh_prepare(pfem_mesh* m, void* stream) {
     if (m->max_colours < 1 || m->max_colours > 128) { set_error("max_colours must be in [1, 128]"); return PFEM_ERR_ARG; }
     if (m->block_elems < 0) { set_error("block_elems must be >= 0"); return PFEM_ERR_ARG; }
     if (m->elem_order < 0 || m->elem_order > 2) { set_error("elem_order must be 0, 1 or 2"); return PFEM_ERR_ARG; }
+    if (m->geometry < 0 || m->geometry > 1) { set_error("geometry must be 0 or 1"); return PFEM_ERR_ARG; }
     if (m->dim == 3 && ((uintptr_t)m->conn & 15)) { set_error("conn must be 16-byte aligned for dim 3"); return PFEM_ERR_ARG; }
     if (m->plan) release_impl(m);
     return prepare_impl(m, (cudaStream_t)stream);

@@ -96,6 +96,8 @@ struct AsmParams {
     const int32_t* conn;
     const T* grad;
     const T* vol;
+    const double* coords;  // [N][D] fp64 (on-the-fly geometry)
+    int otf;               // form grad / vol from coords in the element pass (direct form)
     MatArgs<T> mat;
     const T* u;            // field (energy / residual) or NH state (tangent)
     const T* v;            // tangent direction

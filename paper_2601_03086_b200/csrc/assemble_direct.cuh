@@ -37,13 +37,25 @@ __device__ __forceinline__ void l2_prefetch(const void* base, size_t total, size
 
 // prefetch block b's record (from its gradients on; conn is not read here) and its
 // per-element moduli into L2 (issued by one thread)
-template <class T>
+template <class T, bool OTF>
 __device__ __forceinline__ void prefetch_record(const AsmParams<T>& p, int b) {
     const size_t rb = (size_t)p.rec.bytes, total = rb * p.n_blocks;
     // the fields the direct kernel reads (RecLayout order): fp32 (ent_pos layout)
-    // [ent_pos, loc_ent), fp64 (loc_ent gather) [g, end); conn is not read here
-    if (sizeof(T) == 4) l2_prefetch(p.recs, total, (size_t)b * rb + p.rec.ent_pos, p.rec.loc_ent - p.rec.ent_pos);
-    else l2_prefetch(p.recs, total, (size_t)b * rb + p.rec.g, rb - p.rec.g);
+    // [ent_pos, loc_ent), fp64 (loc_ent gather) [g, end); conn is not read here; on-the-fly
+    // geometry skips the gradients and volumes [g, eid)
+    const size_t b0 = (size_t)b * rb;
+    if (OTF) {
+        if (sizeof(T) == 4) {
+            l2_prefetch(p.recs, total, b0 + p.rec.ent_pos, p.rec.g - p.rec.ent_pos);
+            l2_prefetch(p.recs, total, b0 + p.rec.eid, p.rec.loc_ent - p.rec.eid);
+        } else {
+            l2_prefetch(p.recs, total, b0 + p.rec.eid, rb - p.rec.eid);
+        }
+    } else if (sizeof(T) == 4) {
+        l2_prefetch(p.recs, total, b0 + p.rec.ent_pos, p.rec.loc_ent - p.rec.ent_pos);
+    } else {
+        l2_prefetch(p.recs, total, b0 + p.rec.g, rb - p.rec.g);
+    }
     const int e0 = __ldg(p.blk_elem + b), e1 = __ldg(p.blk_elem + b + 1);
     const size_t E = (size_t)p.E, ne = (size_t)(e1 - e0);
     if (p.perm) return;   // element-wise materials are gathered through the permutation
@@ -79,7 +91,7 @@ __device__ __forceinline__ X rld(const X* q) {
 // per SM with the 384-element blocks: config 4 134.5 -> 132.4 us); fp64 Neo-Hookean and fp64
 // several-sample calls the compiler's own allocation (a 40-register cap spilled hundreds of
 // bytes per thread)
-template <int D, int MODEL, class T, int OP, int ST, bool MASKED, int NT, bool PERM>
+template <int D, int MODEL, class T, int OP, int ST, bool MASKED, int NT, bool PERM, bool OTF>
 __global__ void __launch_bounds__(NT, ST > 1 ? (sizeof(T) == 4 ? PFEM_DIRECT_MINBS : 0)
                                             : (sizeof(T) == 4 ? 65536 / (NT * 64) : (MODEL == MODEL_LINEAR ? PFEM_DIRECT_MINB64 : 0)))
 k_assemble_direct(const AsmParams<T> p) {
@@ -114,11 +126,15 @@ k_assemble_direct(const AsmParams<T> p) {
                                                      ~size_t(15)));
     // element-wise materials [2][EB] after the force buffer
     T* smat = fbuf + (HAS_FORCE ? (size_t)ST * D * NV * EB : 0);
+    // on-the-fly geometry: the vertex coordinates of the block's node occurrences [ocap][D]
+    double* scoord = reinterpret_cast<double*>(
+        (reinterpret_cast<uintptr_t>(smat + ((PFEM_DIRECT_SMAT && (p.mat.s0 | p.mat.s1)) ? 2 * (size_t)EB : 0)) + 15) &
+        ~uintptr_t(15));
     const bool has_mat = (p.mat.s0 | p.mat.s1) != 0;
     const bool cgdot = OP == OP_TANGENT && p.cg != nullptr;
     if (p.cg && ld_relaxed_i(&p.cg->done)) return;
     const int b = blockIdx.x;
-    if (p.lag > 0 && tid == 0 && b + p.lag < p.n_blocks) prefetch_record<T>(p, b + p.lag);
+    if (p.lag > 0 && tid == 0 && b + p.lag < p.n_blocks) prefetch_record<T, OTF>(p, b + p.lag);
     const unsigned char* rg = p.recs + (size_t)b * p.rec.bytes;
     __shared__ __align__(8) uint64_t s_rbar;
     if constexpr (TMA) {
@@ -170,6 +186,14 @@ k_assemble_direct(const AsmParams<T> p) {
         } else {
             stage_fields<D, T, NT, ST, false>(ust, rgb, 0u, p.u, p, s0, nq, no);
         }
+        if (OTF && s0 == 0) {   // vertex coordinates (fp64) of the block's occurrences
+            const int32_t* so = reinterpret_cast<const int32_t*>(rgb + p.rec.occ_node);
+            for (int o = tid; o < no; o += NT) {
+                const int node = rld<TMA>(so + o) & OCC_NODE_MASK;
+#pragma unroll
+                for (int i = 0; i < D; ++i) cpn<8>(scoord + o * D + i, p.coords + (int64_t)node * D + i);
+            }
+        }
         // element-wise materials of the block, copied into shared memory with the fields (one
         // overlapped latency instead of one dependent gather per element and thread)
         if (PFEM_DIRECT_SMAT && has_mat && s0 == 0) {
@@ -211,12 +235,28 @@ k_assemble_direct(const AsmParams<T> p) {
                 }
             }
             {
-                const T* sg = reinterpret_cast<const T*>(rgb + p.rec.g);
+                if constexpr (OTF) {
+                    // grad N_a and V_e formed in fp64 from the staged vertex coordinates (the
+                    // formula of pfem_mesh_prepare), then rounded to T like the prepared arrays
+                    double X[NV][D], inv[D][D];
 #pragma unroll
-                for (int a = 0; a < D; ++a)
+                    for (int a = 0; a < NV; ++a)
 #pragma unroll
-                    for (int j = 0; j < D; ++j) G.g[a][j] = rld<TMA>(sg + (a * D + j) * EB + el);
-                G.V = rld<TMA>(reinterpret_cast<const T*>(rgb + p.rec.vol) + el);
+                        for (int i = 0; i < D; ++i) X[a][i] = scoord[lv[a] * D + i];
+                    const double det = geometry_of<D>(X, inv);
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+#pragma unroll
+                        for (int j = 0; j < D; ++j) G.g[a][j] = (T)inv[a][j];
+                    G.V = (T)(fabs(det) / (D == 2 ? 2.0 : 6.0));
+                } else {
+                    const T* sg = reinterpret_cast<const T*>(rgb + p.rec.g);
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+#pragma unroll
+                        for (int j = 0; j < D; ++j) G.g[a][j] = rld<TMA>(sg + (a * D + j) * EB + el);
+                    G.V = rld<TMA>(reinterpret_cast<const T*>(rgb + p.rec.vol) + el);
+                }
                 const T m0 = (PFEM_DIRECT_SMAT && p.mat.s0) ? smat[el] : __ldg(p.mat.p0 + (int64_t)e * p.mat.s0);
                 const T m1 = (PFEM_DIRECT_SMAT && p.mat.s1) ? smat[EB + el] : __ldg(p.mat.p1 + (int64_t)e * p.mat.s1);
                 lame_elem<T>(p.mat, lsc, m0, m1, G.mu, G.lam);

@@ -123,6 +123,44 @@ __device__ __forceinline__ void log1p_g(V x, V& l, V& g) {   // float / F2
     }
 }
 
+// P1 geometry from the d+1 vertex coordinates, fp64 (App. B):
+// J = [X_1-X_0 | .. | X_d-X_0] (columns), inv = J^{-1} (row a = grad N_{a+1}), returns det J.
+// The one formula of both the prepared geometry (k_geometry) and the on-the-fly option.
+template <int D>
+__device__ __forceinline__ double geometry_of(const double (&X)[D + 1][D], double (&inv)[D][D]) {
+    double J[D][D];
+#pragma unroll
+    for (int a = 1; a <= D; ++a)
+#pragma unroll
+        for (int i = 0; i < D; ++i) J[i][a - 1] = X[a][i] - X[0][i];
+    double det;
+    if constexpr (D == 2) {
+        det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+        const double r = 1.0 / det;
+        inv[0][0] = J[1][1] * r;
+        inv[0][1] = -J[0][1] * r;
+        inv[1][0] = -J[1][0] * r;
+        inv[1][1] = J[0][0] * r;
+    } else {
+        // cofactors of J: C_ij; inverse = C^T / det
+        const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+        const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+        const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+        det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+        const double r = 1.0 / det;
+        inv[0][0] = c00 * r;
+        inv[1][0] = c01 * r;
+        inv[2][0] = c02 * r;
+        inv[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * r;
+        inv[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * r;
+        inv[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * r;
+        inv[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * r;
+        inv[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * r;
+        inv[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * r;
+    }
+    return det;
+}
+
 template <class T>
 struct MatArgs {
     int kind;

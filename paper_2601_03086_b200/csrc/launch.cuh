@@ -51,6 +51,8 @@ AsmParams<T> make_params(const Call& c) {
     p.conn = c.m->conn;
     p.grad = (const T*)c.m->grad;
     p.vol = (const T*)c.m->vol;
+    p.coords = c.m->coords;
+    p.otf = (c.m->geometry == PFEM_GEOMETRY_ON_THE_FLY && c.mode == PFEM_ASSEMBLE_CSR) ? 1 : 0;
     p.mat.kind = c.mat.kind;
     p.mat.p0 = (const T*)c.mat.p0;
     p.mat.p1 = (const T*)c.mat.p1;
@@ -121,16 +123,18 @@ AsmParams<T> make_params(const Call& c) {
 template <class T>
 constexpr int direct_nt() { return sizeof(T) == 4 ? PFEM_DIRECT_NT32 : PFEM_DIRECT_NT64; }   // direct kernel threads per CTA (measured)
 
-template <int D, int MODEL, class T, int OP, int ST, bool MASKED, int NT, bool PERM>
+template <int D, int MODEL, class T, int OP, int ST, bool MASKED, int NT, bool PERM, bool OTF>
 pfem_status launch_direct(AsmParams<T> p, cudaStream_t s) {
     constexpr bool HAS_FORCE = OP != OP_ENERGY;
     constexpr int NFd = (OP == OP_TANGENT && MODEL == MODEL_NH) ? 2 : 1;
     const size_t rbn = (PFEM_DIRECT_TMA && sizeof(T) == 4) ? ((p.rec.loc_ent - p.rec.ent_pos + 15u) & ~15u) : 0;
-    const size_t smem = rbn + ((NFd * (size_t)p.rec.ocap * D * ST * sizeof(T) + (sizeof(T) == 4 ? 0 : 2 * (size_t)(D + 1) * p.rec.eb) +
+    const size_t smem0 = rbn + ((NFd * (size_t)p.rec.ocap * D * ST * sizeof(T) + (sizeof(T) == 4 ? 0 : 2 * (size_t)(D + 1) * p.rec.eb) +
                                 15) & ~size_t(15)) +
                         (HAS_FORCE ? (size_t)ST * D * (D + 1) * p.rec.eb * sizeof(T) : 0) +
                         ((PFEM_DIRECT_SMAT && (p.mat.s0 | p.mat.s1)) ? 2 * (size_t)p.rec.eb * sizeof(T) : 0);
-    auto kd = k_assemble_direct<D, MODEL, T, OP, ST, MASKED, NT, PERM>;
+    // on-the-fly geometry: the block's vertex coordinates [ocap][D] fp64 after everything else
+    const size_t smem = OTF ? ((smem0 + 15) & ~size_t(15)) + (size_t)p.rec.ocap * D * sizeof(double) : smem0;
+    auto kd = k_assemble_direct<D, MODEL, T, OP, ST, MASKED, NT, PERM, OTF>;
     static size_t configured = 0;
     static int pf_auto = 0;
     if (smem > configured || pf_auto == 0) {
@@ -167,10 +171,17 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
     // Blocks larger than the staged kernel's compile-time capacity always take the direct form.
     // (the staged form reads the record with its compile-time stride EB)
     // (CG products, p.cg set, always take the direct form: the staged kernel has no fused p.q)
-    const bool direct = p.eb_max > EB || p.rec.eb != EB || p.cg != nullptr || (variant >= 0 ? variant == 1 : p.S == 1);
+    // (on-the-fly geometry is a direct-form option)
+    const bool direct = p.otf || p.eb_max > EB || p.rec.eb != EB || p.cg != nullptr ||
+                        (variant >= 0 ? variant == 1 : p.S == 1);
     if (direct) {
-        const pfem_status st = p.perm ? launch_direct<D, MODEL, T, OP, ST, MASKED, direct_nt<T>(), true>(p, s)
-                                      : launch_direct<D, MODEL, T, OP, ST, MASKED, direct_nt<T>(), false>(p, s);
+        pfem_status st;
+        if (p.otf)
+            st = p.perm ? launch_direct<D, MODEL, T, OP, ST, MASKED, direct_nt<T>(), true, true>(p, s)
+                        : launch_direct<D, MODEL, T, OP, ST, MASKED, direct_nt<T>(), false, true>(p, s);
+        else
+            st = p.perm ? launch_direct<D, MODEL, T, OP, ST, MASKED, direct_nt<T>(), true, false>(p, s)
+                        : launch_direct<D, MODEL, T, OP, ST, MASKED, direct_nt<T>(), false, false>(p, s);
         if (st != PFEM_OK) return st;
     } else {
         // the staged copy (RecLayout order) skips conn: every work item stages its fields (and

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "element.cuh"
 
 namespace pfem {
 
@@ -33,43 +34,24 @@ __global__ void k_geometry(int E, const double* __restrict__ X, const int32_t* _
     int v[D + 1];
 #pragma unroll
     for (int a = 0; a <= D; ++a) v[a] = conn[(int64_t)e * (D + 1) + a];
-    double J[D][D];
+    double Xv[D + 1][D];
+#pragma unroll
+    for (int a = 0; a <= D; ++a)
+#pragma unroll
+        for (int i = 0; i < D; ++i) Xv[a][i] = X[(int64_t)v[a] * D + i];
     double eprod = 1.0;
 #pragma unroll
     for (int a = 1; a <= D; ++a) {
         double l2 = 0.0;
 #pragma unroll
         for (int i = 0; i < D; ++i) {
-            J[i][a - 1] = X[(int64_t)v[a] * D + i] - X[(int64_t)v[0] * D + i];
-            l2 += J[i][a - 1] * J[i][a - 1];
+            const double dx = Xv[a][i] - Xv[0][i];
+            l2 += dx * dx;
         }
         eprod *= sqrt(l2);
     }
-    double det, inv[D][D];
-    if (D == 2) {
-        det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
-        double r = 1.0 / det;
-        inv[0][0] = J[1][1] * r;
-        inv[0][1] = -J[0][1] * r;
-        inv[1][0] = -J[1][0] * r;
-        inv[1][1] = J[0][0] * r;
-    } else {
-        // cofactors of J: C_ij; inverse = C^T / det
-        double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
-        double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
-        double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
-        det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
-        double r = 1.0 / det;
-        inv[0][0] = c00 * r;
-        inv[1][0] = c01 * r;
-        inv[2][0] = c02 * r;
-        inv[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * r;
-        inv[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * r;
-        inv[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * r;
-        inv[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * r;
-        inv[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * r;
-        inv[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * r;
-    }
+    double inv[D][D];
+    const double det = geometry_of<D>(Xv, inv);
     if (!(fabs(det) > 64.0 * 2.220446049250313e-16 * eprod)) {
         atomicMin(first_degenerate, e);
         return;

@@ -228,6 +228,61 @@ def test_config3_tangent_full(orc):
     check_tangent(orc, config3(), "csr")
 
 
+# ------------------------------------------------------------------ on-the-fly geometry (§8(f) row f4)
+@pytest.mark.parametrize("prob", SMALL + [config1()], ids=lambda p: p.name)
+def test_geometry_on_the_fly_small(orc, prob):
+    """PFEM_GEOMETRY_ON_THE_FLY: grad N_a and V_e formed in fp64 from the coordinates inside the
+    element pass (the prepare formula) give the oracle's W_e, totals, residual and
+    K.v within the north-star bars, with element-wise materials, parts and masks."""
+    import paper_2601_03086_b200 as pf
+    mesh, mat, u = gpu_problem(prob)
+    mesh.geometry = "on_the_fly"
+    om = oracle_problem(orc, prob)
+    ur = rounded(prob.u, prob.dtype)
+    W_ref, tot_ref = om.energy(ur)
+    tot, W, r = pf.energy(mesh, mat, u, elem_energy=True, residual=True)
+    v = rounded(np.random.default_rng(12).standard_normal(prob.u.shape), prob.dtype)
+    mask = (np.random.default_rng(4).random(prob.n_nodes * prob.dim) < 0.2).astype(np.uint8)
+    kv_ref = om.tangent(v, u=ur if prob.model == "neohookean" else None, mask=mask)
+    kv = pf.tangent_apply(mesh, mat, torch.as_tensor(v, dtype=u.dtype, device="cuda"),
+                          u=u if prob.model == "neohookean" else None, mask=torch.as_tensor(mask, device="cuda"))
+    torch.cuda.synchronize()
+    assert_field(W.cpu().numpy(), W_ref, prob.dtype, "W_e otf")
+    assert_totals(tot.cpu().numpy(), tot_ref, np.abs(tot_ref), prob.dtype)
+    assert_field(r.cpu().numpy(), om.residual(ur), prob.dtype, "residual otf")
+    assert_field(kv.cpu().numpy(), kv_ref, prob.dtype, "Kv otf")
+
+
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_geometry_on_the_fly_full(orc, cfg):
+    """On-the-fly geometry at full size: config-4 masked K.v (fp64) and config-5 fused E+R over
+    64 parts (fp32) against the oracle."""
+    if cfg == 4:
+        p = config4()
+        mesh, mat, u = gpu_problem(p)
+        mesh.geometry = "on_the_fly"
+        import paper_2601_03086_b200 as pf
+        om = oracle_problem(orc, p)
+        v = rounded(np.random.default_rng(9).standard_normal(p.u.shape), p.dtype)
+        ref = om.tangent(v, mask=p.mask)
+        kv = pf.tangent_apply(mesh, mat, torch.as_tensor(v, device="cuda"), mask=torch.as_tensor(p.mask, device="cuda"))
+        torch.cuda.synchronize()
+        assert_field(kv.cpu().numpy(), ref, p.dtype, "Kv otf config 4")
+    else:
+        p = config5()
+        mesh, mat, u = gpu_problem(p)
+        mesh.geometry = "on_the_fly"
+        import paper_2601_03086_b200 as pf
+        om = oracle_problem(orc, p)
+        ur = rounded(p.u, p.dtype)
+        W_ref, tot_ref = om.energy(ur)
+        tot, W, r = pf.energy(mesh, mat, u, elem_energy=True, residual=True)
+        torch.cuda.synchronize()
+        assert_field(W.cpu().numpy(), W_ref, p.dtype, "W_e otf config 5")
+        assert_totals(tot.cpu().numpy(), tot_ref, np.abs(tot_ref), p.dtype)
+        assert_field(r.cpu().numpy(), om.residual(ur), p.dtype, "residual otf config 5")
+
+
 # ------------------------------------------------------------------ determinism, flags
 @pytest.mark.parametrize("mode", ["csr", "colour"])
 def test_bitwise_deterministic(mode):

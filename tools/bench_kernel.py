@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--block-elems", type=int, default=0)
     ap.add_argument("--dtype", default=None)
     ap.add_argument("--order", default="auto", choices=["auto", "input", "locality"])
+    ap.add_argument("--otf", action="store_true", help="geometry formed on the fly from coords")
     a = ap.parse_args()
     prob = CONFIGS[a.config]() if a.config != 2 else CONFIGS[2](dtype=a.dtype or "f32")
     dt = torch.float32 if (a.dtype or prob.dtype) == "f32" else torch.float64
@@ -44,7 +45,7 @@ def main():
     for c in range(a.copies):
         m = pf.Mesh(torch.as_tensor(prob.coords, device=dev), torch.as_tensor(prob.conn, device=dev), dtype=dt,
                     part_elem=pe if prob.n_parts > 1 else None, part_node=pn if prob.n_parts > 1 else None,
-                    block_elems=a.block_elems, elem_order=a.order)
+                    block_elems=a.block_elems, elem_order=a.order, geometry="on_the_fly" if a.otf else "stored")
         mat = pf.Material(prob.model, prob.param_kind, torch.as_tensor(np.asarray(prob.p0), dtype=dt, device=dev),
                           torch.as_tensor(np.asarray(prob.p1), dtype=dt, device=dev))
         u = torch.as_tensor(prob.u, dtype=dt, device=dev)
