@@ -141,6 +141,12 @@ struct AsmParams {
     int32_t* part_cnt;     // [K] reduced chunks per part (0 at rest)
     T* partial;            // [n_occ][S][D]
     CgState* cg;           // non-null: fused p.q and alpha epilogue (S == 1)
+    // pipelined CG (§8(f) row f3): the direct form stages p_new = z + beta p_old (z = D^-1 r or r,
+    // the k_cg_dir formula) instead of copying v, and the node's owner occurrence stores p_new
+    // into `v` (the p buffer of this iteration); p_old is the other buffer
+    const T* cg_r;         // non-null: fused direction update
+    const T* cg_pold;
+    const T* cg_dinv;      // nullable (Jacobi)
     // pretraining-loss epilogue (§8(f) row f2), applied where the assembled value is written:
     // out = phi (.) (value - f_ext) * ep_scale; the last kernel-B CTA writes the batch-mean loss
     int ep;

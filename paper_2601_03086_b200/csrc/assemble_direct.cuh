@@ -180,7 +180,30 @@ k_assemble_direct(const AsmParams<T> p) {
     if (lsc.on && tid == 0) lame_of<T>(p.mat.kind, T(1), __ldg(p.mat.p1), s_lame[0], s_lame[1]);
     for (int s0 = 0; s0 < S; s0 += ST) {
         const int nq = min(ST, S - s0);
-        if (OP == OP_TANGENT) {
+        if (OP == OP_TANGENT && ST == 1 && p.cg_r) {
+            // pipelined CG: p_new = z + beta p_old formed while staging (k_cg_dir's formula, so
+            // the iterates are those of the unfused loop); the owner occurrence stores p_new
+            const int32_t* so = reinterpret_cast<const int32_t*>(rgb + p.rec.occ_node);
+            const T beta = (T)p.cg->beta;
+            T* pnew = const_cast<T*>(p.v);
+            for (int o = tid; o < no; o += NT) {
+                const int word = rld<TMA>(so + o);
+                const int64_t base = (int64_t)(word & OCC_NODE_MASK) * D;
+                T pn[D];
+#pragma unroll
+                for (int i = 0; i < D; ++i) {
+                    const T rv = __ldg(p.cg_r + base + i);
+                    const T z = p.cg_dinv ? __ldg(p.cg_dinv + base + i) * rv : rv;
+                    pn[i] = fma(beta, __ldg(p.cg_pold + base + i), z);
+                }
+#pragma unroll
+                for (int i = 0; i < D; ++i) {
+                    ust[o * D + i] = (MASKED && __ldg(p.mask + base + i)) ? T(0) : pn[i];
+                    if (!(word & OCC_NONOWNER)) pnew[base + i] = pn[i];
+                }
+            }
+            if (NF == 2) stage_fields<D, T, NT, ST, false>(ust + ust_sz, rgb, 0u, p.u, p, s0, nq, no);
+        } else if (OP == OP_TANGENT) {
             stage_fields<D, T, NT, ST, MASKED>(ust, rgb, 0u, p.v, p, s0, nq, no);
             if (NF == 2) stage_fields<D, T, NT, ST, false>(ust + ust_sz, rgb, 0u, p.u, p, s0, nq, no);
         } else {

@@ -138,6 +138,7 @@ k_cg_r0(int64_t n, const uint8_t* __restrict__ mask, const T* __restrict__ b, co
         cg->rho = dinv ? tz : t;
         cg->rho_new = t;
         cg->k = 0;
+        cg->beta = 0.0;   // the pipelined first iteration forms p = z + 0 p (= z, as k_cg_r0 wrote it)
         const double bn2 = cg->bnorm2;
         cg->pad0 = bn2 > 0 ? sqrt(t / bn2) : 0.0;   // rel_res0
         if (history) history[0] = cg->pad0;
@@ -379,7 +380,7 @@ k_cg_true(int64_t n, const uint8_t* __restrict__ mask, const T* __restrict__ b, 
 }
 
 struct CgWs {
-    size_t state, vr, r, p, q, b, dinv, asmws, total;
+    size_t state, vr, r, p, p2, q, b, dinv, asmws, total;
 };
 
 inline CgWs cg_layout(const Plan& P, size_t tsize) {
@@ -390,6 +391,7 @@ inline CgWs cg_layout(const Plan& P, size_t tsize) {
     L.vr = o;    o += align_up(sizeof(VecRed), 256);
     L.r = o;     o += nvec;
     L.p = o;     o += nvec;
+    L.p2 = o;    o += nvec;   // second direction buffer of the pipelined (CSR-mode) iteration
     L.q = o;     o += nvec;
     L.b = o;     o += nvec;
     L.dinv = o;  o += nvec;
@@ -405,7 +407,8 @@ size_t cg_ws_bytes(const Plan& P, int dtype) {
 template <int D, class T>
 static pfem_status tangent(const pfem_mesh* m, const Plan* P, const pfem_material* mat, const void* u,
                            const void* v, void* out, const uint8_t* mask, int mode, void* asmws, CgState* cg,
-                           cudaStream_t s) {
+                           cudaStream_t s, const void* fuse_r = nullptr, const void* fuse_pold = nullptr,
+                           const void* fuse_dinv = nullptr) {
     Call c{};
     c.m = m;
     c.P = P;
@@ -422,6 +425,9 @@ static pfem_status tangent(const pfem_mesh* m, const Plan* P, const pfem_materia
     c.ws = asmws;
     c.stream = s;
     c.cg = mode == PFEM_ASSEMBLE_CSR ? cg : nullptr;
+    c.cg_r = fuse_r;
+    c.cg_pold = fuse_pold;
+    c.cg_dinv = fuse_dinv;
     return run_assemble<D, T>(c);
 }
 
@@ -436,6 +442,7 @@ pfem_status cg_impl(const pfem_mesh* m, const pfem_material* mat, const void* u_
     VecRed* vr = (VecRed*)(w + L.vr);
     T* r = (T*)(w + L.r);
     T* p = (T*)(w + L.p);
+    T* p2 = (T*)(w + L.p2);
     T* q = (T*)(w + L.q);
     T* b = (T*)(w + L.b);
     T* dinv = precond ? (T*)(w + L.dinv) : nullptr;
@@ -473,7 +480,8 @@ pfem_status cg_impl(const pfem_mesh* m, const pfem_material* mat, const void* u_
     PFEM_CUDA_TRY(cudaStreamSynchronize(s));
     if (!h.done) {
         // capture B iterations into a graph on a private stream, replay on `s`
-        const int B = std::max(1, std::min(32, max_iter));
+        // an even B keeps the two direction buffers of the pipelined loop aligned across replays
+        const int B = std::max(1, std::min(32, max_iter + (max_iter & 1)));
         cudaStream_t cs;
         PFEM_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
         cudaGraph_t graph = nullptr;
@@ -482,7 +490,20 @@ pfem_status cg_impl(const pfem_mesh* m, const pfem_material* mat, const void* u_
         pfem_status ce = PFEM_OK;
         cudaError_t cerr = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
         if (cerr != cudaSuccess) { cudaStreamDestroy(cs); return cuda_status(cerr, "cudaStreamBeginCapture"); }
+        const bool fuse = mode == PFEM_ASSEMBLE_CSR;   // pipelined iteration (§8(f) row f3)
         for (int it = 0; it < B && ce == PFEM_OK; ++it) {
+            if (fuse) {
+                // K.v stages p_new = z + beta p_old from r and the other p buffer (its owners
+                // store p_new), kernel B forms p.q and alpha; then x, r, r.r and beta: 3 launches
+                T* pold = (it & 1) ? p2 : p;
+                T* pnew = (it & 1) ? p : p2;
+                ce = tangent<D, T>(m, P, mat, u_state, pnew, q, mask, mode, asmws, st, cs, r, pold, dinv);
+                if (ce != PFEM_OK) break;
+                if (dinv) k_cg_update<T, true><<<G, VEC_NT, 0, cs>>>(n, x, r, pnew, q, st, vr, history, dinv);
+                else k_cg_update<T, false><<<G, VEC_NT, 0, cs>>>(n, x, r, pnew, q, st, vr, history, nullptr);
+                count_launch();
+                continue;
+            }
             ce = tangent<D, T>(m, P, mat, u_state, p, q, mask, mode, asmws, st, cs);
             if (ce != PFEM_OK) break;
             if (mode != PFEM_ASSEMBLE_CSR) {

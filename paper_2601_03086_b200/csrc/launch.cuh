@@ -33,6 +33,9 @@ struct Call {
     size_t ws_bytes;
     cudaStream_t stream;
     CgState* cg;
+    const void* cg_r;      // pipelined CG direction update (AsmParams::cg_r)
+    const void* cg_pold;
+    const void* cg_dinv;
     // pretraining-loss epilogue (pretrain.cu): out = phi (.) (f_int - f_ext) / (S K), loss
     int ep;
     const void* ep_phi;
@@ -102,6 +105,9 @@ AsmParams<T> make_params(const Call& c) {
     p.partial = (T*)(w + L.partial);
     p.part_cnt = (int32_t*)(w + L.part_cnt);
     p.cg = c.cg;
+    p.cg_r = (const T*)c.cg_r;
+    p.cg_pold = (const T*)c.cg_pold;
+    p.cg_dinv = (const T*)c.cg_dinv;
     p.ep = c.ep;
     p.ep_phi = (const T*)c.ep_phi;
     p.ep_scale = (T)(1.0 / ((double)c.S * (double)P.n_parts));

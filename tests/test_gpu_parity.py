@@ -389,11 +389,12 @@ def test_cg_config4_scaled(orc, n):
     xs, _ = om.cg(p.f_ext, p.mask, np.zeros_like(p.f_ext), tol=1e-12, history=False)
     x0w = warm_start(xs, p.mask, seed=4004)
     for x0 in (np.zeros_like(p.f_ext), x0w):
-        for mode in ("csr", "colour"):
+        xo, ro = om.cg(p.f_ext, p.mask, x0, tol=1e-8)
+        spread = om.cg_spread(p.f_ext, p.mask, x0, tol=1e-8)
+        for mode in ("csr", "colour"):   # CSR: the pipelined iteration (§8(f) row f3)
             x, rep = pf.cg(mesh, mat, f, torch.as_tensor(x0, device="cuda"), mask=mask, tol=1e-8, mode=mode)
-            xo, ro = om.cg(p.f_ext, p.mask, x0, tol=1e-8)
             assert rep["converged"] and ro["converged"]
-            assert_cg_count(rep, ro, om.cg_spread(p.f_ext, p.mask, x0, tol=1e-8))
+            assert_cg_count(rep, ro, spread)
             assert rep["true_rel_res_final"] < 2e-8
             assert rel_l2(x.cpu().numpy(), xo) < 1e-6
 
@@ -548,12 +549,13 @@ def test_pcg_config4_scaled(orc, n):
     for x0 in (np.zeros_like(p.f_ext), x0w):
         xo, ro = om.pcg(p.f_ext, p.mask, x0, tol=1e-8)
         assert ro["converged"]
+        spread = om.pcg_spread(p.f_ext, p.mask, x0, tol=1e-8)
         for mode in ("csr", "colour"):
             x, rep = pf.cg(mesh, mat, f, torch.as_tensor(x0, device="cuda"), mask=mask, tol=1e-8, mode=mode,
                            precond="jacobi")
             assert rep["converged"]
             # reading R18 with the oracle PCG's own spread over the five dot orders
-            assert_cg_count(rep, ro, om.pcg_spread(p.f_ext, p.mask, x0, tol=1e-8))
+            assert_cg_count(rep, ro, spread)
             assert rep["true_rel_res_final"] < 2e-8
             assert rel_l2(x.cpu().numpy(), xo) < 1e-6
     # precond "none" through pfem_pcg is pfem_cg
