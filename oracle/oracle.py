@@ -369,3 +369,111 @@ def prepare_problem(prob) -> Mesh:
     """Oracle mesh for a pfem_gen.Problem."""
     pe, pn = prob.parts()
     return prepare(prob.coords, prob.conn, prob.model, prob.param_kind, prob.p0, prob.p1, pe, pn)
+
+
+# ------------------------------------------------------------------ quadrilaterals (§8(f) row f4)
+QUAD_TYPES = {"q4": 1, "q8": 2}
+
+
+def quad_shape(kind: str, xi: float, eta: float):
+    """Shape functions N [nv] and reference derivatives dN [nv, 2] of a Q4 / Q8 element."""
+    nv = 4 if kind == "q4" else 8
+    N = np.zeros(nv)
+    dN = np.zeros((nv, 2))
+    _check(lib().oracle_quad_shape(C.c_int(QUAD_TYPES[kind]), C.c_double(xi), C.c_double(eta), _p(N), _p(dN)),
+           "quad_shape")
+    return N, dN
+
+
+def quad_rule(kind: str):
+    """Gauss points [nq, 2] and weights [nq] (2 x 2 for Q4, 3 x 3 for Q8)."""
+    pts = np.zeros((9, 2))
+    w = np.zeros(9)
+    n = lib().oracle_quad_rule(C.c_int(QUAD_TYPES[kind]), _p(pts), _p(w))
+    return pts[:n].copy(), w[:n].copy()
+
+
+@dataclass
+class QuadMesh:
+    """Oracle-side Q4 / Q8 mesh (2-D, plane strain): geometry is formed per quadrature point."""
+    kind: str
+    coords: np.ndarray
+    conn: np.ndarray
+    mu: np.ndarray
+    lam: np.ndarray
+    model: str
+    part_elem: np.ndarray
+    part_node: np.ndarray
+
+    dim = 2
+
+    @property
+    def n_nodes(self):
+        return self.coords.shape[0]
+
+    @property
+    def n_elems(self):
+        return self.conn.shape[0]
+
+    def _args(self):
+        return (C.c_int(QUAD_TYPES[self.kind]), I64(self.n_nodes), I64(self.n_elems), _p(self.coords),
+                _p(self.conn), C.c_int(MODELS[self.model]), _p(self.mu), _p(self.lam))
+
+    def energy(self, u, f_ext=None, want_elem=True):
+        u = _f64(u).reshape(-1, self.n_nodes, 2)
+        S = u.shape[0]
+        K = len(self.part_elem) - 1
+        W = np.zeros((S, self.n_elems)) if want_elem else None
+        tot = np.zeros((S, K))
+        fe = None if f_ext is None else _f64(f_ext)
+        st = lib().oracle_quad_energy(*self._args(), C.c_int(S), _p(u), C.c_int(K), _p(self.part_elem),
+                                      _p(self.part_node), _p(fe), _p(W), _p(tot))
+        _check(st, "quad energy")
+        return W, tot
+
+    def residual(self, u):
+        u = _f64(u).reshape(-1, self.n_nodes, 2)
+        r = np.zeros_like(u)
+        _check(lib().oracle_quad_residual(*self._args(), C.c_int(u.shape[0]), _p(u), _p(r)), "quad residual")
+        return r
+
+    def tangent(self, v, u=None, mask=None):
+        v = _f64(v).reshape(-1, self.n_nodes, 2)
+        uu = None if u is None else _f64(u).reshape(v.shape)
+        m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
+        out = np.zeros_like(v)
+        _check(lib().oracle_quad_tangent(*self._args(), C.c_int(v.shape[0]), _p(uu), _p(v), _p(m), _p(out)),
+               "quad tangent")
+        return out
+
+    def cg(self, f, mask, x0, tol=1e-8, max_iter=50000, u_state=None, history=True, dot_order=0):
+        lib().oracle_set_dot_order(C.c_int(dot_order))
+        x = _f64(x0).copy().reshape(-1)
+        f = _f64(f).reshape(-1)
+        m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8).reshape(-1)
+        us = None if u_state is None else _f64(u_state).reshape(-1)
+        hist = np.zeros(max_iter + 1) if history else None
+        it = C.c_int32(0)
+        r0, rf, tr = C.c_double(0), C.c_double(0), C.c_double(0)
+        st = lib().oracle_quad_cg(*self._args(), _p(us), _p(f), _p(m), _p(x), C.c_double(tol), C.c_int32(max_iter),
+                                  _p(hist), C.byref(it), C.byref(r0), C.byref(rf), C.byref(tr))
+        lib().oracle_set_dot_order(C.c_int(0))
+        rep = {"status": st, "iterations": it.value, "converged": st == OK, "rel_res0": r0.value,
+               "rel_res_final": rf.value, "true_rel_res_final": tr.value,
+               "history": None if hist is None else hist[: it.value + 1].copy()}
+        return x.reshape(np.shape(x0)), rep
+
+    newton = Mesh.newton
+
+
+def prepare_quad(kind: str, coords, conn, model: str, param_kind: str, p0, p1, part_elem=None,
+                 part_node=None) -> QuadMesh:
+    coords = _f64(coords)
+    conn = _i32(conn)
+    md = C.c_double(0)
+    _check(lib().oracle_quad_check(C.c_int(QUAD_TYPES[kind]), I64(len(coords)), I64(len(conn)), _p(coords),
+                                   _p(conn), C.byref(md)), "quad check")
+    mu, lam = lame(param_kind, p0, p1, conn.shape[0])
+    pe = _i32(part_elem if part_elem is not None else [0, conn.shape[0]])
+    pn = _i32(part_node if part_node is not None else [0, coords.shape[0]])
+    return QuadMesh(kind, coords, conn, mu, lam, model, pe, pn)

@@ -688,12 +688,23 @@ double oracle_dot(int order, int64_t n, const double* a, const double* b) {
     return s;
 }
 
-int oracle_cg(int dim, int64_t n_nodes, int64_t n_elems, const int32_t* conn, const double* grad,
-              const double* vol, int model, const double* mu, const double* lam,
-              const double* u_state, const double* f, const uint8_t* mask, double* x, double tol,
-              int32_t max_iter, double* history, int32_t* iterations, double* rel_res0,
-              double* rel_res_final, double* true_rel_res_final) {
-    const int64_t n = n_nodes * dim;
+/* the operator of a CG solve: out = K v, or (I-M) K (I-M) v + M v when mask != NULL */
+typedef int (*or_apply)(void* ctx, const double* v, const uint8_t* mask, double* out);
+
+struct simplex_op {
+    int dim; int64_t n_nodes, n_elems; const int32_t* conn; const double* grad; const double* vol;
+    int model; const double* mu; const double* lam; const double* u_state;
+};
+static int simplex_apply(void* ctx, const double* v, const uint8_t* mask, double* out) {
+    const struct simplex_op* o = (const struct simplex_op*)ctx;
+    return oracle_tangent(o->dim, o->n_nodes, o->n_elems, o->conn, o->grad, o->vol, o->model, o->mu, o->lam, 1,
+                          o->u_state, v, mask, out);
+}
+
+/* Hestenes-Stiefel CG on the masked operator A (App. B, reading R8-R11) */
+static int cg_core(int64_t n, or_apply A, void* ctx, const double* f, const uint8_t* mask, double* x, double tol,
+                   int32_t max_iter, double* history, int32_t* iterations, double* rel_res0,
+                   double* rel_res_final, double* true_rel_res_final) {
     double* r = (double*)malloc(sizeof(double) * n);
     double* p = (double*)malloc(sizeof(double) * n);
     double* q = (double*)malloc(sizeof(double) * n);
@@ -703,11 +714,11 @@ int oracle_cg(int dim, int64_t n_nodes, int64_t n_elems, const int32_t* conn, co
     int st = OR_OK;
     /* b = (I - M)(f - K x_D): K x_D via the unmasked operator */
     for (int64_t i = 0; i < n; ++i) xd[i] = (mask && mask[i]) ? x[i] : 0.0;
-    oracle_tangent(dim, n_nodes, n_elems, conn, grad, vol, model, mu, lam, 1, u_state, xd, NULL, q);
+    A(ctx, xd, NULL, q);
     for (int64_t i = 0; i < n; ++i) b[i] = (mask && mask[i]) ? 0.0 : f[i] - q[i];
     double bnorm = sqrt(dot(n, b, b));
     /* r = b - A x over free DOFs (constrained rows of A x - (M x0) vanish) */
-    oracle_tangent(dim, n_nodes, n_elems, conn, grad, vol, model, mu, lam, 1, u_state, x, mask, q);
+    A(ctx, x, mask, q);
     for (int64_t i = 0; i < n; ++i) r[i] = (mask && mask[i]) ? 0.0 : b[i] - q[i];
     double rho = dot(n, r, r);
     *iterations = 0;
@@ -724,7 +735,7 @@ int oracle_cg(int dim, int64_t n_nodes, int64_t n_elems, const int32_t* conn, co
         memcpy(p, r, sizeof(double) * n);
         st = OR_ERR_NOT_CONVERGED;
         for (k = 1; k <= max_iter; ++k) {
-            oracle_tangent(dim, n_nodes, n_elems, conn, grad, vol, model, mu, lam, 1, u_state, p, mask, q);
+            A(ctx, p, mask, q);
             double pi = dot(n, p, q);
             if (!(pi > 0.0)) { st = OR_ERR_BREAKDOWN; break; }
             double alpha = rho / pi;
@@ -742,13 +753,23 @@ int oracle_cg(int dim, int64_t n_nodes, int64_t n_elems, const int32_t* conn, co
     *iterations = k;
     *rel_res_final = bnorm > 0 ? sqrt(rho) / bnorm : 0.0;
     /* true residual ||b - A x|| / ||b|| over free DOFs */
-    oracle_tangent(dim, n_nodes, n_elems, conn, grad, vol, model, mu, lam, 1, u_state, x, mask, q);
+    A(ctx, x, mask, q);
     double tr = 0.0;
     for (int64_t i = 0; i < n; ++i)
         if (!(mask && mask[i])) tr += (b[i] - q[i]) * (b[i] - q[i]);
     *true_rel_res_final = bnorm > 0 ? sqrt(tr) / bnorm : 0.0;
     free(r); free(p); free(q); free(xd); free(b);
     return st;
+}
+
+int oracle_cg(int dim, int64_t n_nodes, int64_t n_elems, const int32_t* conn, const double* grad,
+              const double* vol, int model, const double* mu, const double* lam,
+              const double* u_state, const double* f, const uint8_t* mask, double* x, double tol,
+              int32_t max_iter, double* history, int32_t* iterations, double* rel_res0,
+              double* rel_res_final, double* true_rel_res_final) {
+    struct simplex_op o = {dim, n_nodes, n_elems, conn, grad, vol, model, mu, lam, u_state};
+    return cg_core(n_nodes * dim, simplex_apply, &o, f, mask, x, tol, max_iter, history, iterations, rel_res0,
+                   rel_res_final, true_rel_res_final);
 }
 
 /* ------------------------------------------------------------------ */
@@ -923,4 +944,372 @@ int oracle_heat(int dim, int64_t n_nodes, int64_t n_elems, const int32_t* conn, 
         }
     }
     return OR_OK;
+}
+
+/* ================================================================== */
+/* Quadrilateral elements with Gauss quadrature:  */
+/* Q4 bilinear (2x2 Gauss) and Q8 serendipity (3x3 Gauss), 2-D plane    */
+/* strain, isoparametric (App. B: x = N_I x_I, X = N_I X_I), */
+/* the same constitutive laws as the simplex functions (P:527-536,      */
+/* P:709-722), each element integral evaluated by its Gauss rule: the   */
+/* beam's 50 x 50 Q4 mesh (§4.2) and Cook's 30 x 30 Q8 serendipity */
+/* mesh.  Reading R33: node order, rules.           */
+/* ================================================================== */
+#define OR_Q4 1
+#define OR_Q8 2
+
+static int quad_nv(int type) { return type == OR_Q4 ? 4 : 8; }
+
+/* reference coordinates of the nodes: corners counter-clockwise from (-1,-1), then the midsides
+ * (0,-1), (1,0), (0,1), (-1,0) (Q8 only) */
+static const double QXI[8][2] = {{-1, -1}, {1, -1}, {1, 1}, {-1, 1}, {0, -1}, {1, 0}, {0, 1}, {-1, 0}};
+
+/* shape functions N_a(xi, eta) and their reference derivatives dN[a][0] = dN_a/dxi,
+ * dN[a][1] = dN_a/deta */
+int oracle_quad_shape(int type, double xi, double eta, double* N, double* dN) {
+    if (type == OR_Q4) {
+        for (int a = 0; a < 4; ++a) {
+            const double xa = QXI[a][0], ya = QXI[a][1];
+            N[a] = 0.25 * (1.0 + xi * xa) * (1.0 + eta * ya);
+            dN[2 * a + 0] = 0.25 * xa * (1.0 + eta * ya);
+            dN[2 * a + 1] = 0.25 * ya * (1.0 + xi * xa);
+        }
+        return OR_OK;
+    }
+    if (type != OR_Q8) return OR_ERR_ARG;
+    for (int a = 0; a < 4; ++a) {   /* corners: 1/4 (1 + xi xa)(1 + eta ya)(xi xa + eta ya - 1) */
+        const double xa = QXI[a][0], ya = QXI[a][1];
+        N[a] = 0.25 * (1.0 + xi * xa) * (1.0 + eta * ya) * (xi * xa + eta * ya - 1.0);
+        dN[2 * a + 0] = 0.25 * xa * (1.0 + eta * ya) * (2.0 * xi * xa + eta * ya);
+        dN[2 * a + 1] = 0.25 * ya * (1.0 + xi * xa) * (xi * xa + 2.0 * eta * ya);
+    }
+    for (int a = 4; a < 8; ++a) {
+        const double xa = QXI[a][0], ya = QXI[a][1];
+        if (xa == 0.0) {            /* 1/2 (1 - xi^2)(1 + eta ya) */
+            N[a] = 0.5 * (1.0 - xi * xi) * (1.0 + eta * ya);
+            dN[2 * a + 0] = -xi * (1.0 + eta * ya);
+            dN[2 * a + 1] = 0.5 * ya * (1.0 - xi * xi);
+        } else {                    /* 1/2 (1 + xi xa)(1 - eta^2) */
+            N[a] = 0.5 * (1.0 + xi * xa) * (1.0 - eta * eta);
+            dN[2 * a + 0] = 0.5 * xa * (1.0 - eta * eta);
+            dN[2 * a + 1] = -eta * (1.0 + xi * xa);
+        }
+    }
+    return OR_OK;
+}
+
+/* tensor-product Gauss-Legendre rule: 2 x 2 for Q4, 3 x 3 for Q8; points eta-major */
+int oracle_quad_rule(int type, double* pts, double* w) {
+    const double g2[2] = {-1.0 / sqrt(3.0), 1.0 / sqrt(3.0)}, w2[2] = {1.0, 1.0};
+    const double g3[3] = {-sqrt(0.6), 0.0, sqrt(0.6)}, w3[3] = {5.0 / 9.0, 8.0 / 9.0, 5.0 / 9.0};
+    const int m = type == OR_Q4 ? 2 : 3;
+    const double* g = type == OR_Q4 ? g2 : g3;
+    const double* wg = type == OR_Q4 ? w2 : w3;
+    int k = 0;
+    for (int j = 0; j < m; ++j)
+        for (int i = 0; i < m; ++i, ++k) {
+            pts[2 * k] = g[i];
+            pts[2 * k + 1] = g[j];
+            w[k] = wg[i] * wg[j];
+        }
+    return k;
+}
+
+/* geometry at one quadrature point: J_ij = sum_a X_{a,i} dN_a/dxi_j, dN_a/dX = dN_a/dxi J^-1;
+ * returns det J */
+static double quad_qp(int type, const double* coords, const int32_t* c, double xi, double eta, double dNdX[8][2]) {
+    const int nv = quad_nv(type);
+    double N[8], dN[16];
+    oracle_quad_shape(type, xi, eta, N, dN);
+    double J[2][2] = {{0, 0}, {0, 0}};
+    for (int a = 0; a < nv; ++a)
+        for (int i = 0; i < 2; ++i)
+            for (int j = 0; j < 2; ++j) J[i][j] += coords[(int64_t)c[a] * 2 + i] * dN[2 * a + j];
+    const double det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    const double Ji[2][2] = {{J[1][1] / det, -J[0][1] / det}, {-J[1][0] / det, J[0][0] / det}};
+    for (int a = 0; a < nv; ++a)
+        for (int k = 0; k < 2; ++k) dNdX[a][k] = dN[2 * a] * Ji[0][k] + dN[2 * a + 1] * Ji[1][k];
+    return det;
+}
+
+/* smallest det J over every element's quadrature points (validity: > 0) */
+int oracle_quad_check(int type, int64_t n_nodes, int64_t n_elems, const double* coords, const int32_t* conn,
+                      double* min_det) {
+    if (type != OR_Q4 && type != OR_Q8) return OR_ERR_ARG;
+    const int nv = quad_nv(type);
+    double pts[18], w[9];
+    const int nq = oracle_quad_rule(type, pts, w);
+    double m = INFINITY;
+    int64_t bad = -1;
+    for (int64_t e = 0; e < n_elems; ++e) {
+        for (int a = 0; a < nv; ++a)
+            if (conn[e * nv + a] < 0 || conn[e * nv + a] >= n_nodes) { g_err_index = e; return OR_ERR_ARG; }
+        for (int q = 0; q < nq; ++q) {
+            double dNdX[8][2];
+            const double det = quad_qp(type, coords, conn + e * nv, pts[2 * q], pts[2 * q + 1], dNdX);
+            if (det < m) m = det;
+            if (!(det > 0.0) && bad < 0) bad = e;
+        }
+    }
+    *min_det = m;
+    if (bad >= 0) { g_err_index = bad; return OR_ERR_DEGENERATE; }
+    return OR_OK;
+}
+
+/* Voigt B (eps11, eps22, 2 eps12) of a 2-D element with nv nodes, column a*2 + i */
+static void quad_B(int nv, double g[8][2], double B[3][16]) {
+    memset(B, 0, sizeof(double) * 3 * 16);
+    for (int a = 0; a < nv; ++a) {
+        B[0][2 * a + 0] = g[a][0];
+        B[1][2 * a + 1] = g[a][1];
+        B[2][2 * a + 0] = g[a][1];
+        B[2][2 * a + 1] = g[a][0];
+    }
+}
+
+/* F = I + sum_a u_a (x) grad N_a (isoparametric) */
+static void quad_F(int nv, const int32_t* c, const double* u, double g[8][2], double F[3][3]) {
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) F[i][j] = (i == j) ? 1.0 : 0.0;
+    for (int a = 0; a < nv; ++a)
+        for (int i = 0; i < 2; ++i)
+            for (int j = 0; j < 2; ++j) F[i][j] += u[(int64_t)c[a] * 2 + i] * g[a][j];
+}
+
+/* element energy and internal force of one quadrature point, accumulated with weight wd = w det J */
+static int quad_point(int nv, int model, double g[8][2], double wd, double mu, double lam, const int32_t* c,
+                      const double* u, double* W, double* f) {
+    if (model == OR_LINEAR) {
+        double B[3][16], D[6][6], eps[3] = {0, 0, 0}, sig[3] = {0, 0, 0};
+        quad_B(nv, g, B);
+        voigt_D(2, mu, lam, D);
+        for (int r = 0; r < 3; ++r)
+            for (int a = 0; a < nv; ++a)
+                for (int i = 0; i < 2; ++i) eps[r] += B[r][2 * a + i] * u[(int64_t)c[a] * 2 + i];
+        for (int r = 0; r < 3; ++r)
+            for (int q = 0; q < 3; ++q) sig[r] += D[r][q] * eps[q];
+        if (W) {
+            double psi = 0.0;
+            for (int r = 0; r < 3; ++r) psi += 0.5 * sig[r] * eps[r];
+            *W += wd * psi;
+        }
+        if (f)
+            for (int k = 0; k < 2 * nv; ++k) {
+                double acc = 0.0;
+                for (int r = 0; r < 3; ++r) acc += B[r][k] * sig[r];
+                f[k] += wd * acc;
+            }
+        return OR_OK;
+    }
+    double F[3][3], S[3][3], Ci[3][3], J, lnJ, psi;
+    quad_F(nv, c, u, g, F);
+    const int st = nh_state(2, F, mu, lam, S, Ci, &J, &lnJ, &psi);
+    if (W) *W += wd * psi;
+    if (f)
+        for (int a = 0; a < nv; ++a)
+            for (int i = 0; i < 2; ++i) {
+                double acc = 0.0;
+                for (int k = 0; k < 2; ++k)
+                    for (int l = 0; l < 2; ++l) acc += g[a][l] * F[i][k] * S[k][l];
+                f[2 * a + i] += wd * acc;
+            }
+    return st;
+}
+
+/* K_e v_e of one quadrature point (linear: B^T D B v; NH: B0^T C^SE B0 v + G0^T S G0 v), added
+ * with weight wd */
+static int quad_point_tangent(int nv, int model, double g[8][2], double wd, double mu, double lam,
+                              const int32_t* c, const double* u, const double* ve, double* out) {
+    double B[3][16], D[6][6], S[3][3] = {{0}};
+    int st = OR_OK;
+    if (model == OR_LINEAR) {
+        quad_B(nv, g, B);
+        voigt_D(2, mu, lam, D);
+    } else {
+        double F[3][3], Ci[3][3], J, lnJ, psi;
+        quad_F(nv, c, u, g, F);
+        st = nh_state(2, F, mu, lam, S, Ci, &J, &lnJ, &psi);
+        for (int x = 0; x < 3; ++x)
+            for (int y = 0; y < 3; ++y) {
+                int I = VI2[x][0], Jx = VI2[x][1], K2 = VI2[y][0], L = VI2[y][1];
+                D[x][y] = lam * Ci[I][Jx] * Ci[K2][L] + (mu - lam * lnJ) * (Ci[I][K2] * Ci[Jx][L] + Ci[I][L] * Ci[Jx][K2]);
+            }
+        memset(B, 0, sizeof(B));
+        for (int x = 0; x < 3; ++x) {
+            int Kk = VI2[x][0], L = VI2[x][1];
+            for (int a = 0; a < nv; ++a)
+                for (int i = 0; i < 2; ++i)
+                    B[x][2 * a + i] = (Kk == L) ? F[i][Kk] * g[a][L] : F[i][Kk] * g[a][L] + F[i][L] * g[a][Kk];
+        }
+    }
+    double eps[3], sig[3];
+    for (int x = 0; x < 3; ++x) {
+        double acc = 0.0;
+        for (int q = 0; q < 2 * nv; ++q) acc += B[x][q] * ve[q];
+        eps[x] = acc;
+    }
+    for (int x = 0; x < 3; ++x) {
+        double acc = 0.0;
+        for (int y = 0; y < 3; ++y) acc += D[x][y] * eps[y];
+        sig[x] = acc;
+    }
+    for (int p = 0; p < 2 * nv; ++p) {
+        double acc = 0.0;
+        for (int x = 0; x < 3; ++x) acc += B[x][p] * sig[x];
+        out[p] += wd * acc;
+    }
+    if (model != OR_LINEAR)
+        for (int a = 0; a < nv; ++a)
+            for (int b = 0; b < nv; ++b) {
+                double gsg = 0.0;
+                for (int k = 0; k < 2; ++k)
+                    for (int l = 0; l < 2; ++l) gsg += g[a][k] * S[k][l] * g[b][l];
+                for (int i = 0; i < 2; ++i) out[2 * a + i] += wd * gsg * ve[2 * b + i];
+            }
+    return st;
+}
+
+/* energy, internal force and tangent of Q4 / Q8 meshes: element integrals by the Gauss rule,
+ * per-element outputs, node sums sequential in ascending (element, node) order (as the simplex
+ * functions); totals W_{s,k} - f_ext . u per part (reading R6) */
+int oracle_quad_energy(int type, int64_t n_nodes, int64_t n_elems, const double* coords, const int32_t* conn,
+                       int model, const double* mu, const double* lam, int n_samples, const double* u,
+                       int n_parts, const int32_t* part_elem, const int32_t* part_node, const double* f_ext,
+                       double* W_e, double* totals) {
+    const int nv = quad_nv(type);
+    double pts[18], w[9];
+    const int nq = oracle_quad_rule(type, pts, w);
+    double* W = W_e ? W_e : (double*)malloc(sizeof(double) * (size_t)n_elems * n_samples);
+    if (!W) return OR_ERR_CAPACITY;
+    int64_t first_bad = -1;
+    for (int s = 0; s < n_samples; ++s) {
+        const double* us = u + (int64_t)s * n_nodes * 2;
+#pragma omp parallel for schedule(static)
+        for (int64_t e = 0; e < n_elems; ++e) {
+            double We = 0.0;
+            for (int q = 0; q < nq; ++q) {
+                double g[8][2];
+                const double det = quad_qp(type, coords, conn + e * nv, pts[2 * q], pts[2 * q + 1], g);
+                if (quad_point(nv, model, g, w[q] * det, mu[e], lam[e], conn + e * nv, us, &We, NULL) != OR_OK) {
+#pragma omp critical
+                    { if (first_bad < 0 || e < first_bad) first_bad = e; }
+                }
+            }
+            W[(int64_t)s * n_elems + e] = We;
+        }
+        for (int k = 0; k < n_parts; ++k) {
+            double acc = 0.0;
+            for (int64_t e = part_elem[k]; e < part_elem[k + 1]; ++e) acc += W[(int64_t)s * n_elems + e];
+            if (f_ext) {
+                double work = 0.0;
+                for (int64_t n = part_node[k]; n < part_node[k + 1]; ++n)
+                    for (int i = 0; i < 2; ++i) work += f_ext[n * 2 + i] * us[n * 2 + i];
+                acc -= work;
+            }
+            totals[(int64_t)s * n_parts + k] = acc;
+        }
+    }
+    if (!W_e) free(W);
+    if (first_bad >= 0) { g_err_index = first_bad; return OR_ERR_INVERTED; }
+    return OR_OK;
+}
+
+int oracle_quad_residual(int type, int64_t n_nodes, int64_t n_elems, const double* coords, const int32_t* conn,
+                         int model, const double* mu, const double* lam, int n_samples, const double* u,
+                         double* r) {
+    const int nv = quad_nv(type), ne = 2 * nv;
+    double pts[18], w[9];
+    const int nq = oracle_quad_rule(type, pts, w);
+    double* fe = (double*)malloc(sizeof(double) * (size_t)n_elems * ne);
+    if (!fe) return OR_ERR_CAPACITY;
+    int64_t first_bad = -1;
+    for (int s = 0; s < n_samples; ++s) {
+        const double* us = u + (int64_t)s * n_nodes * 2;
+        double* rs = r + (int64_t)s * n_nodes * 2;
+#pragma omp parallel for schedule(static)
+        for (int64_t e = 0; e < n_elems; ++e) {
+            double* f = fe + e * ne;
+            for (int k = 0; k < ne; ++k) f[k] = 0.0;
+            for (int q = 0; q < nq; ++q) {
+                double g[8][2];
+                const double det = quad_qp(type, coords, conn + e * nv, pts[2 * q], pts[2 * q + 1], g);
+                if (quad_point(nv, model, g, w[q] * det, mu[e], lam[e], conn + e * nv, us, NULL, f) != OR_OK) {
+#pragma omp critical
+                    { if (first_bad < 0 || e < first_bad) first_bad = e; }
+                }
+            }
+        }
+        for (int64_t k = 0; k < n_nodes * 2; ++k) rs[k] = 0.0;
+        for (int64_t e = 0; e < n_elems; ++e)
+            for (int a = 0; a < nv; ++a)
+                for (int i = 0; i < 2; ++i) rs[(int64_t)conn[e * nv + a] * 2 + i] += fe[e * ne + 2 * a + i];
+    }
+    free(fe);
+    if (first_bad >= 0) { g_err_index = first_bad; return OR_ERR_INVERTED; }
+    return OR_OK;
+}
+
+int oracle_quad_tangent(int type, int64_t n_nodes, int64_t n_elems, const double* coords, const int32_t* conn,
+                        int model, const double* mu, const double* lam, int n_samples, const double* u,
+                        const double* v, const uint8_t* mask, double* Kv) {
+    const int nv = quad_nv(type), ne = 2 * nv;
+    double pts[18], w[9];
+    const int nq = oracle_quad_rule(type, pts, w);
+    double* fe = (double*)malloc(sizeof(double) * (size_t)n_elems * ne);
+    if (!fe) return OR_ERR_CAPACITY;
+    int64_t first_bad = -1;
+    for (int s = 0; s < n_samples; ++s) {
+        const double* vs = v + (int64_t)s * n_nodes * 2;
+        const double* us = u ? u + (int64_t)s * n_nodes * 2 : NULL;
+        double* out = Kv + (int64_t)s * n_nodes * 2;
+#pragma omp parallel for schedule(static)
+        for (int64_t e = 0; e < n_elems; ++e) {
+            const int32_t* c = conn + e * nv;
+            double ve[16];
+            for (int a = 0; a < nv; ++a)
+                for (int i = 0; i < 2; ++i) {
+                    const int64_t dof = (int64_t)c[a] * 2 + i;
+                    ve[2 * a + i] = (mask && mask[dof]) ? 0.0 : vs[dof];
+                }
+            double* f = fe + e * ne;
+            for (int k = 0; k < ne; ++k) f[k] = 0.0;
+            for (int q = 0; q < nq; ++q) {
+                double g[8][2];
+                const double det = quad_qp(type, coords, c, pts[2 * q], pts[2 * q + 1], g);
+                if (quad_point_tangent(nv, model, g, w[q] * det, mu[e], lam[e], c, us, ve, f) != OR_OK) {
+#pragma omp critical
+                    { if (first_bad < 0 || e < first_bad) first_bad = e; }
+                }
+            }
+        }
+        for (int64_t k = 0; k < n_nodes * 2; ++k) out[k] = 0.0;
+        for (int64_t e = 0; e < n_elems; ++e)
+            for (int a = 0; a < nv; ++a)
+                for (int i = 0; i < 2; ++i) out[(int64_t)conn[e * nv + a] * 2 + i] += fe[e * ne + 2 * a + i];
+        if (mask)
+            for (int64_t k = 0; k < n_nodes * 2; ++k)
+                if (mask[k]) out[k] = vs[k];
+    }
+    free(fe);
+    if (first_bad >= 0) { g_err_index = first_bad; return OR_ERR_INVERTED; }
+    return OR_OK;
+}
+
+struct quad_op {
+    int type; int64_t n_nodes, n_elems; const double* coords; const int32_t* conn;
+    int model; const double* mu; const double* lam; const double* u_state;
+};
+static int quad_apply(void* ctx, const double* v, const uint8_t* mask, double* out) {
+    const struct quad_op* o = (const struct quad_op*)ctx;
+    return oracle_quad_tangent(o->type, o->n_nodes, o->n_elems, o->coords, o->conn, o->model, o->mu, o->lam, 1,
+                               o->u_state, v, mask, out);
+}
+
+int oracle_quad_cg(int type, int64_t n_nodes, int64_t n_elems, const double* coords, const int32_t* conn,
+                   int model, const double* mu, const double* lam, const double* u_state, const double* f,
+                   const uint8_t* mask, double* x, double tol, int32_t max_iter, double* history,
+                   int32_t* iterations, double* rel_res0, double* rel_res_final, double* true_rel_res_final) {
+    struct quad_op o = {type, n_nodes, n_elems, coords, conn, model, mu, lam, u_state};
+    return cg_core(n_nodes * 2, quad_apply, &o, f, mask, x, tol, max_iter, history, iterations, rel_res0,
+                   rel_res_final, true_rel_res_final);
 }

@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from .meshes import (boundary_faces_on_plane, fourier_field, kuhn_cube,
-                     plate_with_holes, square_t3)
+                     plate_with_holes, quad_grid, square_t3)
 
 
 @dataclass
@@ -38,6 +38,7 @@ class Problem:
     f_ext: np.ndarray | None = None     # [N, d] float64
     mask: np.ndarray | None = None      # [N*d] uint8, 1 = Dirichlet DOF
     meta: dict = field(default_factory=dict)
+    elem: str = "simplex"               # "simplex" (T3 / T4) | "q4" | "q8"
 
     @property
     def n_nodes(self):
@@ -209,6 +210,68 @@ def newton_block(n_nodes: int = 9, traction=(0.02, 0.0, 0.01), mu: float = 0.4, 
     u = np.zeros((1,) + coords.shape)
     return Problem("newton_block", 3, coords, conn, "neohookean", "lame", np.array([mu]), np.array([lam]),
                    u, dtype, f_ext=f_ext, mask=mask.ravel())
+
+
+def _edge_loads(coords, nodes, traction_y):
+    """Nodal loads on a straight boundary edge (input data, no shape-function arithmetic): each
+    edge node receives t_y(y_n) times its tributary length (half the distance to each neighbour
+    along the edge), in the y direction."""
+    ys = coords[nodes, 1]
+    order = np.argsort(ys)
+    nodes, ys = nodes[order], ys[order]
+    trib = np.zeros(len(nodes))
+    gaps = np.diff(ys)
+    trib[:-1] += 0.5 * gaps
+    trib[1:] += 0.5 * gaps
+    f = np.zeros_like(coords)
+    f[nodes, 1] = traction_y(ys) * trib * np.hypot(1.0, 0.0)
+    return f
+
+
+def beam_q4(n_cells: int = 50, seed_base: int = 6000, t_scale: float = 1e-3, dtype: str = "f64") -> Problem:
+    """Hyperelastic beam (§4.2): W x H = 4 x 1, uniform n x n Q4 mesh (50 x 50 = 2500
+    elements), compressible Neo-Hookean, plane strain; left end x = 0 clamped; downward
+    traction t_y(y) on the right end x = 4 as nodal loads; E and nu per element from smooth
+    random fields (stand-ins for the paper's Gaussian random fields): E = 1 + 0.5 tanh(Phi_1),
+    nu = 0.3 + 0.05 tanh(Phi_2) at the element centroid; t_y = -t_scale (1 + 0.5 tanh(Phi_3(y))).
+    S = 1; ``u`` is the zero start."""
+    coords, conn = quad_grid(n_cells, n_cells, "q4", corners=((0, 0), (4, 0), (4, 1), (0, 1)))
+    rng = np.random.default_rng(seed_base + 2)
+    cen = coords[conn].mean(axis=1)
+    E = 1.0 + 0.5 * np.tanh(fourier_field(cen / 4.0, rng)[:, 0] * 4.0)
+    nu = 0.3 + 0.05 * np.tanh(fourier_field(cen / 4.0, rng)[:, 0] * 4.0)
+    phi3 = fourier_field(np.stack([np.zeros(len(coords)), coords[:, 1]], 1), rng)[:, 1]
+    right = np.where(np.abs(coords[:, 0] - 4.0) < 1e-12)[0]
+    tvals = dict(zip(coords[right, 1], -t_scale * (1.0 + 0.5 * np.tanh(4.0 * phi3[right]))))
+    f_ext = _edge_loads(coords, right, lambda ys: np.array([tvals[y] for y in ys]))
+    mask = np.zeros((len(coords), 2), np.uint8)
+    mask[np.abs(coords[:, 0]) < 1e-12, :] = 1
+    u = np.zeros((1,) + coords.shape)
+    return Problem("beam_q4", 2, coords, conn, "neohookean", "young_poisson", E, nu, u, dtype, f_ext=f_ext,
+                   mask=mask.ravel(), elem="q4")
+
+
+def cook_q8(n_cells: int = 30, seed_base: int = 7000, t_scale: float = 2e-3, dtype: str = "f64") -> Problem:
+    """Hyperelastic Cook's membrane (§4.2): the classical tapered panel with corners
+    (0, 0), (48, 44), (48, 60), (0, 44), uniform n x n Q8 serendipity mesh (30 x 30 = 900
+    elements), compressible Neo-Hookean, plane strain; left edge x = 0 clamped; traction
+    t_y on the right edge x = 48 as nodal loads; E, nu per element from smooth random fields
+    (E = 1 + 0.5 tanh(Phi_1), nu = 0.3 + 0.05 tanh(Phi_2)); t_y = t_scale (1 + 0.5 tanh(Phi_3(y))).
+    S = 1; ``u`` is the zero start."""
+    coords, conn = quad_grid(n_cells, n_cells, "q8", corners=((0, 0), (48, 44), (48, 60), (0, 44)))
+    rng = np.random.default_rng(seed_base + 2)
+    cen = coords[conn[:, :4]].mean(axis=1)
+    E = 1.0 + 0.5 * np.tanh(fourier_field(cen / 60.0, rng)[:, 0] * 4.0)
+    nu = 0.3 + 0.05 * np.tanh(fourier_field(cen / 60.0, rng)[:, 0] * 4.0)
+    phi3 = fourier_field(np.stack([np.zeros(len(coords)), coords[:, 1] / 60.0], 1), rng)[:, 1]
+    right = np.where(np.abs(coords[:, 0] - 48.0) < 1e-9)[0]
+    tvals = dict(zip(coords[right, 1], t_scale * (1.0 + 0.5 * np.tanh(4.0 * phi3[right]))))
+    f_ext = _edge_loads(coords, right, lambda ys: np.array([tvals[y] for y in ys]))
+    mask = np.zeros((len(coords), 2), np.uint8)
+    mask[np.abs(coords[:, 0]) < 1e-12, :] = 1
+    u = np.zeros((1,) + coords.shape)
+    return Problem("cook_q8", 2, coords, conn, "neohookean", "young_poisson", E, nu, u, dtype, f_ext=f_ext,
+                   mask=mask.ravel(), elem="q8")
 
 
 CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}

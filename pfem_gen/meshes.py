@@ -173,3 +173,48 @@ def fourier_field(X: np.ndarray, rng: np.random.Generator, n_modes: int = 8, kma
     for c in range(d):
         out[:, c] = (np.sin(arg + ph[c][None, :]) * (a[c] / (2 * np.pi * knorm))[None, :]).sum(1)
     return out
+
+
+# --------------------------------------------------------------------------
+# 2-D structured quadrilateral meshes (Q4 / Q8), §8(f) row f4
+# --------------------------------------------------------------------------
+def quad_grid(nx: int, ny: int, kind: str = "q4", corners=((0.0, 0.0), (1.0, 0.0), (1.0, 1.0), (0.0, 1.0))):
+    """Structured nx x ny quadrilateral mesh of the bilinear map of the unit square onto the
+    quadrilateral `corners` (counter-clockwise A, B, C, D: (s,t) -> (1-s)(1-t)A + s(1-t)B + stC
+    + (1-s)tD).  kind "q4": (nx+1)(ny+1) nodes x-fastest, element (i, j) = (n00, n10, n11, n01),
+    counter-clockwise.  kind "q8": serendipity — the (2nx+1)(2ny+1) half-step grid without the
+    cell centres, renumbered in x-fastest order ((2nx+1)(2ny+1) - nx ny nodes); element nodes
+    are the four corners (counter-clockwise) then the midsides of edges 01, 12, 23, 30.  Every
+    cell edge is straight (the map is linear along s and t), so midside nodes are edge
+    midpoints.  Returns coords [N,2] float64, conn [E,4|8] int32."""
+    A, B, Cc, D = (np.asarray(c, np.float64) for c in corners)
+
+    def emap(s, t):
+        return ((1 - s) * (1 - t))[:, None] * A + (s * (1 - t))[:, None] * B + (s * t)[:, None] * Cc + \
+            ((1 - s) * t)[:, None] * D
+
+    if kind == "q4":
+        i, j = np.meshgrid(np.arange(nx + 1), np.arange(ny + 1), indexing="xy")
+        coords = emap(i.ravel() / nx, j.ravel() / ny)
+        ci, cj = np.meshgrid(np.arange(nx), np.arange(ny), indexing="xy")
+        n00 = (cj * (nx + 1) + ci).ravel()
+        conn = np.stack([n00, n00 + 1, n00 + nx + 2, n00 + nx + 1], axis=1)
+        return coords, conn.astype(np.int32)
+    if kind != "q8":
+        raise ValueError(kind)
+    mx, my = 2 * nx + 1, 2 * ny + 1
+    i, j = np.meshgrid(np.arange(mx), np.arange(my), indexing="xy")
+    i, j = i.ravel(), j.ravel()
+    keep = ~((i % 2 == 1) & (j % 2 == 1))
+    new_id = np.full(mx * my, -1, np.int64)
+    new_id[keep] = np.arange(int(keep.sum()))
+    coords = emap(i[keep] / (2 * nx), j[keep] / (2 * ny))
+    ci, cj = np.meshgrid(np.arange(nx), np.arange(ny), indexing="xy")
+    ci, cj = 2 * ci.ravel(), 2 * cj.ravel()
+
+    def g(a, b):
+        return new_id[b * mx + a]
+
+    conn = np.stack([g(ci, cj), g(ci + 2, cj), g(ci + 2, cj + 2), g(ci, cj + 2),
+                     g(ci + 1, cj), g(ci + 2, cj + 1), g(ci + 1, cj + 2), g(ci, cj + 1)], axis=1)
+    return coords, conn.astype(np.int32)
