@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define PFEM_ABI_VERSION 5
+#define PFEM_ABI_VERSION 6
 
 typedef enum {
     PFEM_OK = 0,
@@ -95,6 +95,14 @@ typedef enum {
                                       the solvers built on them; COLOUR mode reads grad / vol      */
 } pfem_geometry;
 
+/* Element family (SURVEY §8(f) row f4 for the quadrilaterals). */
+typedef enum {
+    PFEM_ELEM_SIMPLEX = 0,   /* P1 triangles (dim 2) / tetrahedra (dim 3), one-point rule (reading R4)  */
+    PFEM_ELEM_Q4 = 1,        /* bilinear quadrilateral, 2 x 2 Gauss (dim 2; beam P:774)              */
+    PFEM_ELEM_Q8 = 2         /* serendipity quadrilateral, 3 x 3 Gauss (dim 2; Cook P:846); nodes:
+                                4 corners counter-clockwise, then midsides of edges 01, 12, 23, 30   */
+} pfem_elem_type;
+
 typedef struct pfem_plan pfem_plan;   /* opaque, library-owned device data */
 
 /* Mesh descriptor.  Inputs are set by the caller; pfem_mesh_prepare fills the outputs. */
@@ -109,6 +117,10 @@ typedef struct {
                                       elements in a locality order; results are unchanged up to
                                       rounding and are reported in input element order           */
     int32_t geometry;              /* pfem_geometry; may change between calls (coords must stay valid) */
+    int32_t elem_type;             /* pfem_elem_type; conn is [n_elems][nodes per element].  Q4 / Q8:
+                                      dim 2, CSR assembly only, no Jacobi / heat / pretraining calls;
+                                      grad / vol are not written (the Gauss-point geometry lives in
+                                      the plan)                                                     */
     const double* coords;          /* [n_nodes][dim], float64 always                             */
     const int32_t* conn;           /* [n_elems][dim+1], node ids in [0, n_nodes)                 */
     const int32_t* part_elem;      /* [n_parts+1] element offsets (device), NULL if n_parts == 1 */

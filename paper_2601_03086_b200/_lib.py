@@ -24,6 +24,7 @@ class pfem_mesh(C.Structure):
     _fields_ = [
         ("dim", C.c_int32), ("n_nodes", C.c_int32), ("n_elems", C.c_int32), ("n_parts", C.c_int32),
         ("dtype", C.c_int32), ("block_elems", C.c_int32), ("elem_order", C.c_int32), ("geometry", C.c_int32),
+        ("elem_type", C.c_int32),
         ("coords", C.c_void_p), ("conn", C.c_void_p), ("part_elem", C.c_void_p), ("part_node", C.c_void_p),
         ("grad", C.c_void_p), ("vol", C.c_void_p), ("csr_ptr", C.c_void_p), ("csr_ent", C.c_void_p),
         ("colour", C.c_void_p), ("colour_elems", C.c_void_p), ("colour_ptr", C.c_void_p),

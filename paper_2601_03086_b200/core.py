@@ -35,6 +35,7 @@ def _require_cuda(*ts):
 
 
 GEOMETRY = {"stored": 0, "on_the_fly": 1}
+ELEM_TYPES = {"simplex": 0, "q4": 1, "q8": 2}
 
 
 class Mesh:
@@ -42,7 +43,7 @@ class Mesh:
 
     def __init__(self, coords: torch.Tensor, conn: torch.Tensor, dtype=torch.float64, part_elem=None,
                  part_node=None, block_elems: int = 0, max_colours: int = 128, stream=None,
-                 elem_order: str = "auto", geometry: str = "stored"):
+                 elem_order: str = "auto", geometry: str = "stored", elem_type: str = "simplex"):
         lib = L.load()
         _require_cuda(coords, conn)
         dev = coords.device
@@ -50,8 +51,12 @@ class Mesh:
         self.conn = conn.to(torch.int32).contiguous()
         N, d = self.coords.shape
         E = self.conn.shape[0]
-        if self.conn.shape[1] != d + 1:
-            raise ValueError("conn must be [E, dim+1]")
+        nv = {"simplex": d + 1, "q4": 4, "q8": 8}[elem_type]
+        if self.conn.shape[1] != nv:
+            raise ValueError(f"conn must be [E, {nv}] for {elem_type} elements")
+        if elem_type != "simplex" and d != 2:
+            raise ValueError("Q4 / Q8 elements are 2-D")
+        self.elem_type = elem_type
         self.dim, self.n_nodes, self.n_elems = d, N, E
         self.dtype = dtype
         K = 1
@@ -64,7 +69,7 @@ class Mesh:
         self.grad = torch.empty((d * d, E), dtype=dtype, device=dev)
         self.vol = torch.empty(E, dtype=dtype, device=dev)
         self.csr_ptr = torch.empty(N + 1, dtype=torch.int32, device=dev)
-        self.csr_ent = torch.empty(E * (d + 1), dtype=torch.int32, device=dev)
+        self.csr_ent = torch.empty(E * nv, dtype=torch.int32, device=dev)
         self.colour = torch.empty(E, dtype=torch.int32, device=dev)
         self.colour_elems = torch.empty(E, dtype=torch.int32, device=dev)
         self.colour_ptr = torch.empty(max_colours + 1, dtype=torch.int32, device=dev)
@@ -74,6 +79,7 @@ class Mesh:
         m.block_elems = block_elems
         m.elem_order = {"input": 0, "locality": 1, "auto": 2}[elem_order]
         m.geometry = GEOMETRY[geometry]
+        m.elem_type = ELEM_TYPES[elem_type]
         m.coords, m.conn = self.coords.data_ptr(), self.conn.data_ptr()
         m.part_elem = self.part_elem.data_ptr() if self.part_elem is not None else None
         m.part_node = self.part_node.data_ptr() if self.part_node is not None else None

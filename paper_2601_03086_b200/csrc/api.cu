@@ -90,6 +90,10 @@ static pfem_status common_checks(const pfem_mesh* m, const pfem_material* mat, i
         return PFEM_ERR_ARG;
     }
     if (mode != PFEM_ASSEMBLE_CSR && mode != PFEM_ASSEMBLE_COLOUR) { set_error("bad assembly mode"); return PFEM_ERR_ARG; }
+    if (m->elem_type != PFEM_ELEM_SIMPLEX && mode != PFEM_ASSEMBLE_CSR) {
+        set_error("quadrilateral meshes assemble in CSR mode only");
+        return PFEM_ERR_ARG;
+    }
     if (m->geometry != PFEM_GEOMETRY_STORED && m->geometry != PFEM_GEOMETRY_ON_THE_FLY) {
         set_error("bad geometry option");
         return PFEM_ERR_ARG;
@@ -140,6 +144,8 @@ pfem_status pfem_mesh_prepare(pfem_mesh* m, void* stream) {
     if (m->block_elems < 0) { set_error("block_elems must be >= 0"); return PFEM_ERR_ARG; }
     if (m->elem_order < 0 || m->elem_order > 2) { set_error("elem_order must be 0, 1 or 2"); return PFEM_ERR_ARG; }
     if (m->geometry < 0 || m->geometry > 1) { set_error("geometry must be 0 or 1"); return PFEM_ERR_ARG; }
+    if (m->elem_type < PFEM_ELEM_SIMPLEX || m->elem_type > PFEM_ELEM_Q8) { set_error("bad elem_type"); return PFEM_ERR_ARG; }
+    if (m->elem_type != PFEM_ELEM_SIMPLEX && m->dim != 2) { set_error("Q4 / Q8 elements need dim 2"); return PFEM_ERR_ARG; }
     if (m->dim == 3 && ((uintptr_t)m->conn & 15)) { set_error("conn must be 16-byte aligned for dim 3"); return PFEM_ERR_ARG; }
     if (m->plan) release_impl(m);
     return prepare_impl(m, (cudaStream_t)stream);
@@ -152,6 +158,7 @@ pfem_status pfem_plan_export(const pfem_mesh* m, int32_t* blk_elem, int32_t* blk
     pfem_status st = check_mesh(m, true);
     if (st) return st;
     const Plan* P = reinterpret_cast<const Plan*>(m->plan);
+    if (P->elem_type != PFEM_ELEM_SIMPLEX) { set_error("quadrilateral meshes have no block plan"); return PFEM_ERR_ARG; }
     cudaError_t e = cudaSuccess;
     if (blk_elem && e == cudaSuccess) e = cudaMemcpy(blk_elem, P->blk_elem, sizeof(int32_t) * (P->n_blocks + 1), cudaMemcpyDeviceToHost);
     if (blk_occ && e == cudaSuccess) e = cudaMemcpy(blk_occ, P->blk_occ, sizeof(int32_t) * (P->n_blocks + 1), cudaMemcpyDeviceToHost);
@@ -222,6 +229,7 @@ pfem_status pfem_pretrain_loss(const pfem_mesh* m, const pfem_material* mat, int
                                int64_t sample_stride, const void* phi, const void* f_ext, void* u, void* totals,
                                void* grad, double* loss, int32_t mode, pfem_flags* flags, void* ws, size_t ws_bytes,
                                void* stream) {
+    if (m && m->elem_type != PFEM_ELEM_SIMPLEX) { set_error("pfem_pretrain_loss: simplex meshes only"); return PFEM_ERR_ARG; }
     pfem_status st = common_checks(m, mat, n_samples, sample_stride, mode, ws, ws_bytes);
     if (st) return st;
     if (!H || !totals || !grad || !loss) { set_error("pfem_pretrain_loss: H, totals, grad and loss are required"); return PFEM_ERR_ARG; }
@@ -270,6 +278,7 @@ pfem_status pfem_heat(const pfem_mesh* m, const void* k, int64_t k_stride, int32
                       int64_t sample_stride, const void* f_nodal, void* elem_energy, void* totals, void* flux,
                       int32_t options, void* ws, size_t ws_bytes, void* stream) {
     pfem_status st = check_mesh(m, true);   // runs on the prepared mesh (the flux path reads the plan)
+    if (!st && m->elem_type != PFEM_ELEM_SIMPLEX) { set_error("pfem_heat: simplex meshes only"); return PFEM_ERR_ARG; }
     if (st) return st;
     if (!k || !T) { set_error("pfem_heat: k and T are required"); return PFEM_ERR_ARG; }
     if (k_stride < 0) { set_error("pfem_heat: negative k_stride"); return PFEM_ERR_ARG; }
@@ -347,6 +356,7 @@ pfem_status pfem_tangent_diag(const pfem_mesh* m, const pfem_material* mat, cons
                               const uint8_t* mask, void* stream) {
     pfem_status st = check_mesh(m, true);
     if (st) return st;
+    if (m->elem_type != PFEM_ELEM_SIMPLEX) { set_error("pfem_tangent_diag: simplex meshes only"); return PFEM_ERR_ARG; }
     if ((st = check_mat(mat))) return st;
     if (!diag) { set_error("pfem_tangent_diag: diag is required"); return PFEM_ERR_ARG; }
     if (mat->model == PFEM_NEOHOOKEAN && !u_state) { set_error("pfem_tangent_diag: Neo-Hookean needs u_state"); return PFEM_ERR_ARG; }
@@ -359,6 +369,10 @@ pfem_status pfem_pcg(const pfem_mesh* m, const pfem_material* mat, const void* u
                      const uint8_t* mask, int32_t precond, void* x, double tol, int32_t max_iter, int32_t mode,
                      double* history, pfem_cg_report* report, void* ws, size_t ws_bytes, void* stream) {
     if (precond != PFEM_PRECOND_NONE && precond != PFEM_PRECOND_JACOBI) { set_error("pfem_pcg: bad precond"); return PFEM_ERR_ARG; }
+    if (precond == PFEM_PRECOND_JACOBI && m && m->elem_type != PFEM_ELEM_SIMPLEX) {
+        set_error("pfem_pcg: Jacobi preconditioning on simplex meshes only");
+        return PFEM_ERR_ARG;
+    }
     pfem_status st = check_mesh(m, true);
     if (st) return st;
     if ((st = check_mat(mat))) return st;

@@ -490,7 +490,8 @@ pfem_status cg_impl(const pfem_mesh* m, const pfem_material* mat, const void* u_
         pfem_status ce = PFEM_OK;
         cudaError_t cerr = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
         if (cerr != cudaSuccess) { cudaStreamDestroy(cs); return cuda_status(cerr, "cudaStreamBeginCapture"); }
-        const bool fuse = mode == PFEM_ASSEMBLE_CSR;   // pipelined iteration (§8(f) row f3)
+        // pipelined iteration (§8(f) row f3): the simplex CSR element kernel
+        const bool fuse = mode == PFEM_ASSEMBLE_CSR && P->elem_type == PFEM_ELEM_SIMPLEX;
         for (int it = 0; it < B && ce == PFEM_OK; ++it) {
             if (fuse) {
                 // K.v stages p_new = z + beta p_old from r and the other p buffer (its owners
@@ -506,7 +507,7 @@ pfem_status cg_impl(const pfem_mesh* m, const pfem_material* mat, const void* u_
             }
             ce = tangent<D, T>(m, P, mat, u_state, p, q, mask, mode, asmws, st, cs);
             if (ce != PFEM_OK) break;
-            if (mode != PFEM_ASSEMBLE_CSR) {
+            if (!fuse) {   // (the simplex CSR kernel forms p.q and alpha itself)
                 k_cg_pq<T><<<G, VEC_NT, 0, cs>>>(n, p, q, st, vr);
                 count_launch();
             }

@@ -84,6 +84,11 @@ inline RecLayout rec_layout(int D, size_t tsize, int eb, int ocap, bool with_eid
 struct Plan {
     uint64_t serial = 0;              // unique per prepared plan in this process (workspace caches key on it)
     int32_t dim = 0, n_nodes = 0, n_elems = 0, n_parts = 0;
+    int32_t elem_type = 0;            // pfem_elem_type; quadrilaterals have no block plan (quad.cu)
+    int32_t nv = 0;                   // nodes per element
+    void* quad_geo = nullptr;         // [E][nq][2 nv + 1] dN/dX and w det J per Gauss point (dtype)
+    int32_t* quad_pos = nullptr;      // [E * nv] CSR entry of every (element, node)
+    void* pool_quad = nullptr;
     int32_t n_blocks = 0, n_occ = 0, eb_max = 0;
     int32_t* blk_elem = nullptr;      // [n_blocks+1] in plan positions (see elem_perm)
     int32_t elem_order = 0;           // 0 input order, 1 locality (Morton) order of the positions
@@ -154,7 +159,10 @@ inline WsLayout ws_layout(const Plan& p, int S, size_t tsize) {
     L.part_cnt = o; o += align_up(sizeof(int32_t) * (size_t)(p.n_parts + 1), 256);   // reduced chunks per part
     L.blk_sum = o;  o += align_up(sizeof(double) * (2 * (size_t)S + 2) * (p.n_blocks + 1), 256);
     L.chunk_sum = o;  o += align_up(sizeof(double) * (2 * (size_t)S + 1) * (p.n_chunks + 1), 256);
-    L.partial = o;  o += align_up(tsize * (size_t)S * std::max(p.n_seg, 1) * p.dim, 256);
+    // segments of multi-block nodes (simplices) / nodal forces at their CSR entries (quadrilaterals)
+    const size_t seg = tsize * (size_t)S * std::max(p.n_seg, 1) * p.dim;
+    const size_t qeb = p.elem_type ? tsize * (size_t)S * p.n_elems * p.nv * 2 : 0;
+    L.partial = o;  o += align_up(std::max(seg, qeb), 256);
     L.wtmp = o;     o += align_up(tsize * (size_t)S * p.n_elems, 256);
     L.total = o;
     return L;

@@ -326,8 +326,12 @@ pfem_status run_model(const Call& c) {
     return PFEM_ERR_ARG;
 }
 
+template <class T>
+pfem_status run_quad(const Call& c);   // quad.cu: Q4 / Q8 elements (§8(f) row f4)
+
 template <int D, class T>
 pfem_status run_assemble(const Call& c) {
+    if (c.P->elem_type != PFEM_ELEM_SIMPLEX) return run_quad<T>(c);
     return c.model == MODEL_NH ? run_model<D, MODEL_NH, T>(c) : run_model<D, MODEL_LINEAR, T>(c);
 }
 

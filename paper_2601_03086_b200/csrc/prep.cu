@@ -533,8 +533,13 @@ inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
 
+pfem_status quad_prepare_geometry(const pfem_mesh* m, Plan* P, cudaStream_t s);   // quad.cu
+void release_impl(pfem_mesh* m);
+
 pfem_status prepare_impl(pfem_mesh* m, cudaStream_t s) {
-    const int D = m->dim, nv = D + 1, N = m->n_nodes, E = m->n_elems;
+    const bool quad = m->elem_type != PFEM_ELEM_SIMPLEX;
+    const int D = m->dim, N = m->n_nodes, E = m->n_elems;
+    const int nv = quad ? (m->elem_type == PFEM_ELEM_Q4 ? 4 : 8) : D + 1;
     const int K = m->n_parts;
     // ---------------- validation of connectivity
     DevBuf scratch;
@@ -547,8 +552,9 @@ pfem_status prepare_impl(pfem_mesh* m, cudaStream_t s) {
     PFEM_CUDA_TRY(cudaMemcpyAsync(sc, init, sizeof(init), cudaMemcpyHostToDevice, s));
     k_check_conn<<<nblk((int64_t)E * nv, 256), 256, 0, s>>>(nv, E, N, m->conn, sc + 0);
     PFEM_LAUNCH_CHECK("k_check_conn");
-    // ---------------- K1 geometry
-    if (D == 2) {
+    // ---------------- K1 geometry (quadrilaterals: per Gauss point, after the CSR)
+    if (quad) {
+    } else if (D == 2) {
         if (m->dtype == PFEM_F32)
             k_geometry<2, float><<<nblk(E, 256), 256, 0, s>>>(E, m->coords, m->conn, (float*)m->grad,
                                                                 (float*)m->vol, sc + 1, sc + 2);
@@ -633,6 +639,41 @@ pfem_status prepare_impl(pfem_mesh* m, cudaStream_t s) {
         PFEM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(t2, tb, m->colour, keys_out, vals_in,
                                                       m->colour_elems, E, 0, end_bit, s));
         count_launch();
+    }
+    // ---------------- quadrilaterals: Gauss-point geometry and CSR entry positions, no block plan
+    if (quad) {
+        Plan* P = new Plan();
+        static std::atomic<uint64_t> quad_serial{1ull << 40};
+        P->serial = ++quad_serial;
+        P->dim = D; P->n_nodes = N; P->n_elems = E; P->n_parts = K;
+        P->elem_type = m->elem_type;
+        P->nv = nv;
+        std::vector<int32_t> qpe{0, E}, qpn{0, N};
+        if (K > 1) {
+            qpe.resize(K + 1);
+            qpn.resize(K + 1);
+            PFEM_CUDA_TRY(cudaMemcpyAsync(qpe.data(), m->part_elem, sizeof(int32_t) * (K + 1), cudaMemcpyDeviceToHost, s));
+            PFEM_CUDA_TRY(cudaMemcpyAsync(qpn.data(), m->part_node, sizeof(int32_t) * (K + 1), cudaMemcpyDeviceToHost, s));
+        }
+        cudaError_t ce = cudaMallocAsync(&P->pool, 2 * align_up(sizeof(int32_t) * (K + 1), 256), s);
+        if (ce != cudaSuccess) { delete P; return cuda_status(ce, "plan alloc"); }
+        P->part_elem = (int32_t*)P->pool;
+        P->part_node = (int32_t*)((char*)P->pool + align_up(sizeof(int32_t) * (K + 1), 256));
+        PFEM_CUDA_TRY(cudaMemcpyAsync(P->part_elem, qpe.data(), sizeof(int32_t) * (K + 1), cudaMemcpyHostToDevice, s));
+        PFEM_CUDA_TRY(cudaMemcpyAsync(P->part_node, qpn.data(), sizeof(int32_t) * (K + 1), cudaMemcpyHostToDevice, s));
+        P->colour_ptr_host.resize(m->n_colours + 1);
+        PFEM_CUDA_TRY(cudaMemcpyAsync(P->colour_ptr_host.data(), m->colour_ptr, sizeof(int32_t) * (m->n_colours + 1),
+                                      cudaMemcpyDeviceToHost, s));
+        m->plan = reinterpret_cast<pfem_plan*>(P);   // released by release_impl on failure below
+        const pfem_status st = quad_prepare_geometry(m, P, s);
+        if (st != PFEM_OK) {
+            release_impl(m);
+            return st;
+        }
+        m->n_negative = 0;
+        m->n_blocks = 0;
+        m->n_occ = 0;
+        return PFEM_OK;
     }
     // ---------------- plan: element blocks (host bookkeeping on the part offsets)
     std::vector<int32_t> pe(K + 1), pn(K + 1);
@@ -971,6 +1012,7 @@ void release_impl(pfem_mesh* m) {
     if (P->pool_src) cudaFree(P->pool_src);
     if (P->pool_rec) cudaFree(P->pool_rec);
     if (P->pool_perm) cudaFree(P->pool_perm);
+    if (P->pool_quad) cudaFree(P->pool_quad);
     delete P;
     m->plan = nullptr;
 }

@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
 def test_binding_loads_and_reports_abi_version():
     import paper_2601_03086_b200 as pf
     lib = pf.load()
-    assert lib.pfem_abi_version() == 5
+    assert lib.pfem_abi_version() == 6
     assert lib.pfem_last_error() is not None
 
 

@@ -752,3 +752,94 @@ def test_inversion_flags_staged_items():
     bad = ~np.isfinite(Wn)
     assert f[0] == int(bad.sum()) and f[0] >= 2 and f[1] == 0
     assert np.all(np.isfinite(Wn[[0, 1, 3, 4, 6]]))
+
+
+# ------------------------------------------------------------------ Q4 / Q8 elements (§8(f) row f4)
+def quad_problem(kind, dtype, model="neohookean", S=3, seed=61, n_cells=None):
+    from pfem_gen import beam_q4, cook_q8
+    p = (beam_q4 if kind == "q4" else cook_q8)(**({"n_cells": n_cells} if n_cells else {}), dtype=dtype)
+    rng = np.random.default_rng(seed)
+    L = np.ptp(p.coords, axis=0).max()
+    p.u = np.stack([0.02 * L * fourier_field(p.coords / L, rng) for _ in range(S)])
+    p.model = model
+    return p
+
+
+def quad_gpu(p, dtype=None):
+    import paper_2601_03086_b200 as pf
+    dt = {"f32": torch.float32, "f64": torch.float64}[dtype or p.dtype]
+    mesh = pf.Mesh(torch.as_tensor(p.coords, device="cuda"), torch.as_tensor(p.conn, device="cuda"), dtype=dt,
+                   elem_type=p.elem)
+    mat = pf.Material(p.model, p.param_kind, torch.as_tensor(np.asarray(p.p0), dtype=dt, device="cuda"),
+                      torch.as_tensor(np.asarray(p.p1), dtype=dt, device="cuda"))
+    return mesh, mat, torch.as_tensor(p.u, dtype=dt, device="cuda")
+
+
+def quad_oracle(orc, p):
+    return orc.prepare_quad(p.elem, p.coords, p.conn, p.model, p.param_kind, rounded(p.p0, p.dtype),
+                            rounded(p.p1, p.dtype))
+
+
+@pytest.mark.parametrize("kind", ["q4", "q8"])
+def test_quad_prepare_bitexact(orc, kind):
+    """Q4 / Q8 meshes: the CSR and the greedy colouring are bit-exact with the oracle's
+    definitions (reading R12 with d+1 replaced by the element's node count)."""
+    p = quad_problem(kind, "f64")
+    mesh, _, _ = quad_gpu(p)
+    ptr, ent = orc.csr(p.conn, p.n_nodes)
+    assert np.array_equal(mesh.csr_ptr.cpu().numpy(), ptr) and np.array_equal(mesh.csr_ent.cpu().numpy(), ent)
+    col, nc = orc.colour(p.conn, p.n_nodes, ptr, ent)
+    assert mesh.n_colours == nc and np.array_equal(mesh.colour.cpu().numpy(), col)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("model", ["linear", "neohookean"])
+@pytest.mark.parametrize("kind", ["q4", "q8"])
+def test_quad_energy_residual_tangent(orc, kind, model, dtype):
+    """Beam (50 x 50 Q4) and Cook (30 x 30 Q8) meshes, three displacement fields,
+    element-wise (E, nu): W_e, totals with nodal loads, the residual and the masked K.v against the
+    Gauss-quadrature oracle within the north-star bars."""
+    import paper_2601_03086_b200 as pf
+    p = quad_problem(kind, dtype, model)
+    mesh, mat, u = quad_gpu(p)
+    om = quad_oracle(orc, p)
+    ur = rounded(p.u, dtype)
+    fe = rounded(p.f_ext, dtype)
+    W_ref, tot_ref = om.energy(ur, f_ext=fe)
+    _, w_ref = om.energy(ur, want_elem=False)
+    tot, W, r = pf.energy(mesh, mat, u, f_ext=torch.as_tensor(fe, dtype=u.dtype, device="cuda"), elem_energy=True,
+                          residual=True)
+    v = rounded(np.random.default_rng(5).standard_normal(p.u.shape), dtype)
+    Kv = pf.tangent_apply(mesh, mat, torch.as_tensor(v, dtype=u.dtype, device="cuda"),
+                          u=u if model == "neohookean" else None, mask=torch.as_tensor(p.mask, device="cuda"))
+    torch.cuda.synchronize()
+    assert_field(W.cpu().numpy(), W_ref, dtype, "W_e")
+    assert_totals(tot.cpu().numpy(), tot_ref, np.abs(w_ref) + np.abs(w_ref - tot_ref), dtype)
+    assert_field(r.cpu().numpy(), om.residual(ur), dtype, "residual")
+    ref = om.tangent(v, u=ur if model == "neohookean" else None, mask=p.mask)
+    assert_field(Kv.cpu().numpy(), ref, dtype, "Kv")
+
+
+@pytest.mark.parametrize("kind", ["q4", "q8"])
+def test_quad_newton_matches_oracle(orc, kind):
+    """Newton warm start on the hyperelastic beam (Q4) and Cook's membrane (Q8) at reduced size
+    (App. B): the same number of Newton steps as the oracle, residual
+    histories within 1e-9 above the rounding floor, U within 1e-9; a converged start takes 0 steps."""
+    import paper_2601_03086_b200 as pf
+    from pfem_gen import beam_q4, cook_q8
+    p = (beam_q4 if kind == "q4" else cook_q8)(n_cells=12)
+    mesh, mat, u = quad_gpu(p)
+    om = quad_oracle(orc, p)
+    f = torch.as_tensor(p.f_ext, device="cuda")
+    mask = torch.as_tensor(p.mask, device="cuda")
+    tol = 1e-10 * float(np.linalg.norm(p.f_ext))
+    ug, rg = pf.newton(mesh, mat, u[0], f_ext=f, mask=mask, tol=tol, cg_tol=1e-12)
+    uo, ro = om.newton(p.u[0], p.f_ext, p.mask, tol=tol, cg_tol=1e-12)
+    assert rg["converged"] and ro["converged"] and rg["iterations"] == ro["iterations"] >= 2
+    ho, hg = ro["history"], rg["history"]
+    # relative 1e-9, plus the rounding floor of r = f_int - f_ext (1e-11 of the initial residual:
+    # the converged entries are rounding noise of a cancellation, ~1e-12 of ||r_0|| on both sides)
+    assert np.all(np.abs(hg - ho) <= 1e-9 * ho + 1e-11 * ho[0]), (hg, ho)
+    assert rel_l2(ug.cpu().numpy(), uo) < 1e-9
+    _, r1 = pf.newton(mesh, mat, ug, f_ext=f, mask=mask, tol=10 * tol, cg_tol=1e-12)
+    assert r1["iterations"] == 0
