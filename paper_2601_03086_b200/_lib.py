@@ -108,12 +108,9 @@ SIGNATURES = {
 
 
 def load(path: str = LIB_PATH):
-    """Load libpfem.so (raises if it was not built: there is no fallback).  PFEM_LIB names an
-    alternative in-tree build (development A/B measurements, ``build(tag=...)``)."""
+    """Load libpfem.so (raises if it was not built: there is no fallback)."""
     global _lib
     if _lib is None:
-        if os.environ.get("PFEM_LIB") and path == LIB_PATH:
-            path = os.path.join(HERE, os.path.basename(os.environ["PFEM_LIB"]))
         if not os.path.exists(path):
             raise ImportError(f"libpfem.so not found at {path}; run `python -m paper_2601_03086_b200.build` "
                               "(there is no CPU fallback)")

@@ -44,8 +44,8 @@ def needs_build() -> bool:
 
 def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False, tag: str = "",
           defines: tuple = ()) -> str:
-    """Build libpfem.so.  Development A/B builds: ``tag`` + ``defines`` (-D...) produce
-    libpfem_<tag>.so, selected at load time by PFEM_LIB=libpfem_<tag>.so."""
+    """Build libpfem.so.  Development builds: ``tag`` + ``defines`` (-D...) produce
+    libpfem_<tag>.so beside it (loaded explicitly with ``_lib.load(path)``)."""
     lib = LIB if not tag else os.path.join(HERE, f"libpfem_{tag}.so")
     bdir = BUILD if not tag else BUILD + "_" + tag
     if not tag and not force and not needs_build():

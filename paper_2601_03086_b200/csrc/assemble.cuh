@@ -30,49 +30,14 @@
 #include "common.cuh"
 #include "element.cuh"
 
-#ifndef PFEM_STAGED_MINB
-#define PFEM_STAGED_MINB 2
-#endif
-#ifndef PFEM_EB3
-#define PFEM_EB3 256          // staged-kernel block capacity for T4 (measurement switch)
-#endif
-#ifndef PFEM_STAGED_NT
-#define PFEM_STAGED_NT 256    // staged-kernel threads per CTA (measurement switch)
-#endif
-#ifndef PFEM_MAT_HOIST
-#define PFEM_MAT_HOIST 1      // uniform material: Lame constants hoisted out of the element loop
-#endif
-#ifndef PFEM_P2_UNROLL4
-#define PFEM_P2_UNROLL4 0     // phase-2 gathers four entries at a time (measured slower: off)
-#endif
-#ifndef PFEM_STAGED_OPERM
-#define PFEM_STAGED_OPERM 1   // phase-2 threads take occurrences in descending entry count
-#endif
-#ifndef PFEM_STAGED_EPOS
-#define PFEM_STAGED_EPOS 0
-#endif
-#ifndef PFEM_F0_DERIVED
-#define PFEM_F0_DERIVED 0     // vertex-0 forces formed in phase 2 (a quarter less force buffer)
-#endif
-#ifndef PFEM_DBG
-#define PFEM_DBG 0            // compile the PFEM_DEBUG ablation switches into the staged kernel (tools)
-#endif
-#ifndef PFEM_HP2_2D
-#define PFEM_HP2_2D 1         // two phase-2 threads per occurrence for T3 as well
-#endif
-#ifndef PFEM_STAGED_HP2
-#define PFEM_STAGED_HP2 1
-#endif
-#ifndef PFEM_STAGED_L2PF
-#define PFEM_STAGED_L2PF 1
-#endif
-#ifndef PFEM_STAGED_SCALAR
-#define PFEM_STAGED_SCALAR 0
-#endif
-
 namespace pfem {
 
 enum { OP_ENERGY = 0, OP_ENERGY_RESIDUAL = 1, OP_RESIDUAL = 2, OP_TANGENT = 3 };
+// staged kernel shape (measured): 256 threads, 2 resident CTAs per SM, T4 blocks of
+// at most 256 elements (T3: 512)
+constexpr int STAGED_MINB = 2;
+constexpr int STAGED_NT = 256;
+constexpr int EB3 = 256;
 constexpr int ASM_NT = 256;   // main (element / occurrence) threads per CTA
 constexpr int FIX_WARPS = 1;  // fix-up warps per CTA (+1 publisher warp)
 constexpr int FIX_UNROLL = 4; // segments loaded together by one fix-up lane
@@ -80,7 +45,7 @@ constexpr int CHUNK = 32;     // blocks per reduction chunk (== CHUNK_BLOCKS of 
 
 template <int D>
 struct EbOf {
-    static constexpr int value = D == 3 ? PFEM_EB3 : 512;   // compile-time block capacity
+    static constexpr int value = D == 3 ? EB3 : 512;   // compile-time block capacity
 };
 
 struct CgState {
@@ -109,7 +74,6 @@ struct AsmParams {
     pfem_flags* uflags;    // nullable
     // plan
     int n_blocks, n_occ, eb_max, n_chunks, lag;
-    int dbg;               // experiment switches (PFEM_DEBUG env): 1 no phase-1 math, 2 no phase 2, 4 no fix-up, 8 no sums, 16 no staging
     const int32_t* blk_elem;
     const int32_t* blk_chunk;
     const int32_t* chunk_blk;
@@ -465,31 +429,6 @@ __device__ __forceinline__ void sacc_reg(const T (&b)[SD], T (&acc)[SD]) {
     }
 }
 
-// one entry's two-sample force vector from a force buffer without vertex-0 rows (F0D): slot
-// j = a * EB + el; vertex 0 is ((-f1) - f2) - f3 (the order forces() forms it in)
-template <int D, class T, int ST>
-__device__ __forceinline__ void entry_f0d(const T* fbuf, int j, int EB, int SD, int qs, float2 (&x)[D]) {
-    if (j >= EB) {
-        const T* b = fbuf + (size_t)(j - EB) * SD + qs;
-#pragma unroll
-        for (int i = 0; i < D; ++i) x[i] = *reinterpret_cast<const float2*>(b + i * ST);
-    } else {
-        const T* b1 = fbuf + (size_t)j * SD + qs;
-        const size_t step = (size_t)EB * SD;
-#pragma unroll
-        for (int i = 0; i < D; ++i) {
-            const float2 q1 = *reinterpret_cast<const float2*>(b1 + i * ST);
-            F2 s = -F2(q1.x, q1.y);
-#pragma unroll
-            for (int a = 1; a < D; ++a) {
-                const float2 q = *reinterpret_cast<const float2*>(b1 + a * step + i * ST);
-                s = s - F2(q.x, q.y);
-            }
-            x[i] = s.v;
-        }
-    }
-}
-
 template <int D, class T, int NT, int ST, bool MASKED>
 __device__ __forceinline__ void stage_fields(T* ust, const unsigned char* rec, uint32_t base, const T* src,
                                              const AsmParams<T>& p, int s0, int nq, int no) {
@@ -520,7 +459,7 @@ __device__ __forceinline__ void stage_fields(T* ust, const unsigned char* rec, u
 // FEXT: the call passes f_ext (Pi = W - f.u; the pretraining epilogue); without it the f.u
 // code is compiled out
 template <int D, int MODEL, class T, int OP, int ST, bool MASKED, int EB, int NT, bool FEXT>
-__global__ void __launch_bounds__(NT, PFEM_STAGED_MINB)
+__global__ void __launch_bounds__(NT, STAGED_MINB)
 k_assemble(const AsmParams<T> p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr bool HAS_FORCE = OP != OP_ENERGY;
@@ -530,17 +469,11 @@ k_assemble(const AsmParams<T> p) {
     // staged fields (one buffer, refilled for the next block after phase 1): u (energy /
     // residual), v (linear tangent), v then u (NH tangent: the linearisation state)
     constexpr int NF = (OP == OP_TANGENT && MODEL == MODEL_NH) ? 2 : 1;
-    using V = std::conditional_t<(sizeof(T) == 4 && ST % 2 == 0 && !PFEM_STAGED_SCALAR), F2, T>;
+    using V = std::conditional_t<(sizeof(T) == 4 && ST % 2 == 0), F2, T>;
     constexpr int L = VTraits<V>::L;
-    // EPOS (fp32): fbuf[(d+1) EB entries][D][ST], each element vertex's forces stored at its
-    // block-CSR entry (ent_pos), so an occurrence's entries are contiguous in phase 2.
-    // !EPOS (fp64): fbuf[NV][EB][D][ST] in element order, gathered through loc_ent.
-    constexpr bool EPOS = sizeof(T) == 4 && PFEM_STAGED_EPOS;
-    constexpr int HP = (sizeof(T) == 4 && ST == 4 && (D == 3 || PFEM_HP2_2D) && !EPOS && PFEM_STAGED_HP2) ? 2 : 1;   // phase-2 threads per occurrence
+    // fbuf[NV][EB][D][ST] in element order, gathered through loc_ent in phase 2
+    constexpr int HP = (sizeof(T) == 4 && ST == 4) ? 2 : 1;   // phase-2 threads per occurrence
     constexpr int STH = ST / HP;
-    // F0D: vertex 0's forces are not stored; phase 2 forms them as ((-f1) - f2) - f3, the same
-    // operations phase 1 used (a quarter less force buffer)
-    constexpr bool F0D = PFEM_F0_DERIVED && HP == 2;
     constexpr int SDH = D * STH;
     const T* staged_src = (OP == OP_TANGENT) ? p.v : p.u;
     // shared layout: rec[2] | mat[2][2][EB] | ust[2][OCAP][D][ST] | fbuf[NV][EB][D][ST]
@@ -574,7 +507,7 @@ k_assemble(const AsmParams<T> p) {
     int n_inv = 0, first_inv = INT32_MAX, n_nonfin = 0;
     const LameScale<T> lsc = lame_scale<T>(p.mat);
     // uniform material: the Lame constants once per thread (the same arithmetic per element)
-    const bool mat_uniform = PFEM_MAT_HOIST && p.mat.s0 == 0 && p.mat.s1 == 0;
+    const bool mat_uniform = p.mat.s0 == 0 && p.mat.s1 == 0;
     T mu_u = T(0), lam_u = T(0);
     if (mat_uniform) lame_elem<T>(p.mat, lsc, __ldg(p.mat.p0), __ldg(p.mat.p1), mu_u, lam_u);
     const int G = gridDim.x;
@@ -603,7 +536,7 @@ k_assemble(const AsmParams<T> p) {
         unsigned char* const sg_nxt = cur ? stage0 : stage1;
         if (tn < NI) stage_block<D, T, NT>(sg_nxt, mstage + 2 * EB * (cur ^ 1), &s_bar[cur ^ 1], p, bn);
         else cp_commit();
-        if (PFEM_STAGED_L2PF && tid == 32 && tn + G < NI) {
+        if (tid == 32 && tn + G < NI) {
             // the record after next into L2, so next iteration's bulk copy is an L2 hit
             const size_t rb = p.rec.bytes, off = (size_t)((tn + G) % nb) * rb + p.rec_base;
             const uintptr_t a0 = (uintptr_t)(p.recs + off), a1 = (uintptr_t)(p.recs + off + (p.rec_end - p.rec_base));
@@ -619,7 +552,6 @@ k_assemble(const AsmParams<T> p) {
         const uint16_t* soe = reinterpret_cast<const uint16_t*>(sg + p.rec.occ_ent);
         const uint16_t* sle = reinterpret_cast<const uint16_t*>(sg + p.rec.loc_ent);
         const uint16_t* slc = reinterpret_cast<const uint16_t*>(sg + p.rec.lconn);
-        const uint16_t* sep = reinterpret_cast<const uint16_t*>(sg + p.rec.ent_pos);   // valid iff EPOS
         const int32_t* sseg = reinterpret_cast<const int32_t*>(sg + p.rec.occ_seg);
         const int32_t* seid = reinterpret_cast<const int32_t*>(sg + p.rec.eid);
         const T* smat = mstage + 2 * EB * cur;
@@ -668,24 +600,17 @@ k_assemble(const AsmParams<T> p) {
                     G_.mu *= G_.V;
                     G_.lam *= G_.V;
                 }
-                int lv[NV], ep[NV];   // vertex -> staged occurrence, vertex -> block-CSR entry
+                int lv[NV];   // vertex -> staged occurrence
                 if constexpr (D == 3) {
                     const uint2 c = *reinterpret_cast<const uint2*>(slc + el * NV);
                     lv[0] = c.x & 0xffff; lv[1] = c.x >> 16; lv[2] = c.y & 0xffff; lv[3] = c.y >> 16;
-                    if (EPOS) {
-                        const uint2 q = *reinterpret_cast<const uint2*>(sep + el * NV);
-                        ep[0] = q.x & 0xffff; ep[1] = q.x >> 16; ep[2] = q.y & 0xffff; ep[3] = q.y >> 16;
-                    }
                 } else {
 #pragma unroll
-                    for (int a = 0; a < NV; ++a) {
-                        lv[a] = slc[el * NV + a];
-                        if (EPOS) ep[a] = sep[el * NV + a];
-                    }
+                    for (int a = 0; a < NV; ++a) lv[a] = slc[el * NV + a];
                 }
 #pragma unroll
                 for (int qq = 0; qq < ST; qq += L) {
-                    if (qq >= nq || (PFEM_DBG && (p.dbg & 1))) break;
+                    if (qq >= nq) break;
                     const int s = s0 + qq;
                     const int64_t lstride = (L > 1 && qq + 1 >= nq) ? 0 : p.sstride;
                     V x[NV][D], H[D][D], P[D][D], psi = V(T(0));
@@ -736,13 +661,12 @@ k_assemble(const AsmParams<T> p) {
                         for (int a = 0; a < NV; ++a)
 #pragma unroll
                             for (int i = 0; i < D; ++i)
-                                if (!F0D || a > 0)
-                                    *reinterpret_cast<V*>(fbuf + ((size_t)(EPOS ? ep[a] : (a - (F0D ? 1 : 0)) * EB + el) * D + i) * ST + qq) = f[a][i];
+                                *reinterpret_cast<V*>(fbuf + ((size_t)(a * EB + el) * D + i) * ST + qq) = f[a][i];
                         if (!HAS_PSI && !isfinite(pfem::lane(f[0][0], 0))) ++n_nonfin;
                     }
                 }
             }
-            if (HAS_PSI && !(PFEM_DBG && (p.dbg & 8))) {
+            if (HAS_PSI) {
                 // per-warp energy sums now, while other warps finish phase 1 (s_red is free:
                 // the previous item's warp 0 read it before this item's first barrier)
                 T wv[ST];
@@ -754,7 +678,7 @@ k_assemble(const AsmParams<T> p) {
             // the next block's fields, into the same buffer once every thread's phase-1 reads
             // are done (the barrier before phase 2); its record has had phase 1 to land, and
             // the copies have phase 2 to complete
-            const bool do_p2 = (HAS_FORCE || FEXT) && !(PFEM_DBG && (p.dbg & 2));
+            const bool do_p2 = HAS_FORCE || FEXT;
             bar_main(NT);   // every thread's phase-1 reads of the field buffer are done
             {
                 if (tn < NI) {
@@ -774,7 +698,7 @@ k_assemble(const AsmParams<T> p) {
                 // warps share the gather and each entry chain is half as long)
                 const uint16_t* sop = reinterpret_cast<const uint16_t*>(sg + p.rec.occ_perm);
                 for (int w = tid; w < HP * no; w += NT) {
-                    const int oi = PFEM_STAGED_OPERM ? (int)sop[HP == 1 ? w : w / HP] : (HP == 1 ? w : w / HP);
+                    const int oi = (int)sop[HP == 1 ? w : w / HP];
                     const int qs = HP == 1 ? 0 : (w % HP) * STH;   // first sample of this thread
                     const int word = socc[oi];
                     const int node = word & OCC_NODE_MASK;
@@ -783,52 +707,21 @@ k_assemble(const AsmParams<T> p) {
 #pragma unroll
                         for (int k = 0; k < SDH; ++k) accs[k] = T(0);
                         const int kb = soe[oi], k1 = soe[oi + 1];
-                        if constexpr (EPOS) {
-                            for (int k = kb; k < k1; ++k) sacc<T, SD>(fbuf + (size_t)k * SD, accs);
-                        } else if constexpr (HP == 1) {
+                        if constexpr (HP == 1) {
                             for (int k = kb; k < k1; ++k) sacc<T, SDH>(fbuf + (size_t)sle[k] * SD, accs);
                         } else {
                             // entries in pairs: both gathers in flight before the adds (the
                             // adds stay in ascending entry order)
                             int k = kb;
-#if PFEM_P2_UNROLL4
-                            for (; k + 3 < k1; k += 4) {   // four entries' gathers in flight
-                                const int j0 = sle[k], j1 = sle[k + 1], j2 = sle[k + 2], j3 = sle[k + 3];
-                                const T* b0 = fbuf + (size_t)j0 * SD + qs;
+                            for (; k + 1 < k1; k += 2) {
+                                const int j0 = sle[k], j1 = sle[k + 1];
+                                const T* b0 = fbuf + (size_t)j0 * SD + qs;   // (record loc_ent = slot)
                                 const T* b1 = fbuf + (size_t)j1 * SD + qs;
-                                const T* b2 = fbuf + (size_t)j2 * SD + qs;
-                                const T* b3 = fbuf + (size_t)j3 * SD + qs;
-                                float2 x0[D], x1[D], x2[D], x3[D];
+                                float2 x0[D], x1[D];
 #pragma unroll
                                 for (int i = 0; i < D; ++i) {
                                     x0[i] = *reinterpret_cast<const float2*>(b0 + i * ST);
                                     x1[i] = *reinterpret_cast<const float2*>(b1 + i * ST);
-                                    x2[i] = *reinterpret_cast<const float2*>(b2 + i * ST);
-                                    x3[i] = *reinterpret_cast<const float2*>(b3 + i * ST);
-                                }
-#pragma unroll
-                                for (int i = 0; i < D; ++i) {
-                                    F2 a0(accs[2 * i], accs[2 * i + 1]);
-                                    a0 = (((a0 + F2(x0[i].x, x0[i].y)) + F2(x1[i].x, x1[i].y)) + F2(x2[i].x, x2[i].y)) +
-                                         F2(x3[i].x, x3[i].y);
-                                    accs[2 * i] = a0.v.x; accs[2 * i + 1] = a0.v.y;
-                                }
-                            }
-#endif
-                            for (; k + 1 < k1; k += 2) {
-                                const int j0 = sle[k], j1 = sle[k + 1];
-                                float2 x0[D], x1[D];
-                                if constexpr (F0D) {
-                                    entry_f0d<D, T, ST>(fbuf, j0, EB, SD, qs, x0);
-                                    entry_f0d<D, T, ST>(fbuf, j1, EB, SD, qs, x1);
-                                } else {
-                                    const T* b0 = fbuf + (size_t)j0 * SD + qs;   // (record loc_ent = slot)
-                                    const T* b1 = fbuf + (size_t)j1 * SD + qs;
-#pragma unroll
-                                    for (int i = 0; i < D; ++i) {
-                                        x0[i] = *reinterpret_cast<const float2*>(b0 + i * ST);
-                                        x1[i] = *reinterpret_cast<const float2*>(b1 + i * ST);
-                                    }
                                 }
 #pragma unroll
                                 for (int i = 0; i < D; ++i) {
@@ -838,19 +731,12 @@ k_assemble(const AsmParams<T> p) {
                                 }
                             }
                             if (k < k1) {
-                                const int j0 = sle[k];
-                                float2 x0[D];
-                                if constexpr (F0D) {
-                                    entry_f0d<D, T, ST>(fbuf, j0, EB, SD, qs, x0);
-                                } else {
-                                    const T* b0 = fbuf + (size_t)j0 * SD + qs;
-#pragma unroll
-                                    for (int i = 0; i < D; ++i) x0[i] = *reinterpret_cast<const float2*>(b0 + i * ST);
-                                }
+                                const T* b0 = fbuf + (size_t)sle[k] * SD + qs;
 #pragma unroll
                                 for (int i = 0; i < D; ++i) {
+                                    const float2 x0 = *reinterpret_cast<const float2*>(b0 + i * ST);
                                     F2 a0(accs[2 * i], accs[2 * i + 1]);
-                                    a0 = a0 + F2(x0[i].x, x0[i].y);
+                                    a0 = a0 + F2(x0.x, x0.y);
                                     accs[2 * i] = a0.v.x; accs[2 * i + 1] = a0.v.y;
                                 }
                             }
@@ -901,7 +787,7 @@ k_assemble(const AsmParams<T> p) {
             }
         }
         // ---------------- per-item sums (the item's samples) and CG dot
-        if ((HAS_PSI || cgdot) && !(PFEM_DBG && (p.dbg & 8))) {
+        if (HAS_PSI || cgdot) {
             if (HAS_PSI) {   // (the energy sums went to s_red after phase 1)
 #pragma unroll
                 for (int q = 0; q < ST; ++q) {
@@ -916,7 +802,7 @@ k_assemble(const AsmParams<T> p) {
             }
         }
         bar_main(NT);   // phase 2 done (fbuf free), s_red complete
-        if ((HAS_PSI || cgdot) && !(PFEM_DBG && (p.dbg & 8)) && warp == 0) {
+        if ((HAS_PSI || cgdot) && warp == 0) {
             if (HAS_PSI && lane < 2 * nq) {
                 const int q = lane % nq, kind = lane / nq;
                 double r = 0.0;

@@ -64,36 +64,18 @@ __device__ __forceinline__ void prefetch_record(const AsmParams<T>& p, int b) {
     if (p.mat.s1) l2_prefetch(p.mat.p1, E * sizeof(T), e0 * sizeof(T), ne * sizeof(T));
 }
 
-#ifndef PFEM_DIRECT_MINB64
-#define PFEM_DIRECT_MINB64 4   // fp64 linear single-sample calls: 4 CTAs per SM (64 registers; config 4 134.5 -> 132.4 us)
-#endif
-#ifndef PFEM_DIRECT_SMAT
-#define PFEM_DIRECT_SMAT 0   // element-wise materials copied into shared memory with the fields (measured slower: off)
-#endif
-#ifndef PFEM_DIRECT_TMA
-#define PFEM_DIRECT_TMA 0   // fp32: the block's record copied to shared memory by one bulk copy (measurement switch)
-#endif
-// record read: shared-memory copy (plain load) or global (read-only path)
-template <bool SM, class X>
-__device__ __forceinline__ X rld(const X* q) {
-    if constexpr (SM) return *q;
-    else return __ldg(q);
-}
-
-#ifndef PFEM_DIRECT_SCALAR
-#define PFEM_DIRECT_SCALAR 0
-#endif
-#ifndef PFEM_DIRECT_MINBS
-#define PFEM_DIRECT_MINBS 6
-#endif
+// resident CTAs the register budget aims at (measured): fp64 linear single-sample calls 4 per SM
+// (64 registers; config 4 134.5 -> 132.4 us), several-sample fp32 calls 6
+constexpr int DIRECT_MINB64 = 4;
+constexpr int DIRECT_MINBS = 6;
 // register budget (measured): fp32 single-sample calls 64 registers (8% faster on config 5
 // than the default); several-sample fp32 calls 80; fp64 linear single-sample calls 64 (4 CTAs
 // per SM with the 384-element blocks: config 4 134.5 -> 132.4 us); fp64 Neo-Hookean and fp64
 // several-sample calls the compiler's own allocation (a 40-register cap spilled hundreds of
 // bytes per thread)
 template <int D, int MODEL, class T, int OP, int ST, bool MASKED, int NT, bool PERM, bool OTF>
-__global__ void __launch_bounds__(NT, ST > 1 ? (sizeof(T) == 4 ? PFEM_DIRECT_MINBS : 0)
-                                            : (sizeof(T) == 4 ? 65536 / (NT * 64) : (MODEL == MODEL_LINEAR ? PFEM_DIRECT_MINB64 : 0)))
+__global__ void __launch_bounds__(NT, ST > 1 ? (sizeof(T) == 4 ? DIRECT_MINBS : 0)
+                                            : (sizeof(T) == 4 ? 65536 / (NT * 64) : (MODEL == MODEL_LINEAR ? DIRECT_MINB64 : 0)))
 k_assemble_direct(const AsmParams<T> p) {
     // shared: ust[NF][OCAP][D][ST] (staged nodal fields) | [le[(d+1) EB] u16] | fbuf
     // EPOS (fp32): fbuf[(d+1) EB entries][D][ST], element vertex forces scattered to their
@@ -108,7 +90,7 @@ k_assemble_direct(const AsmParams<T> p) {
     constexpr int NV = D + 1;
     constexpr int SD = ST * D;
     constexpr int NF = (OP == OP_TANGENT && MODEL == MODEL_NH) ? 2 : 1;   // NH tangent stages u and v
-    using V = std::conditional_t<(sizeof(T) == 4 && ST % 2 == 0 && !PFEM_DIRECT_SCALAR), F2, T>;
+    using V = std::conditional_t<(sizeof(T) == 4 && ST % 2 == 0), F2, T>;
     constexpr int L = VTraits<V>::L;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // single-sample instantiations serve S = 1 only (dispatch_st); folding it into the fp64 code
@@ -116,43 +98,22 @@ k_assemble_direct(const AsmParams<T> p) {
     const int S = (ST == 1 && sizeof(T) == 8) ? 1 : p.S;
     const int EB = p.rec.eb;                                    // record / fbuf stride
     const size_t ust_sz = (size_t)p.rec.ocap * D * ST;
-    constexpr bool TMA = PFEM_DIRECT_TMA && sizeof(T) == 4;
-    // TMA: smem_raw = [record bytes ent_pos .. loc_ent) | ust | fbuf
-    const uint32_t rb0 = p.rec.ent_pos, rbn = TMA ? ((p.rec.loc_ent - p.rec.ent_pos + 15u) & ~15u) : 0u;
-    T* ust = reinterpret_cast<T*>(smem_raw + rbn);
+    T* ust = reinterpret_cast<T*>(smem_raw);
     constexpr bool EPOS = sizeof(T) == 4;
     uint16_t* le = reinterpret_cast<uint16_t*>(ust + NF * ust_sz);
-    T* fbuf = reinterpret_cast<T*>(smem_raw + rbn + ((NF * ust_sz * sizeof(T) + (EPOS ? 0 : 2 * (size_t)NV * EB) + 15) &
-                                                     ~size_t(15)));
-    // element-wise materials [2][EB] after the force buffer
-    T* smat = fbuf + (HAS_FORCE ? (size_t)ST * D * NV * EB : 0);
+    T* fbuf = reinterpret_cast<T*>(smem_raw + ((NF * ust_sz * sizeof(T) + (EPOS ? 0 : 2 * (size_t)NV * EB) + 15) &
+                                               ~size_t(15)));
     // on-the-fly geometry: the vertex coordinates of the block's node occurrences [ocap][D]
     double* scoord = reinterpret_cast<double*>(
-        (reinterpret_cast<uintptr_t>(smat + ((PFEM_DIRECT_SMAT && (p.mat.s0 | p.mat.s1)) ? 2 * (size_t)EB : 0)) + 15) &
-        ~uintptr_t(15));
-    const bool has_mat = (p.mat.s0 | p.mat.s1) != 0;
+        (reinterpret_cast<uintptr_t>(fbuf + (HAS_FORCE ? (size_t)ST * D * NV * EB : 0)) + 15) & ~uintptr_t(15));
     const bool cgdot = OP == OP_TANGENT && p.cg != nullptr;
     if (p.cg && ld_relaxed_i(&p.cg->done)) return;
     const int b = blockIdx.x;
     if (p.lag > 0 && tid == 0 && b + p.lag < p.n_blocks) prefetch_record<T, OTF>(p, b + p.lag);
     const unsigned char* rg = p.recs + (size_t)b * p.rec.bytes;
-    __shared__ __align__(8) uint64_t s_rbar;
-    if constexpr (TMA) {
-        if (tid == 0) {
-            mbar_init(&s_rbar, 1);
-            mbar_fence_init();
-            mbar_expect_tx(&s_rbar, p.rec.loc_ent - rb0);
-            tma_bulk_g2s(smem_raw, rg + rb0, p.rec.loc_ent - rb0, &s_rbar);
-        }
-    }
-    // record bytes: from the shared copy (TMA) or from global memory
-    const unsigned char* rgb = TMA ? (const unsigned char*)smem_raw - rb0 : rg;
+    const unsigned char* rgb = rg;   // the record is read from global memory (read-only path)
     const int e0 = __ldg(p.blk_elem + b), ne = __ldg(p.blk_elem + b + 1) - e0;
     const int no = __ldg(p.blk_occ + b + 1) - __ldg(p.blk_occ + b);
-    if constexpr (TMA) {
-        __syncthreads();            // the mbarrier is initialised
-        mbar_wait(&s_rbar, 0);      // the record has landed
-    }
     const int32_t* socc = reinterpret_cast<const int32_t*>(rgb + p.rec.occ_node);
     const uint16_t* soe = reinterpret_cast<const uint16_t*>(rgb + p.rec.occ_ent);
     const int32_t* sseg = reinterpret_cast<const int32_t*>(rgb + p.rec.occ_seg);
@@ -163,10 +124,10 @@ k_assemble_direct(const AsmParams<T> p) {
     // this thread's first occurrence: phase-2 metadata loaded now, in flight during phase 1
     int w_0 = 0, kb_0 = 0, k1_0 = 0, sl_0 = -1;
     if ((HAS_FORCE || p.f_ext) && tid < no) {
-        w_0 = rld<TMA>(socc + tid);
-        kb_0 = rld<TMA>(soe + tid);
-        k1_0 = rld<TMA>(soe + tid + 1);
-        sl_0 = rld<TMA>(sseg + tid);
+        w_0 = __ldg(socc + tid);
+        kb_0 = __ldg(soe + tid);
+        k1_0 = __ldg(soe + tid + 1);
+        sl_0 = __ldg(sseg + tid);
     }
     int n_inv = 0, first_inv = INT32_MAX, n_nonfin = 0;
     double dot_acc = 0.0;
@@ -187,7 +148,7 @@ k_assemble_direct(const AsmParams<T> p) {
             const T beta = (T)p.cg->beta;
             T* pnew = const_cast<T*>(p.v);
             for (int o = tid; o < no; o += NT) {
-                const int word = rld<TMA>(so + o);
+                const int word = __ldg(so + o);
                 const int64_t base = (int64_t)(word & OCC_NODE_MASK) * D;
                 T pn[D];
 #pragma unroll
@@ -212,18 +173,9 @@ k_assemble_direct(const AsmParams<T> p) {
         if (OTF && s0 == 0) {   // vertex coordinates (fp64) of the block's occurrences
             const int32_t* so = reinterpret_cast<const int32_t*>(rgb + p.rec.occ_node);
             for (int o = tid; o < no; o += NT) {
-                const int node = rld<TMA>(so + o) & OCC_NODE_MASK;
+                const int node = __ldg(so + o) & OCC_NODE_MASK;
 #pragma unroll
                 for (int i = 0; i < D; ++i) cpn<8>(scoord + o * D + i, p.coords + (int64_t)node * D + i);
-            }
-        }
-        // element-wise materials of the block, copied into shared memory with the fields (one
-        // overlapped latency instead of one dependent gather per element and thread)
-        if (PFEM_DIRECT_SMAT && has_mat && s0 == 0) {
-            for (int el = tid; el < ne; el += NT) {
-                const int64_t e = PERM ? (int64_t)rld<TMA>(reinterpret_cast<const int32_t*>(rgb + p.rec.eid) + el) : e0 + el;
-                if (p.mat.s0) cpn<sizeof(T)>(smat + el, p.mat.p0 + e * p.mat.s0);
-                if (p.mat.s1) cpn<sizeof(T)>(smat + EB + el, p.mat.p1 + e * p.mat.s1);
             }
         }
         cp_commit();
@@ -238,14 +190,14 @@ k_assemble_direct(const AsmParams<T> p) {
         for (int el = tid; el < ne; el += NT) {
             // input element id (W_e, material, flags): identity order needs no load, and the
             // material load then does not wait on the id
-            const int e = PERM ? rld<TMA>(reinterpret_cast<const int32_t*>(rgb + p.rec.eid) + el) : e0 + el;
+            const int e = PERM ? __ldg(reinterpret_cast<const int32_t*>(rgb + p.rec.eid) + el) : e0 + el;
             Geo<D, T> G;
             int lv[NV], ep[NV];   // vertex -> staged occurrence, vertex -> block-CSR entry
             if constexpr (D == 3) {
-                const uint2 c = rld<TMA>(reinterpret_cast<const uint2*>(rgb + p.rec.lconn) + el);
+                const uint2 c = __ldg(reinterpret_cast<const uint2*>(rgb + p.rec.lconn) + el);
                 lv[0] = c.x & 0xffff; lv[1] = c.x >> 16; lv[2] = c.y & 0xffff; lv[3] = c.y >> 16;
                 if (EPOS) {
-                    const uint2 q = rld<TMA>(reinterpret_cast<const uint2*>(rgb + p.rec.ent_pos) + el);
+                    const uint2 q = __ldg(reinterpret_cast<const uint2*>(rgb + p.rec.ent_pos) + el);
                     ep[0] = q.x & 0xffff; ep[1] = q.x >> 16; ep[2] = q.y & 0xffff; ep[3] = q.y >> 16;
                 }
             } else {
@@ -253,8 +205,8 @@ k_assemble_direct(const AsmParams<T> p) {
                 const uint16_t* lp = reinterpret_cast<const uint16_t*>(rgb + p.rec.ent_pos) + el * NV;
 #pragma unroll
                 for (int a = 0; a < NV; ++a) {
-                    lv[a] = rld<TMA>(lc + a);
-                    if (EPOS) ep[a] = rld<TMA>(lp + a);
+                    lv[a] = __ldg(lc + a);
+                    if (EPOS) ep[a] = __ldg(lp + a);
                 }
             }
             {
@@ -277,11 +229,11 @@ k_assemble_direct(const AsmParams<T> p) {
 #pragma unroll
                     for (int a = 0; a < D; ++a)
 #pragma unroll
-                        for (int j = 0; j < D; ++j) G.g[a][j] = rld<TMA>(sg + (a * D + j) * EB + el);
-                    G.V = rld<TMA>(reinterpret_cast<const T*>(rgb + p.rec.vol) + el);
+                        for (int j = 0; j < D; ++j) G.g[a][j] = __ldg(sg + (a * D + j) * EB + el);
+                    G.V = __ldg(reinterpret_cast<const T*>(rgb + p.rec.vol) + el);
                 }
-                const T m0 = (PFEM_DIRECT_SMAT && p.mat.s0) ? smat[el] : __ldg(p.mat.p0 + (int64_t)e * p.mat.s0);
-                const T m1 = (PFEM_DIRECT_SMAT && p.mat.s1) ? smat[EB + el] : __ldg(p.mat.p1 + (int64_t)e * p.mat.s1);
+                const T m0 = __ldg(p.mat.p0 + (int64_t)e * p.mat.s0);
+                const T m1 = __ldg(p.mat.p1 + (int64_t)e * p.mat.s1);
                 lame_elem<T>(p.mat, lsc, m0, m1, G.mu, G.lam);
                 G.mu *= G.V;
                 G.lam *= G.V;
@@ -342,19 +294,19 @@ k_assemble_direct(const AsmParams<T> p) {
             // ---------------- phase 2: block-local CSR gather, thread per occurrence
             for (int oi = tid; oi < no; oi += NT) {
                 const bool first = oi == tid;
-                const int word = first ? w_0 : rld<TMA>(socc + oi);
+                const int word = first ? w_0 : __ldg(socc + oi);
                 const int node = word & OCC_NODE_MASK;
                 if (HAS_FORCE) {
                     T accs[SD];
 #pragma unroll
                     for (int k = 0; k < SD; ++k) accs[k] = T(0);
-                    const int k1 = first ? k1_0 : rld<TMA>(soe + oi + 1);
-                    for (int k = first ? kb_0 : rld<TMA>(soe + oi); k < k1; ++k) {
+                    const int k1 = first ? k1_0 : __ldg(soe + oi + 1);
+                    for (int k = first ? kb_0 : __ldg(soe + oi); k < k1; ++k) {
                         const int slot = EPOS ? k : (int)le[k];   // (record loc_ent = force-buffer slot)
                         sacc<T, SD>(fbuf + (size_t)slot * SD, accs);
                     }
                     if (word & (OCC_NONOWNER | OCC_EARLIER)) {
-                        const int slot = first ? sl_0 : rld<TMA>(sseg + oi);
+                        const int slot = first ? sl_0 : __ldg(sseg + oi);
 #pragma unroll
                         for (int q = 0; q < ST; ++q) {
                             if (q >= nq) break;

@@ -13,9 +13,6 @@
 namespace pfem {
 
 constexpr int HT_NT = 256;
-#ifndef PFEM_HEAT_EC
-#define PFEM_HEAT_EC 1   // element-centric fluxes through a CSR-ordered entry buffer (else per-node recompute)
-#endif
 
 template <int D, class T>
 __device__ __forceinline__ void heat_grad(const int32_t* __restrict__ conn, const T* __restrict__ grad, int E,
@@ -324,7 +321,7 @@ pfem_status heat_impl(const pfem_mesh* m, const void* k, int64_t kstride, int S,
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const bool ec = r && ws && PFEM_HEAT_EC;   // element-centric fluxes (W_e formed in the same pass)
+    const bool ec = r && ws;   // element-centric fluxes through a CSR-ordered entry buffer (W_e formed in the same pass)
     if (W && !ec) {
         const int g = std::max(1, std::min(8 * nsm, (E + HT_NT - 1) / HT_NT));
         k_heat_elem<D, T><<<g, HT_NT, 0, s>>>(E, N, S, sstride, m->conn, (const T*)m->grad, (const T*)m->vol,

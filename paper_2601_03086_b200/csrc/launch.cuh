@@ -112,32 +112,21 @@ AsmParams<T> make_params(const Call& c) {
     p.ep_phi = (const T*)c.ep_phi;
     p.ep_scale = (T)(1.0 / ((double)c.S * (double)P.n_parts));
     p.ep_loss = c.ep_loss;
-    p.dbg = 0;
     p.lag = 0;
     return p;
 }
 
-#ifndef PFEM_NTB
-#define PFEM_NTB 256
-#endif
-#ifndef PFEM_DIRECT_NT64
-#define PFEM_DIRECT_NT64 256
-#endif
-#ifndef PFEM_DIRECT_NT32
-#define PFEM_DIRECT_NT32 128
-#endif
+constexpr int NTB_FINISH = 256;   // kernel B threads per CTA (128 / 512 measured no better)
 template <class T>
-constexpr int direct_nt() { return sizeof(T) == 4 ? PFEM_DIRECT_NT32 : PFEM_DIRECT_NT64; }   // direct kernel threads per CTA (measured)
+constexpr int direct_nt() { return sizeof(T) == 4 ? 128 : 256; }   // direct kernel threads per CTA (measured)
 
 template <int D, int MODEL, class T, int OP, int ST, bool MASKED, int NT, bool PERM, bool OTF>
 pfem_status launch_direct(AsmParams<T> p, cudaStream_t s) {
     constexpr bool HAS_FORCE = OP != OP_ENERGY;
     constexpr int NFd = (OP == OP_TANGENT && MODEL == MODEL_NH) ? 2 : 1;
-    const size_t rbn = (PFEM_DIRECT_TMA && sizeof(T) == 4) ? ((p.rec.loc_ent - p.rec.ent_pos + 15u) & ~15u) : 0;
-    const size_t smem0 = rbn + ((NFd * (size_t)p.rec.ocap * D * ST * sizeof(T) + (sizeof(T) == 4 ? 0 : 2 * (size_t)(D + 1) * p.rec.eb) +
-                                15) & ~size_t(15)) +
-                        (HAS_FORCE ? (size_t)ST * D * (D + 1) * p.rec.eb * sizeof(T) : 0) +
-                        ((PFEM_DIRECT_SMAT && (p.mat.s0 | p.mat.s1)) ? 2 * (size_t)p.rec.eb * sizeof(T) : 0);
+    const size_t smem0 = ((NFd * (size_t)p.rec.ocap * D * ST * sizeof(T) + (sizeof(T) == 4 ? 0 : 2 * (size_t)(D + 1) * p.rec.eb) +
+                           15) & ~size_t(15)) +
+                         (HAS_FORCE ? (size_t)ST * D * (D + 1) * p.rec.eb * sizeof(T) : 0);
     // on-the-fly geometry: the block's vertex coordinates [ocap][D] fp64 after everything else
     const size_t smem = OTF ? ((smem0 + 15) & ~size_t(15)) + (size_t)p.rec.ocap * D * sizeof(double) : smem0;
     auto kd = k_assemble_direct<D, MODEL, T, OP, ST, MASKED, NT, PERM, OTF>;
@@ -152,8 +141,7 @@ pfem_status launch_direct(AsmParams<T> p, cudaStream_t s) {
         PFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kd, NT, smem));
         pf_auto = std::max(1, std::min(per_sm, 2) * nsm);   // measured: a deeper prefetch evicts
     }
-    static const int pf = getenv("PFEM_PF") ? atoi(getenv("PFEM_PF")) : -1;
-    p.lag = pf >= 0 ? pf : pf_auto;   // L2 prefetch distance in blocks (~ one wave ahead)
+    p.lag = pf_auto;   // L2 prefetch distance in blocks (~ one wave ahead)
     kd<<<std::max(1, p.n_blocks), NT, smem, s>>>(p);
     PFEM_LAUNCH_CHECK("k_assemble_direct");
     return PFEM_OK;
@@ -164,22 +152,16 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
     constexpr bool HAS_FORCE = OP != OP_ENERGY;
     constexpr bool HAS_PSI = OP == OP_ENERGY || OP == OP_ENERGY_RESIDUAL;
     constexpr int EB = EbOf<D>::value;
-    constexpr int NT = PFEM_STAGED_NT;
+    constexpr int NT = STAGED_NT;
     constexpr int NF = (OP == OP_TANGENT && MODEL == MODEL_NH) ? 2 : 1;   // staged fields (single buffer)
-    // PFEM_DEBUG ablation switches (incomplete results) exist only in PFEM_DBG=1 builds
-    static const int dbg = (PFEM_DBG && getenv("PFEM_DEBUG")) ? atoi(getenv("PFEM_DEBUG")) : 0;
-    static const int variant = getenv("PFEM_VARIANT") ? atoi(getenv("PFEM_VARIANT")) : -1;
-    p.dbg = dbg;
     // kernel A form: direct (one CTA per block, small shared memory) for single-sample calls,
     // where the kernel is bound by memory latency and occupancy pays; staged persistent
     // otherwise (several samples per element: arithmetic-heavy, staging amortised).
-    // PFEM_VARIANT=0/1 forces staged/direct (measurement switch).
     // Blocks larger than the staged kernel's compile-time capacity always take the direct form.
     // (the staged form reads the record with its compile-time stride EB)
     // (CG products, p.cg set, always take the direct form: the staged kernel has no fused p.q)
     // (on-the-fly geometry is a direct-form option)
-    const bool direct = p.otf || p.eb_max > EB || p.rec.eb != EB || p.cg != nullptr ||
-                        (variant >= 0 ? variant == 1 : p.S == 1);
+    const bool direct = p.otf || p.eb_max > EB || p.rec.eb != EB || p.cg != nullptr || p.S == 1;
     if (direct) {
         pfem_status st;
         if (p.otf)
@@ -190,18 +172,14 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
                         : launch_direct<D, MODEL, T, OP, ST, MASKED, direct_nt<T>(), false, false>(p, s);
         if (st != PFEM_OK) return st;
     } else {
-        // the staged copy (RecLayout order) skips conn: every work item stages its fields (and
-        // the NH state u); fp32 with the force buffer in entry order would read ent_pos and not
-        // loc_ent, the element-major buffer reads loc_ent
-        constexpr bool EPOS = sizeof(T) == 4 && PFEM_STAGED_EPOS;
-        p.rec_base = EPOS ? p.rec.ent_pos : p.rec.g;
-        p.rec_end = EPOS ? p.rec.loc_ent : p.rec.bytes;
-        constexpr bool F0D = PFEM_F0_DERIVED && sizeof(T) == 4 && ST == 4 && (D == 3 || PFEM_HP2_2D) && !EPOS &&
-                             PFEM_STAGED_HP2;   // (the kernel's HP == 2 condition)
+        // the staged copy (RecLayout order) skips conn and ent_pos: every work item stages its
+        // fields (and the NH state u); the element-major force buffer is gathered through loc_ent
+        p.rec_base = p.rec.g;
+        p.rec_end = p.rec.bytes;
         const size_t smem = 2 * (size_t)(p.rec_end - p.rec_base) +
                             (((p.mat.s0 | p.mat.s1) != 0) ? 4 * EB * sizeof(T) : 0) +
                             (size_t)NF * p.rec.ocap * D * ST * sizeof(T) +
-                            (HAS_FORCE ? (size_t)ST * D * (D + 1 - (F0D ? 1 : 0)) * EB * sizeof(T) : 0);
+                            (HAS_FORCE ? (size_t)ST * D * (D + 1) * EB * sizeof(T) : 0);
         const int fx = (HAS_PSI && p.f_ext) ? 1 : 0;
         auto kern = fx ? k_assemble<D, MODEL, T, OP, ST, MASKED, EB, NT, HAS_PSI> : k_assemble<D, MODEL, T, OP, ST, MASKED, EB, NT, false>;
         static int resident_[2] = {0, 0};   // per instantiation: co-resident CTAs (persistent grid)
@@ -227,7 +205,7 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
         PFEM_LAUNCH_CHECK("k_assemble");
     }
     // kernel B: finish multi-block nodes + reductions (programmatic dependent launch)
-    constexpr int NTB = PFEM_NTB;   // kernel B threads per CTA
+    constexpr int NTB = NTB_FINISH;
     const int nsc = (p.S + ST - 1) / ST;
     const int n_items = HAS_FORCE ? P_nfix(p) * nsc : 0;
     int gridb = std::max({1, (n_items + NTB - 1) / NTB, 0});
@@ -238,11 +216,9 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
         int dev = 0, nsm = 0;
         PFEM_CUDA_TRY(cudaGetDevice(&dev));
         PFEM_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        const char* env = getenv("PFEM_GRIDB");
-        cap_b = env ? std::max(1, atoi(env)) : 8 * nsm;
+        cap_b = 8 * nsm;   // (592 / 296 / 148 measured slower)
     }
     gridb = std::max(1, std::min(gridb, std::min(p.n_blocks, cap_b)));
-    if (dbg & 32) return PFEM_OK;   // measurement switch: kernel A alone (results incomplete)
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(gridb);
     cfg.blockDim = dim3(NTB);
@@ -252,9 +228,8 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = (dbg & 128) ? 0 : 1;   // measurement switch: plain stream order instead of PDL
-    PFEM_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_node_finish<D, T, ST, MASKED, NTB>, p, HAS_PSI ? 1 : 0,
-                                     (dbg & 64) ? 0 : n_items));
+    cfg.numAttrs = 1;
+    PFEM_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_node_finish<D, T, ST, MASKED, NTB>, p, HAS_PSI ? 1 : 0, n_items));
     count_launch();
     return PFEM_OK;
 }
@@ -262,8 +237,6 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
 template <int D, int MODEL, class T, int OP, bool MASKED>
 pfem_status dispatch_st(const AsmParams<T>& p, cudaStream_t s) {
     constexpr int STBIG = sizeof(T) == 4 ? 4 : 2;
-    static const int st_env = getenv("PFEM_ST") ? atoi(getenv("PFEM_ST")) : 0;   // measurement switch
-    if (p.S > 1 && st_env == 2 && sizeof(T) == 4) return launch_csr<D, MODEL, T, OP, 2, MASKED>(p, s);
     if (p.S > 1) return launch_csr<D, MODEL, T, OP, STBIG, MASKED>(p, s);
     return launch_csr<D, MODEL, T, OP, 1, MASKED>(p, s);
 }
