@@ -189,6 +189,23 @@ def warm_start(u_star: np.ndarray, mask: np.ndarray, seed: int, rel: float = 0.0
     return x0.reshape(u_star.shape)
 
 
+def smooth_warm_start(u_star: np.ndarray, coords: np.ndarray, mask: np.ndarray, seed: int, rel: float = 0.01):
+    """Perturbed-exact warm start with a SMOOTH error, the shape of a network prediction's error:
+    x0 = u* + rel * rms(u*) * Phi(X) / rms(Phi) on free DOFs, Phi a seeded smooth Fourier field
+    over the bounding box (white noise on a slender mesh makes the Neo-Hookean tangent
+    indefinite at x0, which no network prediction does)."""
+    rng = np.random.default_rng(seed)
+    lo, hi = coords.min(0), coords.max(0)
+    phi = fourier_field((coords - lo) / np.maximum(hi - lo, 1e-300), rng).reshape(-1)
+    flat = u_star.reshape(-1)
+    free = mask.reshape(-1) == 0
+    rms = np.sqrt(np.mean(flat[free] ** 2))
+    rphi = np.sqrt(np.mean(phi[free] ** 2))
+    x0 = flat.copy()
+    x0[free] += rel * rms * phi[free] / rphi
+    return x0.reshape(u_star.shape)
+
+
 def small_cube_problem(n_nodes: int = 12, seed_base: int = 4000, brick: int | None = None,
                        n_spheres: int = 20) -> Problem:
     """Config-4 recipe at reduced size (n_nodes^3), for CG iteration-count parity."""
