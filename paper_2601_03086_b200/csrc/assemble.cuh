@@ -93,6 +93,7 @@ struct AsmParams {
     const int32_t* fix_src;
     const int32_t* occ_seg;   // [n_occ] segment slot of a multi-block occurrence
     int n_fix;
+    int n_seg_total;       // segments of multi-block nodes (bounds of occ_seg slots)
     int perm;              // plan positions are a permutation of the input elements
     RecLayout rec;
     uint32_t rec_base;     // staged kernel: record bytes [rec_base, rec_end) are copied
@@ -609,6 +610,8 @@ k_assemble(const AsmParams<T> p) {
                     for (int a = 0; a < NV; ++a) lv[a] = slc[el * NV + a];
                 }
 #pragma unroll
+                for (int a = 0; a < NV; ++a) PFEM_DCHECK(lv[a] < no);
+#pragma unroll
                 for (int qq = 0; qq < ST; qq += L) {
                     if (qq >= nq) break;
                     const int s = s0 + qq;
@@ -699,6 +702,7 @@ k_assemble(const AsmParams<T> p) {
                 const uint16_t* sop = reinterpret_cast<const uint16_t*>(sg + p.rec.occ_perm);
                 for (int w = tid; w < HP * no; w += NT) {
                     const int oi = (int)sop[HP == 1 ? w : w / HP];
+                    PFEM_DCHECK(oi < no);
                     const int qs = HP == 1 ? 0 : (w % HP) * STH;   // first sample of this thread
                     const int word = socc[oi];
                     const int node = word & OCC_NODE_MASK;
@@ -707,6 +711,7 @@ k_assemble(const AsmParams<T> p) {
 #pragma unroll
                         for (int k = 0; k < SDH; ++k) accs[k] = T(0);
                         const int kb = soe[oi], k1 = soe[oi + 1];
+                        PFEM_DCHECK(kb <= k1 && k1 <= NV * ne);
                         if constexpr (HP == 1) {
                             for (int k = kb; k < k1; ++k) sacc<T, SDH>(fbuf + (size_t)sle[k] * SD, accs);
                         } else {
@@ -715,6 +720,7 @@ k_assemble(const AsmParams<T> p) {
                             int k = kb;
                             for (; k + 1 < k1; k += 2) {
                                 const int j0 = sle[k], j1 = sle[k + 1];
+                                PFEM_DCHECK(j0 % EB < ne && j1 % EB < ne && j0 < NV * EB && j1 < NV * EB);
                                 const T* b0 = fbuf + (size_t)j0 * SD + qs;   // (record loc_ent = slot)
                                 const T* b1 = fbuf + (size_t)j1 * SD + qs;
                                 float2 x0[D], x1[D];
@@ -746,6 +752,7 @@ k_assemble(const AsmParams<T> p) {
                             // this block's segment of a multi-block node: seg[slot][s][d], slots
                             // node-major (a node's segments contiguous, ascending block)
                             const int slot = sseg[oi];
+                            PFEM_DCHECK(slot >= 0 && slot < p.n_seg_total);
 #pragma unroll
                             for (int qq = 0; qq < STH; ++qq) {
                                 const int q = qs + qq;
@@ -859,6 +866,7 @@ k_node_finish(const AsmParams<T> p, int op_psi, int n_items) {
         const bool first = item == item0;
         const int node = first ? node0 : __ldg(p.fix_node + f);
         const int k0 = first ? k00 : __ldg(p.fix_src_ptr + f), k1 = first ? k10 : __ldg(p.fix_src_ptr + f + 1);
+        PFEM_DCHECK(k0 < k1 && k1 <= p.n_seg_total && node >= 0 && node < p.N);
         // the node's segments are contiguous: seg[k][s][d], k in [k0, k1) (ascending block)
         T acc[SD];
         ld_seg_vec<T, SD>(p.partial + ((int64_t)k0 * S + s0) * D, acc, nq * D);

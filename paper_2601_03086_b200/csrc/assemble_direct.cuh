@@ -196,6 +196,8 @@ k_assemble_direct(const AsmParams<T> p) {
             if constexpr (D == 3) {
                 const uint2 c = __ldg(reinterpret_cast<const uint2*>(rgb + p.rec.lconn) + el);
                 lv[0] = c.x & 0xffff; lv[1] = c.x >> 16; lv[2] = c.y & 0xffff; lv[3] = c.y >> 16;
+#pragma unroll
+                for (int a = 0; a < NV; ++a) PFEM_DCHECK(lv[a] < no);
                 if (EPOS) {
                     const uint2 q = __ldg(reinterpret_cast<const uint2*>(rgb + p.rec.ent_pos) + el);
                     ep[0] = q.x & 0xffff; ep[1] = q.x >> 16; ep[2] = q.y & 0xffff; ep[3] = q.y >> 16;
@@ -303,10 +305,12 @@ k_assemble_direct(const AsmParams<T> p) {
                     const int k1 = first ? k1_0 : __ldg(soe + oi + 1);
                     for (int k = first ? kb_0 : __ldg(soe + oi); k < k1; ++k) {
                         const int slot = EPOS ? k : (int)le[k];   // (record loc_ent = force-buffer slot)
+                        PFEM_DCHECK(slot < (D + 1) * EB && (EPOS || slot % EB < ne));
                         sacc<T, SD>(fbuf + (size_t)slot * SD, accs);
                     }
                     if (word & (OCC_NONOWNER | OCC_EARLIER)) {
                         const int slot = first ? sl_0 : __ldg(sseg + oi);
+                        PFEM_DCHECK(slot >= 0 && slot < p.n_seg_total);
 #pragma unroll
                         for (int q = 0; q < ST; ++q) {
                             if (q >= nq) break;

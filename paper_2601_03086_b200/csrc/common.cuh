@@ -168,6 +168,16 @@ inline WsLayout ws_layout(const Plan& p, int S, size_t tsize) {
     return L;
 }
 
+// ------------------------------------------------------------------ checked builds
+// PFEM_CHECKED (tools/checked_tests.sh): every plan-derived index is bounds-checked on the device
+// and a violation traps (the kernel faults, the call returns PFEM_ERR_CUDA) — the stand-in for
+// compute-sanitizer, which this pool does not offer.  Release builds compile the checks out.
+#ifdef PFEM_CHECKED
+#define PFEM_DCHECK(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define PFEM_DCHECK(cond) do { } while (0)
+#endif
+
 // ------------------------------------------------------------------ device helpers
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
     int v;

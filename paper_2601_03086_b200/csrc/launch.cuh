@@ -92,6 +92,7 @@ AsmParams<T> make_params(const Call& c) {
     p.fix_src = P.fix_src;
     p.occ_seg = P.occ_seg;
     p.n_fix = P.n_fix;
+    p.n_seg_total = P.n_seg;
     p.perm = P.elem_perm != nullptr;
     p.rec = P.rec;
     p.rec_base = 0;

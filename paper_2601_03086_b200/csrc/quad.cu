@@ -226,7 +226,9 @@ k_quad_elem(const QuadArgs<T> p) {
         const int64_t nnz = (int64_t)p.E * NV;
 #pragma unroll
         for (int a = 0; a < NV; ++a) {
-            const int64_t k = (int64_t)s * nnz + __ldg(p.pos + (int64_t)e * NV + a);
+            const int32_t pk = __ldg(p.pos + (int64_t)e * NV + a);
+            PFEM_DCHECK(pk >= 0 && pk < nnz);
+            const int64_t k = (int64_t)s * nnz + pk;
             p.ebuf[2 * k] = f[a][0];
             p.ebuf[2 * k + 1] = f[a][1];
         }

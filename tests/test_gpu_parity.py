@@ -843,3 +843,48 @@ def test_quad_newton_matches_oracle(orc, kind):
     assert rel_l2(ug.cpu().numpy(), uo) < 1e-9
     _, r1 = pf.newton(mesh, mat, ug, f_ext=f, mask=mask, tol=10 * tol, cg_tol=1e-12)
     assert r1["iterations"] == 0
+
+
+def test_bitwise_deterministic_all_paths():
+    """Every kernel family is bitwise reproducible run to run (no float atomics, fixed orders;
+    also the race check of the checked-build suite: a data race would perturb the bits): the
+    staged form with a ragged sample chunk, the direct form, on-the-fly geometry, the pipelined
+    CG (the solution), Jacobi PCG, the pretraining epilogue and the Q4 / Q8 path."""
+    import paper_2601_03086_b200 as pf
+    from pfem_gen import beam_q4, small_cube_problem
+    rng = np.random.default_rng(123)
+    c, t, _ = plate_with_holes(30, np.random.default_rng(4))
+    mesh = pf.Mesh(torch.as_tensor(c, device="cuda"), torch.as_tensor(t, device="cuda"), dtype=torch.float32,
+                   block_elems=150)
+    mat = pf.Material("neohookean", "lame", torch.as_tensor(rng.uniform(0.3, 1, len(t)), dtype=torch.float32, device="cuda"),
+                      torch.as_tensor(rng.uniform(0.3, 1, len(t)), dtype=torch.float32, device="cuda"))
+    u5 = torch.as_tensor(np.stack([0.05 * fourier_field(c, rng) for _ in range(5)]), dtype=torch.float32, device="cuda")
+    f = torch.as_tensor(0.01 * rng.standard_normal(c.shape), dtype=torch.float32, device="cuda")
+    p4 = small_cube_problem(n_nodes=10, brick=4)
+    m4, mat4, _ = gpu_problem(p4)
+    f4, mk4 = torch.as_tensor(p4.f_ext, device="cuda"), torch.as_tensor(p4.mask, device="cuda")
+    pq = beam_q4(n_cells=10)
+    mq = pf.Mesh(torch.as_tensor(pq.coords, device="cuda"), torch.as_tensor(pq.conn, device="cuda"), elem_type="q4")
+    matq = pf.Material(pq.model, pq.param_kind, torch.as_tensor(pq.p0, device="cuda"), torch.as_tensor(pq.p1, device="cuda"))
+    uq = torch.as_tensor(0.01 * rng.standard_normal((2,) + pq.coords.shape), device="cuda")
+
+    def run():
+        out = []
+        out += list(pf.energy(mesh, mat, u5, f_ext=f, elem_energy=True, residual=True))
+        out += list(pf.energy(mesh, mat, u5[:1], elem_energy=True, residual=True))
+        mesh.geometry = "on_the_fly"
+        out += list(pf.energy(mesh, mat, u5[:1], elem_energy=True, residual=True))
+        mesh.geometry = "stored"
+        out.append(pf.tangent_apply(mesh, mat, u5, u=u5))
+        out += list(pf.pretrain_loss(mesh, mat, u5, f_ext=f)[:3])
+        out.append(pf.cg(m4, mat4, f4, torch.zeros_like(f4), mask=mk4, tol=1e-8)[0])
+        out.append(pf.cg(m4, mat4, f4, torch.zeros_like(f4), mask=mk4, tol=1e-8, precond="jacobi")[0])
+        out += list(pf.energy(mq, matq, uq, elem_energy=True, residual=True))
+        out.append(pf.tangent_apply(mq, matq, uq, u=uq))
+        torch.cuda.synchronize()
+        return [o.clone() for o in out]
+
+    ref = run()
+    for _ in range(2):
+        for a, b in zip(run(), ref):
+            assert torch.equal(a, b)
