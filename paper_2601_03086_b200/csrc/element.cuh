@@ -52,17 +52,45 @@ __device__ __forceinline__ F2 fma(F2 a, float b, F2 c) { return fma(a, F2(b), c)
 __device__ __forceinline__ F2 fma(float a, F2 b, F2 c) { return fma(F2(a), b, c); }
 using ::fma;   // keep the float / double overloads visible next to the F2 ones
 
+// ------------------------------------------------------------------ F4: 4 x fp32 lanes (two F2)
+// Four samples of one element in lockstep: every operation is two independent FFMA2 / FADD2 /
+// FMUL2, which doubles the instruction-level parallelism of the element arithmetic, and the
+// staged fields / force buffer move 16 bytes per shared-memory access.
+struct __align__(16) F4 {
+    F2 a, b;
+    __device__ __forceinline__ F4() {}
+    __device__ __forceinline__ explicit F4(float s) : a(s), b(s) {}
+    __device__ __forceinline__ F4(F2 x, F2 y) : a(x), b(y) {}
+};
+__device__ __forceinline__ F4 operator+(F4 x, F4 y) { return F4(x.a + y.a, x.b + y.b); }
+__device__ __forceinline__ F4 operator-(F4 x, F4 y) { return F4(x.a - y.a, x.b - y.b); }
+__device__ __forceinline__ F4 operator-(F4 x) { return F4(-x.a, -x.b); }
+__device__ __forceinline__ F4 operator*(F4 x, F4 y) { return F4(x.a * y.a, x.b * y.b); }
+__device__ __forceinline__ F4 operator+(F4 x, float y) { return F4(x.a + y, x.b + y); }
+__device__ __forceinline__ F4 operator+(float x, F4 y) { return F4(x + y.a, x + y.b); }
+__device__ __forceinline__ F4 operator-(F4 x, float y) { return F4(x.a - y, x.b - y); }
+__device__ __forceinline__ F4 operator-(float x, F4 y) { return F4(x - y.a, x - y.b); }
+__device__ __forceinline__ F4 operator*(F4 x, float y) { return F4(x.a * y, x.b * y); }
+__device__ __forceinline__ F4 operator*(float x, F4 y) { return F4(x * y.a, x * y.b); }
+__device__ __forceinline__ F4& operator+=(F4& x, F4 y) { x = x + y; return x; }
+__device__ __forceinline__ F4 fma(F4 x, F4 y, F4 z) { return F4(fma(x.a, y.a, z.a), fma(x.b, y.b, z.b)); }
+__device__ __forceinline__ F4 fma(F4 x, float y, F4 z) { return F4(fma(x.a, y, z.a), fma(x.b, y, z.b)); }
+__device__ __forceinline__ F4 fma(float x, F4 y, F4 z) { return F4(fma(x, y.a, z.a), fma(x, y.b, z.b)); }
+
 template <class V> struct VTraits;
 template <> struct VTraits<float> { using S = float; static constexpr int L = 1; };
 template <> struct VTraits<double> { using S = double; static constexpr int L = 1; };
 template <> struct VTraits<F2> { using S = float; static constexpr int L = 2; };
+template <> struct VTraits<F4> { using S = float; static constexpr int L = 4; };
 
 __device__ __forceinline__ float lane(float x, int) { return x; }
 __device__ __forceinline__ double lane(double x, int) { return x; }
 __device__ __forceinline__ float lane(F2 x, int k) { return k ? x.v.y : x.v.x; }
+__device__ __forceinline__ float lane(F4 x, int k) { return k < 2 ? lane(x.a, k) : lane(x.b, k - 2); }
 __device__ __forceinline__ void set_lane(float& x, int, float s) { x = s; }
 __device__ __forceinline__ void set_lane(double& x, int, double s) { x = s; }
 __device__ __forceinline__ void set_lane(F2& x, int k, float s) { if (k) x.v.y = s; else x.v.x = s; }
+__device__ __forceinline__ void set_lane(F4& x, int k, float s) { if (k < 2) set_lane(x.a, k, s); else set_lane(x.b, k - 2, s); }
 
 // reciprocal: fp32 MUFU.RCP + one Newton step (~0.5 ulp); fp64 IEEE division
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -79,6 +107,7 @@ __device__ __forceinline__ F2 vrcp(F2 x) {
     F2 r(rcp_approx(x.v.x), rcp_approx(x.v.y));
     return fma(r, fma(-x, r, F2(1.0f)), r);
 }
+__device__ __forceinline__ F4 vrcp(F4 x) { return F4(vrcp(x.a), vrcp(x.b)); }
 
 // ln J = log1p(x) and g(x) = x - log1p(x) >= 0 together, cancellation-free.
 // |x| < 1/2: z = x/(2+x) (|z| < 1/3), log1p = 2 z (1 + z^2 s(z^2)), g = x^2/(2+x) - 2 z^3 s(z^2),
