@@ -431,6 +431,36 @@ static pfem_status tangent(const pfem_mesh* m, const Plan* P, const pfem_materia
     return run_assemble<D, T>(c);
 }
 
+// Instantiated CG graphs, reused across calls: a graph bakes in every pointer and launch
+// parameter of its B captured iterations, so it is keyed on all of them (plan serial, mesh
+// arrays, material, state, mask, solution, workspace, history, B, mode, preconditioner).
+// A few per host thread; the least recently captured one is replaced.
+struct CgGraphKey {
+    uint64_t serial;
+    const void* ptr[12];
+    int64_t val[8];
+    bool operator==(const CgGraphKey& o) const {
+        if (serial != o.serial) return false;
+        for (int i = 0; i < 12; ++i)
+            if (ptr[i] != o.ptr[i]) return false;
+        for (int i = 0; i < 8; ++i)
+            if (val[i] != o.val[i]) return false;
+        return true;
+    }
+};
+struct CgGraphEntry {
+    CgGraphKey key;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int64_t per_graph = 0;
+    int device = -1;
+};
+constexpr int CG_GRAPH_CACHE = 4;
+static thread_local CgGraphEntry g_cg_graphs[CG_GRAPH_CACHE];
+static thread_local int g_cg_next = 0;
+static thread_local cudaStream_t g_cg_stream = nullptr;
+static thread_local int g_cg_stream_dev = -1;
+
 template <int D, class T>
 pfem_status cg_impl(const pfem_mesh* m, const pfem_material* mat, const void* u_state, const void* rhs,
                     const uint8_t* mask, void* xv, double tol, int max_iter, int mode, double* history,
@@ -482,14 +512,30 @@ pfem_status cg_impl(const pfem_mesh* m, const pfem_material* mat, const void* u_
         // capture B iterations into a graph on a private stream, replay on `s`
         // an even B keeps the two direction buffers of the pipelined loop aligned across replays
         const int B = std::max(1, std::min(32, max_iter + (max_iter & 1)));
-        cudaStream_t cs;
-        PFEM_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        CgGraphKey key{};
+        key.serial = P->serial;
+        const void* kp[12] = {m->conn, m->grad, m->vol, m->coords, mat->p0, mat->p1, u_state, mask, x, ws, history,
+                              (const void*)s};
+        for (int i = 0; i < 12; ++i) key.ptr[i] = kp[i];
+        const int64_t kv[8] = {B, mode, precond, mat->model, mat->kind, mat->stride0, mat->stride1,
+                               (int64_t)m->geometry * 16 + (int64_t)sizeof(T)};
+        for (int i = 0; i < 8; ++i) key.val[i] = kv[i];
+        CgGraphEntry* hit = nullptr;
+        for (auto& en : g_cg_graphs)
+            if (en.exec && en.device == dev && en.key == key) hit = &en;
+        cudaError_t cerr = cudaSuccess;
+        if (!hit) {
+        if (g_cg_stream == nullptr || g_cg_stream_dev != dev) {
+            PFEM_CUDA_TRY(cudaStreamCreateWithFlags(&g_cg_stream, cudaStreamNonBlocking));
+            g_cg_stream_dev = dev;
+        }
+        cudaStream_t cs = g_cg_stream;
         cudaGraph_t graph = nullptr;
         cudaGraphExec_t exec = nullptr;
         int64_t launches_before = pfem_launch_count(0);
         pfem_status ce = PFEM_OK;
-        cudaError_t cerr = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
-        if (cerr != cudaSuccess) { cudaStreamDestroy(cs); return cuda_status(cerr, "cudaStreamBeginCapture"); }
+        cerr = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+        if (cerr != cudaSuccess) return cuda_status(cerr, "cudaStreamBeginCapture");
         // pipelined iteration (§8(f) row f3): the simplex CSR element kernel
         const bool fuse = mode == PFEM_ASSEMBLE_CSR && P->elem_type == PFEM_ELEM_SIMPLEX;
         for (int it = 0; it < B && ce == PFEM_OK; ++it) {
@@ -525,12 +571,26 @@ pfem_status cg_impl(const pfem_mesh* m, const pfem_material* mat, const void* u_
         if (ce == PFEM_OK && cerr == cudaSuccess) cerr = cudaGraphInstantiate(&exec, graph, 0);
         if (ce != PFEM_OK || cerr != cudaSuccess) {
             if (graph) cudaGraphDestroy(graph);
-            cudaStreamDestroy(cs);
             if (ce != PFEM_OK) return ce;
             return cuda_status(cerr, "cg graph capture");
         }
         // the captured launches were counted at capture; count replays instead
         count_launch((int)-per_graph);
+        CgGraphEntry& en = g_cg_graphs[g_cg_next];
+        g_cg_next = (g_cg_next + 1) % CG_GRAPH_CACHE;
+        if (en.exec) {
+            cudaGraphExecDestroy(en.exec);
+            cudaGraphDestroy(en.graph);
+        }
+        en.key = key;
+        en.graph = graph;
+        en.exec = exec;
+        en.per_graph = per_graph;
+        en.device = dev;
+        hit = &en;
+        }
+        cudaGraphExec_t exec = hit->exec;
+        const int64_t per_graph = hit->per_graph;
         int launched = 0;
         while (true) {
             cerr = cudaGraphLaunch(exec, s);
@@ -542,9 +602,6 @@ pfem_status cg_impl(const pfem_mesh* m, const pfem_material* mat, const void* u_
             cerr = cudaStreamSynchronize(s);
             if (cerr != cudaSuccess || h.done || launched >= max_iter + B) break;
         }
-        cudaGraphExecDestroy(exec);
-        cudaGraphDestroy(graph);
-        cudaStreamDestroy(cs);
         if (cerr != cudaSuccess) return cuda_status(cerr, "cg loop");
     }
     // true residual ||b - A x|| / ||b||
