@@ -307,6 +307,11 @@ pfem_status pfem_tangent_apply(const pfem_mesh* m, const pfem_material* mat, int
  *   x        in: x0 (constrained entries = prescribed values); out: solution / partial
  *   history  nullable device double [max_iter+1]: ||r_k|| / ||b_free||
  *   report   host
+ * Iteration: in CSR mode on simplex meshes the pipelined form of SURVEY §8(f) row f3 (reading
+ * R34): the element kernel forms p = z + beta p while staging p, kernel B forms p.q and alpha,
+ * one update pass forms x, r, r.r and beta — 3 launches, the iterates of the unfused loop.
+ * COLOUR mode and Q4 / Q8 meshes run the unfused 4-launch loop.  32 iterations are captured in a
+ * CUDA graph, cached per host thread for calls with the same arrays, workspace and options.
  * Synchronises `stream`.  Returns PFEM_OK, PFEM_ERR_NOT_CONVERGED or PFEM_ERR_BREAKDOWN
  * (report filled in all three cases).
  * --------------------------------------------------------------------------------- */
