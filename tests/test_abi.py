@@ -50,3 +50,32 @@ def test_oracle_not_imported_by_product():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "pfem_oracle" not in txt, f
+
+
+def test_ctypes_structs_match_the_header_layout(tmp_path):
+    """Every struct the binding mirrors has the header's size and field offsets: a C program
+    compiled against include/pfem.h prints offsetof / sizeof, compared with ctypes."""
+    import subprocess
+    from paper_2601_03086_b200 import _lib as L
+    structs = {"pfem_mesh": L.pfem_mesh, "pfem_material": L.pfem_material, "pfem_flags": L.pfem_flags,
+               "pfem_cg_report": L.pfem_cg_report, "pfem_newton_report": L.pfem_newton_report}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "pfem.h"', 'int main(void) {']
+    for name, cls in structs.items():
+        lines.append(f'    printf("{name} size %zu\\n", sizeof({name}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'    printf("{name} {fname} %zu\\n", offsetof({name}, {fname}));')
+    lines += ['    return 0;', '}']
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    out = subprocess.check_output([str(exe)], text=True).split("\n")
+    got = {}
+    for ln in out:
+        if ln.strip():
+            parts = ln.split()
+            got[(parts[0], parts[1])] = int(parts[2])
+    for name, cls in structs.items():
+        assert got[(name, "size")] == ctypes.sizeof(cls), name
+        for fname, _ in cls._fields_:
+            assert got[(name, fname)] == getattr(cls, fname).offset, (name, fname)
