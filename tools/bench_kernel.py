@@ -35,11 +35,15 @@ def main():
     ap.add_argument("--order", default="auto", choices=["auto", "input", "locality"])
     ap.add_argument("--otf", action="store_true", help="geometry formed on the fly from coords")
     ap.add_argument("--lib", default=None, help="an alternative in-tree build (libpfem_<tag>.so)")
+    ap.add_argument("--brick", type=int, default=0, help="configs 3 / 4: generator brick size (0 = default)")
     a = ap.parse_args()
     if a.lib:
         from paper_2601_03086_b200 import _lib
         _lib.load(os.path.join(ROOT, "paper_2601_03086_b200", a.lib))
-    prob = CONFIGS[a.config]() if a.config != 2 else CONFIGS[2](dtype=a.dtype or "f32")
+    if a.brick and a.config in (3, 4):
+        prob = CONFIGS[a.config](brick=a.brick)
+    else:
+        prob = CONFIGS[a.config]() if a.config != 2 else CONFIGS[2](dtype=a.dtype or "f32")
     dt = torch.float32 if (a.dtype or prob.dtype) == "f32" else torch.float64
     s = 4 if dt == torch.float32 else 8
     dev = "cuda"
