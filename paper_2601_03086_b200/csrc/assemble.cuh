@@ -523,24 +523,39 @@ k_assemble(const AsmParams<T> p) {
     const int G = gridDim.x;
     int t = blockIdx.x;
     uint32_t par0 = 0u, par1 = 0u;   // mbarrier phase of each record buffer (registers, no arrays)
+    // item t = (chunk c, block b), t = c nb + b, advanced by G without divisions
+    int b = t, c = 0;
+    while (b >= nb) { b -= nb; ++c; }
+    int bn = b + G, cn = c;
+    while (bn >= nb) { bn -= nb; ++cn; }
+    // block metadata of the current item (the next item's is loaded one item ahead)
+    int e0 = 0, ne = 0, no = 0;
     // prologue: record of the first block, then its fields
     const bool has_mat = (p.mat.s0 | p.mat.s1) != 0;
     if (t < NI) {
-        const int bt = t % nb, s0t = (t / nb) * ST;
-        stage_block<D, T, NT>(stage0, mstage, &s_bar[0], p, bt);
+        e0 = __ldg(p.blk_elem + b);
+        ne = __ldg(p.blk_elem + b + 1) - e0;
+        no = __ldg(p.blk_occ + b + 1) - __ldg(p.blk_occ + b);
+        const int s0t = c * ST;
+        stage_block<D, T, NT>(stage0, mstage, &s_bar[0], p, b);
         mbar_wait(&s_bar[0], 0);
-        const int no0 = __ldg(p.blk_occ + bt + 1) - __ldg(p.blk_occ + bt);
-        stage_fields<D, T, NT, ST, MASKED>(ustage, stage0, p.rec_base, staged_src, p, s0t, min(ST, S - s0t), no0);
-        if (NF == 2) stage_fields<D, T, NT, ST, false>(ustage + ust1, stage0, p.rec_base, p.u, p, s0t, min(ST, S - s0t), no0);
-        if (has_mat) stage_material<T, NT>(mstage, stage0, p.rec_base, p, bt);
+        stage_fields<D, T, NT, ST, MASKED>(ustage, stage0, p.rec_base, staged_src, p, s0t, min(ST, S - s0t), no);
+        if (NF == 2) stage_fields<D, T, NT, ST, false>(ustage + ust1, stage0, p.rec_base, p.u, p, s0t, min(ST, S - s0t), no);
+        if (has_mat) stage_material<T, NT>(mstage, stage0, p.rec_base, p, b);
         cp_commit();
     }
     for (int it = 0; t < NI; ++it, t += G) {
         const int cur = it & 1;
         const int tn = t + G;
-        const int b = t % nb, bn = tn % nb;
-        const int s0 = (t / nb) * ST;          // this item's sample chunk
+        const int s0 = c * ST;                 // this item's sample chunk
         const int nq = min(ST, S - s0);
+        // the next item's block metadata (used at its start and to stage its fields)
+        int e0n = 0, nen = 0, non = 0;
+        if (tn < NI) {
+            e0n = __ldg(p.blk_elem + bn);
+            nen = __ldg(p.blk_elem + bn + 1) - e0n;
+            non = __ldg(p.blk_occ + bn + 1) - __ldg(p.blk_occ + bn);
+        }
         // prefetch the next item's record (its fields follow after phase 1)
         unsigned char* const sg_cur = cur ? stage1 : stage0;
         unsigned char* const sg_nxt = cur ? stage0 : stage1;
@@ -548,12 +563,12 @@ k_assemble(const AsmParams<T> p) {
         else cp_commit();
         if (tid == 32 && tn + G < NI) {
             // the record after next into L2, so next iteration's bulk copy is an L2 hit
-            const size_t rb = p.rec.bytes, off = (size_t)((tn + G) % nb) * rb + p.rec_base;
+            int bnn = bn + G;
+            while (bnn >= nb) bnn -= nb;
+            const size_t rb = p.rec.bytes, off = (size_t)bnn * rb + p.rec_base;
             const uintptr_t a0 = (uintptr_t)(p.recs + off), a1 = (uintptr_t)(p.recs + off + (p.rec_end - p.rec_base));
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((unsigned)(a1 - a0)) : "memory");
         }
-        const int e0 = __ldg(p.blk_elem + b), ne = __ldg(p.blk_elem + b + 1) - e0;
-        const int o0 = __ldg(p.blk_occ + b), no = __ldg(p.blk_occ + b + 1) - o0;
         const unsigned char* sg = sg_cur - p.rec_base;   // record byte offsets apply from here
         const int32_t* sconn = reinterpret_cast<const int32_t*>(sg + p.rec.conn);   // valid iff rec_base <= conn
         const T* sgrad = reinterpret_cast<const T*>(sg + p.rec.g);
@@ -700,8 +715,7 @@ k_assemble(const AsmParams<T> p) {
             {
                 if (tn < NI) {
                     mbar_wait(&s_bar[cur ^ 1], cur ? par0 : par1);
-                    const int non = __ldg(p.blk_occ + bn + 1) - __ldg(p.blk_occ + bn);
-                    const int s0n = (tn / nb) * ST, nqn = min(ST, S - s0n);
+                    const int s0n = cn * ST, nqn = min(ST, S - s0n);
                     stage_fields<D, T, NT, ST, MASKED>(ustage, sg_nxt, p.rec_base, staged_src, p, s0n, nqn, non);
                     if (NF == 2) stage_fields<D, T, NT, ST, false>(ustage + ust1, sg_nxt, p.rec_base, p.u, p, s0n, nqn, non);
                     if (has_mat)
@@ -837,6 +851,9 @@ k_assemble(const AsmParams<T> p) {
             }
         }
         // s_red is rewritten only after the next block's first barrier: warp 0 is done by then
+        b = bn; c = cn; e0 = e0n; ne = nen; no = non;
+        bn += G;
+        while (bn >= nb) { bn -= nb; ++cn; }
     }
     cp_wait<0>();
     if (n_inv) {
