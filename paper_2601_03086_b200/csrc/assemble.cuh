@@ -445,16 +445,32 @@ __device__ __forceinline__ void stage_fields(T* ust, const unsigned char* rec, u
         uint32_t keep[D];
 #pragma unroll
         for (int i = 0; i < D; ++i) keep[i] = MASKED ? (__ldg(p.mask + (int64_t)node * D + i) ? 0u : (uint32_t)sizeof(T)) : (uint32_t)sizeof(T);
-        for (int q = 0; q < nq; ++q) {
+        const int64_t ss = p.sstride;
+        const uint32_t d0 = smem_addr(dst);
+        if (nq == ST) {   // a full chunk: straight-line copies
 #pragma unroll
-            for (int i = 0; i < D; ++i) {
-                if (MASKED)
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(smem_addr(dst + i * ST + q)),
-                                 "l"(g + i), "n"(sizeof(T)), "r"(keep[i]));
-                else
-                    cpn<sizeof(T)>(dst + i * ST + q, g + i);
+            for (int q = 0; q < ST; ++q)
+#pragma unroll
+                for (int i = 0; i < D; ++i) {
+                    if (MASKED)
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(d0 + (uint32_t)((i * ST + q) * sizeof(T))),
+                                     "l"(g + q * ss + i), "n"(sizeof(T)), "r"(keep[i]));
+                    else
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d0 + (uint32_t)((i * ST + q) * sizeof(T))),
+                                     "l"(g + q * ss + i), "n"(sizeof(T)));
+                }
+        } else {
+            for (int q = 0; q < nq; ++q) {
+#pragma unroll
+                for (int i = 0; i < D; ++i) {
+                    if (MASKED)
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(smem_addr(dst + i * ST + q)),
+                                     "l"(g + i), "n"(sizeof(T)), "r"(keep[i]));
+                    else
+                        cpn<sizeof(T)>(dst + i * ST + q, g + i);
+                }
+                g += ss;
             }
-            g += p.sstride;
         }
         // a ragged last chunk: the unused sample lanes are zero (the four-sample lockstep
         // arithmetic then sees F = I there: finite, no inversion, nothing stored)
