@@ -7,6 +7,12 @@
 
 #include "assemble.cuh"
 #include "assemble_direct.cuh"
+#include "assemble_dt.cuh"
+
+#ifndef PFEM_DT
+#define PFEM_DT 1   // fp64 single-sample calls: the in-place form (assemble_dt.cuh; config 4 K.v 131.3 -> 115.6 us);
+                    // 0 = k_assemble_direct (A/B builds)
+#endif
 
 namespace pfem {
 template <class T>
@@ -148,6 +154,36 @@ pfem_status launch_direct(AsmParams<T> p, cudaStream_t s) {
     return PFEM_OK;
 }
 
+// the in-place single-sample form (assemble_dt.cuh).  Returns 1 when launched, 0 when the plan's
+// record layout or the shared-memory size does not suit it (the caller then takes
+// k_assemble_direct), or a negative pfem_status
+template <int D, int MODEL, class T, int OP, bool MASKED, int NT, bool PERM>
+int launch_dt(AsmParams<T> p, cudaStream_t s) {
+    constexpr int NFd = (OP == OP_TANGENT && MODEL == MODEL_NH) ? 2 : 1;
+    const DtLayout L = dt_layout(p.rec, D, (int)sizeof(T), NFd);
+    if (!L.ok) return 0;
+    auto kd = k_assemble_dt<D, MODEL, T, OP, MASKED, NT, PERM>;
+    static size_t configured = 0;
+    static int pf_auto = 0;
+    const size_t smem = L.total;
+    if (smem > configured || pf_auto == 0) {
+        int dev = 0, nsm = 0, per_sm = 0, maxsm = 0;
+        PFEM_CUDA_TRY(cudaGetDevice(&dev));
+        PFEM_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        PFEM_CUDA_TRY(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        if (smem > (size_t)maxsm) return 0;
+        PFEM_CUDA_TRY(cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = std::max(configured, smem);
+        PFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kd, NT, smem));
+        if (per_sm < 1) return 0;
+        pf_auto = std::max(1, std::min(per_sm, 2) * nsm);   // L2 prefetch distance (~ one wave)
+    }
+    p.lag = pf_auto;
+    kd<<<std::max(1, p.n_blocks), NT, smem, s>>>(p);
+    PFEM_LAUNCH_CHECK("k_assemble_dt");
+    return 1;
+}
+
 template <int D, int MODEL, class T, int OP, int ST, bool MASKED>
 pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
     constexpr bool HAS_FORCE = OP != OP_ENERGY;
@@ -164,8 +200,15 @@ pfem_status launch_csr(AsmParams<T> p, cudaStream_t s) {
     // (on-the-fly geometry is a direct-form option)
     const bool direct = p.otf || p.eb_max > EB || p.rec.eb != EB || p.cg != nullptr || p.S == 1;
     if (direct) {
-        pfem_status st;
-        if (p.otf)
+        pfem_status st = PFEM_OK;
+        int done = 0;
+        if (PFEM_DT && ST == 1 && sizeof(T) == 8 && !p.otf) {   // (fp32 config 5: 70.5 -> 74.1 us, not taken)
+            done = p.perm ? launch_dt<D, MODEL, T, OP, MASKED, direct_nt<T>(), true>(p, s)
+                          : launch_dt<D, MODEL, T, OP, MASKED, direct_nt<T>(), false>(p, s);
+            if (done < 0) return (pfem_status)done;
+        }
+        if (done) {
+        } else if (p.otf)
             st = p.perm ? launch_direct<D, MODEL, T, OP, ST, MASKED, direct_nt<T>(), true, true>(p, s)
                         : launch_direct<D, MODEL, T, OP, ST, MASKED, direct_nt<T>(), false, true>(p, s);
         else
