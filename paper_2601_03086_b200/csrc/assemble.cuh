@@ -35,9 +35,9 @@ namespace pfem {
 enum { OP_ENERGY = 0, OP_ENERGY_RESIDUAL = 1, OP_RESIDUAL = 2, OP_TANGENT = 3 };
 // staged kernel shape (measured): 256 threads, 2 resident CTAs per SM, T4 blocks of
 // at most 256 elements (T3: 512)
-constexpr int STAGED_MINB = 2;
-constexpr int STAGED_NT = 256;
-constexpr int EB3 = 256;
+constexpr int STAGED_MINB = PFEM_STAGED_MINB;
+constexpr int STAGED_NT = PFEM_STAGED_NT;
+constexpr int EB3 = PFEM_EB3;
 constexpr int ASM_NT = 256;   // main (element / occurrence) threads per CTA
 constexpr int FIX_WARPS = 1;  // fix-up warps per CTA (+1 publisher warp)
 constexpr int FIX_UNROLL = 4; // segments loaded together by one fix-up lane
@@ -499,6 +499,7 @@ k_assemble(const AsmParams<T> p) {
     constexpr int L = VTraits<V>::L;
     // fbuf[NV][EB][D][ST] in element order, gathered through loc_ent in phase 2
     constexpr int HP = (sizeof(T) == 4 && ST == 4) ? 2 : 1;   // phase-2 threads per occurrence
+    constexpr bool P2DIM = PFEM_P2DIM && sizeof(T) == 4 && ST == 4;   // ... or one per (occurrence, component)
     constexpr int STH = ST / HP;
     constexpr int SDH = D * STH;
     const T* staged_src = (OP == OP_TANGENT) ? p.v : p.u;
@@ -744,6 +745,71 @@ k_assemble(const AsmParams<T> p) {
                 // (fp32 ST = 4: two threads, each summing two samples of every entry, so all
                 // warps share the gather and each entry chain is half as long)
                 const uint16_t* sop = reinterpret_cast<const uint16_t*>(sg + p.rec.occ_perm);
+                if constexpr (P2DIM) {
+                    // fp32, four samples: one thread per (occurrence, component) sums the four
+                    // samples of its component with one 16-byte load per entry.  The D threads
+                    // of an occurrence read the D consecutive 16-byte granules of a force row,
+                    // so a warp's gather spreads over the banks (the sample-pair split read the
+                    // same granule from two lanes: 5.5 wavefronts per LDS.64 against 1.9 ideal,
+                    // and phase 2 ran at the shared-memory pipe's limit; ncu r02b)
+                    for (int w = tid; w < D * no; w += NT) {
+                        const int o = w / D, i = w - o * D;
+                        const int oi = (int)sop[o];
+                        PFEM_DCHECK(oi < no);
+                        const int word = socc[oi];
+                        const int node = word & OCC_NODE_MASK;
+                        if (HAS_FORCE) {
+                            F2 a0(0.0f, 0.0f), a1(0.0f, 0.0f);   // samples (0, 1) and (2, 3)
+                            const int kb = soe[oi], k1 = soe[oi + 1];
+                            PFEM_DCHECK(kb <= k1 && k1 <= NV * ne);
+                            const T* fb = fbuf + i * ST;
+                            int k = kb;
+                            for (; k + 1 < k1; k += 2) {   // ascending entry order, two gathers in flight
+                                const int j0 = sle[k], j1 = sle[k + 1];
+                                PFEM_DCHECK(j0 % EB < ne && j1 % EB < ne && j0 < NV * EB && j1 < NV * EB);
+                                const float4 x0 = *reinterpret_cast<const float4*>(fb + (size_t)j0 * SD);
+                                const float4 x1 = *reinterpret_cast<const float4*>(fb + (size_t)j1 * SD);
+                                a0 = (a0 + F2(x0.x, x0.y)) + F2(x1.x, x1.y);
+                                a1 = (a1 + F2(x0.z, x0.w)) + F2(x1.z, x1.w);
+                            }
+                            if (k < k1) {
+                                const float4 x0 = *reinterpret_cast<const float4*>(fb + (size_t)sle[k] * SD);
+                                a0 = a0 + F2(x0.x, x0.y);
+                                a1 = a1 + F2(x0.z, x0.w);
+                            }
+                            const T acc4[4] = {a0.v.x, a0.v.y, a1.v.x, a1.v.y};
+                            if (word & (OCC_NONOWNER | OCC_EARLIER)) {
+                                const int slot = sseg[oi];
+                                PFEM_DCHECK(slot >= 0 && slot < p.n_seg_total);
+                                T* dst = p.partial + ((int64_t)slot * S + s0) * D + i;
+#pragma unroll
+                                for (int q = 0; q < ST; ++q) {
+                                    if (q >= nq) break;
+                                    dst[q * D] = acc4[q];
+                                }
+                            } else {
+                                const int64_t dof = (int64_t)node * D + i;
+                                const bool fixed = OP == OP_TANGENT && MASKED && __ldg(p.mask + dof);
+#pragma unroll
+                                for (int q = 0; q < ST; ++q) {
+                                    if (q >= nq) break;
+                                    const int64_t at = (int64_t)(s0 + q) * p.sstride + dof;
+                                    const T val = fixed ? __ldg(p.v + at) : acc4[q];
+                                    p.out[at] = out_value(p, dof, val);
+                                }
+                            }
+                        }
+                        if (HAS_PSI && FEXT && !(word & OCC_NONOWNER)) {
+                            const int64_t dof = (int64_t)node * D + i;
+                            const double fe = (double)__ldg(p.f_ext + dof);
+#pragma unroll
+                            for (int q = 0; q < ST; ++q) {
+                                if (q >= nq) break;
+                                fsum[q] += fe * (double)__ldg(p.u + (int64_t)(s0 + q) * p.sstride + dof);
+                            }
+                        }
+                    }
+                } else
                 for (int w = tid; w < HP * no; w += NT) {
                     const int oi = (int)sop[HP == 1 ? w : w / HP];
                     PFEM_DCHECK(oi < no);
@@ -762,6 +828,31 @@ k_assemble(const AsmParams<T> p) {
                             // entries in pairs: both gathers in flight before the adds (the
                             // adds stay in ascending entry order)
                             int k = kb;
+#if PFEM_P2U > 2
+                            // PFEM_P2U entries per iteration, all gathers in flight before the
+                            // adds; a short tail re-reads the last entry and skips its add
+                            for (; k < k1; k += PFEM_P2U) {
+                                int j[PFEM_P2U];
+#pragma unroll
+                                for (int u = 0; u < PFEM_P2U; ++u) j[u] = sle[min(k + u, k1 - 1)];
+                                float2 x[PFEM_P2U][D];
+#pragma unroll
+                                for (int u = 0; u < PFEM_P2U; ++u)
+#pragma unroll
+                                    for (int i = 0; i < D; ++i)
+                                        x[u][i] = *reinterpret_cast<const float2*>(fbuf + (size_t)j[u] * SD + qs + i * ST);
+#pragma unroll
+                                for (int u = 0; u < PFEM_P2U; ++u)
+                                    if (k + u < k1) {
+#pragma unroll
+                                        for (int i = 0; i < D; ++i) {
+                                            F2 a0(accs[2 * i], accs[2 * i + 1]);
+                                            a0 = a0 + F2(x[u][i].x, x[u][i].y);
+                                            accs[2 * i] = a0.v.x; accs[2 * i + 1] = a0.v.y;
+                                        }
+                                    }
+                            }
+#endif
                             for (; k + 1 < k1; k += 2) {
                                 const int j0 = sle[k], j1 = sle[k + 1];
                                 PFEM_DCHECK(j0 % EB < ne && j1 % EB < ne && j0 < NV * EB && j1 < NV * EB);
