@@ -328,7 +328,6 @@ __device__ __forceinline__ void stage_block(unsigned char* st, T* mst, uint64_t*
         mbar_expect_tx(bar, n);
         tma_bulk_g2s(st, p.recs + (size_t)b * p.rec.bytes + p.rec_base, n, bar);
     }
-    cp_commit();   // (empty group: keeps the one-group-per-stage accounting of cp_wait)
 }
 
 // element-wise material of a block whose record has landed in shared memory: cp.async by
@@ -514,7 +513,7 @@ k_assemble(const AsmParams<T> p) {
     const size_t ust_sz = (size_t)NF * ust1;
     T* fbuf = ustage + ust_sz;
     __shared__ __align__(8) uint64_t s_bar[2];
-    __shared__ double s_red[NT / 32][2 * ST + 1];
+    __shared__ double s_red[2][NT / 32][2 * ST + 1];   // per-warp sums of an item, by item parity
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int S = p.S;
     // work items: (block, sample chunk of ST samples), chunk-major, so S > ST calls spread over
@@ -547,6 +546,7 @@ k_assemble(const AsmParams<T> p) {
     while (bn >= nb) { bn -= nb; ++cn; }
     // block metadata of the current item (the next item's is loaded one item ahead)
     int e0 = 0, ne = 0, no = 0;
+    int b_prev = -1, s0_prev = 0, nq_prev = 1, cur_prev = 0;   // the item whose sums warp 0 still has to add
     // prologue: record of the first block, then its fields
     const bool has_mat = (p.mat.s0 | p.mat.s1) != 0;
     if (t < NI) {
@@ -566,18 +566,28 @@ k_assemble(const AsmParams<T> p) {
         const int tn = t + G;
         const int s0 = c * ST;                 // this item's sample chunk
         const int nq = min(ST, S - s0);
-        // the next item's block metadata (used at its start and to stage its fields)
-        int e0n = 0, nen = 0, non = 0;
+        // the next item's block metadata, raw: the differences are formed after phase 1, where
+        // they are first used, so no warp waits on these loads here (the early subtraction
+        // held 6% of the kernel's stall samples, ncu r02b)
+        int e0n = 0, e1n = 0, o0n = 0, o1n = 0;
         if (tn < NI) {
             e0n = __ldg(p.blk_elem + bn);
-            nen = __ldg(p.blk_elem + bn + 1) - e0n;
-            non = __ldg(p.blk_occ + bn + 1) - __ldg(p.blk_occ + bn);
+            e1n = __ldg(p.blk_elem + bn + 1);
+            o0n = __ldg(p.blk_occ + bn);
+            o1n = __ldg(p.blk_occ + bn + 1);
         }
-        // prefetch the next item's record (its fields follow after phase 1)
         unsigned char* const sg_cur = cur ? stage1 : stage0;
         unsigned char* const sg_nxt = cur ? stage0 : stage1;
+        mbar_wait(&s_bar[cur], cur ? par1 : par0);   // this block's record
+        if (cur) par1 ^= 1u; else par0 ^= 1u;
+        cp_wait<0>();                          // this thread's material + field copies of block b
+        // One barrier covers the start of an item: everyone's field copies have landed, and
+        // every thread has left the previous item's phase 2 (its record buffer, the force
+        // buffer and the other half of s_red are free).  There is no barrier at an item's end.
+        bar_main(NT);
+        // prefetch the next item's record into the buffer the previous item used (its fields
+        // follow after phase 1)
         if (tn < NI) stage_block<D, T, NT>(sg_nxt, mstage + 2 * EB * (cur ^ 1), &s_bar[cur ^ 1], p, bn);
-        else cp_commit();
         if (tid == 32 && tn + G < NI) {
             // the record after next into L2, so next iteration's bulk copy is an L2 hit
             int bnn = bn + G;
@@ -598,10 +608,13 @@ k_assemble(const AsmParams<T> p) {
         const int32_t* seid = reinterpret_cast<const int32_t*>(sg + p.rec.eid);
         const T* smat = mstage + 2 * EB * cur;
         const T* ust = ustage;
-        mbar_wait(&s_bar[cur], cur ? par1 : par0);   // this block's record
-        if (cur) par1 ^= 1u; else par0 ^= 1u;
-        cp_wait<1>();                          // this thread's material + field copies of block b
-        bar_main(NT);                          // everyone's field copies have landed
+        // the previous item's per-block sums (its warps' sums are complete: the barrier above)
+        if (HAS_PSI && it > 0 && warp == 0 && lane < 2 * nq_prev) {
+            const int q = lane % nq_prev, kind = lane / nq_prev;
+            double r = 0.0;
+            for (int w = 0; w < NT / 32; ++w) r += s_red[cur ^ 1][w][kind * ST + q];
+            p.blk_sum[(int64_t)(kind * S + s0_prev + q) * p.n_blocks + b_prev] = r;
+        }
         double dot_acc = 0.0;
         double fsum[ST];
 #pragma unroll
@@ -716,13 +729,13 @@ k_assemble(const AsmParams<T> p) {
                 }
             }
             if (HAS_PSI) {
-                // per-warp energy sums now, while other warps finish phase 1 (s_red is free:
-                // the previous item's warp 0 read it before this item's first barrier)
+                // per-warp energy sums now, while other warps finish phase 1 (this half of s_red
+                // was last read by warp 0 before the previous item's first barrier)
                 T wv[ST];
 #pragma unroll
                 for (int q = 0; q < ST; ++q) wv[q] = q < nq ? wacc[q] : T(0);
                 const T r = warp_multi_sum<T, ST>(wv, lane);
-                if ((lane & (32 / ST - 1)) == 0) s_red[warp][lane / (32 / ST)] = (double)r;
+                if ((lane & (32 / ST - 1)) == 0) s_red[cur][warp][lane / (32 / ST)] = (double)r;
             }
             // the next block's fields, into the same buffer once every thread's phase-1 reads
             // are done (the barrier before phase 2); its record has had phase 1 to land, and
@@ -733,6 +746,7 @@ k_assemble(const AsmParams<T> p) {
                 if (tn < NI) {
                     mbar_wait(&s_bar[cur ^ 1], cur ? par0 : par1);
                     const int s0n = cn * ST, nqn = min(ST, S - s0n);
+                    const int non = o1n - o0n;
                     stage_fields<D, T, NT, ST, MASKED>(ustage, sg_nxt, p.rec_base, staged_src, p, s0n, nqn, non);
                     if (NF == 2) stage_fields<D, T, NT, ST, false>(ustage + ust1, sg_nxt, p.rec_base, p.u, p, s0n, nqn, non);
                     if (has_mat)
@@ -928,41 +942,31 @@ k_assemble(const AsmParams<T> p) {
                 }
             }
         }
-        // ---------------- per-item sums (the item's samples) and CG dot
-        if (HAS_PSI || cgdot) {
-            if (HAS_PSI) {   // (the energy sums went to s_red after phase 1)
+        // ---------------- per-item sums (the item's samples): the f.u sums join the energy sums
+        // in this item's half of s_red; warp 0 adds the warps' sums after the next barrier
+        if (HAS_PSI) {
 #pragma unroll
-                for (int q = 0; q < ST; ++q) {
-                    if (q >= nq) break;
-                    const double f2 = FEXT ? warp_sum(fsum[q]) : 0.0;
-                    if (lane == 0) s_red[warp][ST + q] = f2;
-                }
-            }
-            if (cgdot) {
-                const double d2 = warp_sum(dot_acc);
-                if (lane == 0) s_red[warp][2 * ST] = d2;
+            for (int q = 0; q < ST; ++q) {
+                if (q >= nq) break;
+                const double f2 = FEXT ? warp_sum(fsum[q]) : 0.0;
+                if (lane == 0) s_red[cur][warp][ST + q] = f2;
             }
         }
-        bar_main(NT);   // phase 2 done (fbuf free), s_red complete
-        if ((HAS_PSI || cgdot) && warp == 0) {
-            if (HAS_PSI && lane < 2 * nq) {
-                const int q = lane % nq, kind = lane / nq;
-                double r = 0.0;
-                for (int w = 0; w < NT / 32; ++w) r += s_red[w][kind * ST + q];
-                p.blk_sum[(int64_t)(kind * S + s0 + q) * p.n_blocks + b] = r;
-            }
-            if (cgdot && lane == 31) {
-                double r = 0.0;
-                for (int w = 0; w < NT / 32; ++w) r += s_red[w][2 * ST];
-                p.blk_sum[(int64_t)(2 * S) * p.n_blocks + b] = r;
-            }
-        }
-        // s_red is rewritten only after the next block's first barrier: warp 0 is done by then
-        b = bn; c = cn; e0 = e0n; ne = nen; no = non;
+        b_prev = b; s0_prev = s0; nq_prev = nq; cur_prev = cur;
+        b = bn; c = cn; e0 = e0n; ne = e1n - e0n; no = o1n - o0n;
         bn += G;
         while (bn >= nb) { bn -= nb; ++cn; }
     }
     cp_wait<0>();
+    if (HAS_PSI && b_prev >= 0) {   // the last item's per-block sums
+        __syncthreads();
+        if (warp == 0 && lane < 2 * nq_prev) {
+            const int q = lane % nq_prev, kind = lane / nq_prev;
+            double r = 0.0;
+            for (int w = 0; w < NT / 32; ++w) r += s_red[cur_prev][w][kind * ST + q];
+            p.blk_sum[(int64_t)(kind * S + s0_prev + q) * p.n_blocks + b_prev] = r;
+        }
+    }
     if (n_inv) {
         atomicAdd(&p.ctr->n_inv, n_inv);
         atomicMax(&p.ctr->first_inv, INT32_MAX - first_inv);
