@@ -96,6 +96,13 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- bytes model
+# FMA-pipe slots per element-sample of the 3-D Neo-Hookean kernels (counted from
+# the formulas of element.cuh; the compiled phase 1 issues exactly these, 338 / 488 packed
+# FFMA2-class instructions per element for 4 samples)
+FMA_SLOTS_ER_NH3 = 169
+FMA_SLOTS_KV_NH3 = 244
+
+
 def bytes_energy_residual(E, N, d, S, s, want_W=True, mat_per_elem=0, K=1):
     """Algorithmic bytes of one fused energy+residual launch: conn, grad, vol,
     material read once; u read once; r written once; W_e written once; totals."""
@@ -230,6 +237,22 @@ def run_gpu(args):
                             "algorithmic_bytes": B_tg, "avg_launch_us": float(tg_ms.mean()) * 1e3,
                             "achieved": B_tg / (tg_ms.mean() * 1e-3) / 1e9,
                             "frac": B_tg / (tg_ms.mean() * 1e-3) / 1e9 / peak}}
+
+    # ALU view of the same two kernels (config 3 sits past the FP32 ridge).  One
+    # FMA-pipe slot = one lane's FFMA / FMUL / FADD (packed FFMA2 = two slots per lane and issue);
+    # slots per element-sample as the arithmetic of element.cuh is written, peak =
+    # the FFMA2 rate measured now by pfem_fma_peak (outside the timed region).
+    try:
+        pk2, pk1, pk64 = pf.fma_peak("ffma2"), pf.fma_peak("ffma"), pf.fma_peak("dfma")
+        alu = {"unit": "T lane-FMA slots/s", "peak": pk2 / 1e12, "peak_ffma": pk1 / 1e12, "peak_dfma": pk64 / 1e12,
+               "peak_source": "pfem_fma_peak (dependent FFMA2 / FFMA / DFMA chains, measured in this run)"}
+        for key, ops, ms in (("energy_residual", FMA_SLOTS_ER_NH3, er_avg), ("tangent", FMA_SLOTS_KV_NH3, float(tg_ms.mean()))):
+            ach = ops * E * S / (ms * 1e-3)
+            alu[key] = {"slots_per_element_sample": ops, "achieved": ach / 1e12, "frac": ach / pk2,
+                        "floor_us": ops * E * S / pk2 * 1e6}
+        roofline["alu"] = alu
+    except Exception as exc:   # a diagnostic: the bench line stands without it
+        roofline["alu"] = {"error": str(exc)}
 
     # ---------------- e2e: host buffers through the public API, copies inside the timed region.
     # Every step copies its inputs (u, v) from pinned host memory and its results (totals, r,

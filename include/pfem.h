@@ -398,6 +398,14 @@ int64_t pfem_last_error_index(void);
 int32_t pfem_abi_version(void);
 /* number of kernel launches issued by this thread since the last reset (bench evidence) */
 int64_t pfem_launch_count(int32_t reset);
+/* Measured FMA-pipe peak of the current device (the denominators of the ALU
+ * floors; not on the hot path).  kind 0: fp32 FFMA, 1: fp32 packed FFMA2 (two FMAs per lane
+ * and issue slot), 2: fp64 DFMA; every thread of a resident grid runs 8 independent chains of
+ * `iters` dependent FMAs from register operands.  Writes lane FMAs per second (x 2 = flop/s)
+ * to the HOST double *lane_fma_per_s.  Synchronous: it allocates 32 bytes of device memory,
+ * times 4 launches with CUDA events on `stream` and waits for them.
+ * Errors: PFEM_ERR_ARG (kind, iters, null result), PFEM_ERR_CUDA. */
+pfem_status pfem_fma_peak(int32_t kind, int32_t iters, double* lane_fma_per_s, void* stream);
 
 #ifdef __cplusplus
 }

@@ -104,6 +104,7 @@ SIGNATURES = {
     "pfem_last_error_index": (C.c_int64, []),
     "pfem_abi_version": (C.c_int32, []),
     "pfem_launch_count": (C.c_int64, [C.c_int32]),
+    "pfem_fma_peak": (C.c_int32, [C.c_int32, C.c_int32, C.POINTER(C.c_double), C.c_void_p]),
 }
 
 

@@ -379,3 +379,14 @@ def newton(mesh: Mesh, mat: Material, u0: torch.Tensor, f_ext=None, mask=None, t
 
 def launch_count(reset: bool = False) -> int:
     return int(L.load().pfem_launch_count(1 if reset else 0))
+
+
+FMA_KINDS = {"ffma": 0, "ffma2": 1, "dfma": 2}
+
+
+def fma_peak(kind: str = "ffma2", iters: int = 4096) -> float:
+    """pfem_fma_peak: measured FMA-pipe peak of the current device in lane FMAs per second
+    (kind: 'ffma' fp32, 'ffma2' fp32 packed pairs, 'dfma' fp64)."""
+    out = C.c_double(0.0)
+    L.check(L.load().pfem_fma_peak(FMA_KINDS[kind], int(iters), C.byref(out), _stream()))
+    return float(out.value)

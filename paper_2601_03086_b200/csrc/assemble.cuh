@@ -13,7 +13,8 @@
 //            -> fbuf[slot][element][dim][sample] (fp32 samples in FFMA2 pairs); W_e; per-warp
 //            energy sums right after the element loop
 //   phase 2  after one barrier (the next block's fields are then copied into the freed field
-//            buffer): HP threads per node occurrence, occurrences in descending entry count,
+//            buffer): threads per node occurrence (fp32 four samples: one per component),
+//            occurrences in descending entry count,
 //            sum the block-local CSR entries in ascending (element, slot) order.  A node touched
 //            only by this block gets its final value; otherwise the block writes its segment
 //            seg[slot][s][d] (slots node-major, ascending block)
@@ -35,9 +36,9 @@ namespace pfem {
 enum { OP_ENERGY = 0, OP_ENERGY_RESIDUAL = 1, OP_RESIDUAL = 2, OP_TANGENT = 3 };
 // staged kernel shape (measured): 256 threads, 2 resident CTAs per SM, T4 blocks of
 // at most 256 elements (T3: 512)
-constexpr int STAGED_MINB = PFEM_STAGED_MINB;
-constexpr int STAGED_NT = PFEM_STAGED_NT;
-constexpr int EB3 = PFEM_EB3;
+constexpr int STAGED_MINB = 2;
+constexpr int STAGED_NT = 256;
+constexpr int EB3 = 256;
 constexpr int ASM_NT = 256;   // main (element / occurrence) threads per CTA
 constexpr int FIX_WARPS = 1;  // fix-up warps per CTA (+1 publisher warp)
 constexpr int FIX_UNROLL = 4; // segments loaded together by one fix-up lane
@@ -497,10 +498,7 @@ k_assemble(const AsmParams<T> p) {
     using V = std::conditional_t<(sizeof(T) == 4 && ST == 4), F4, std::conditional_t<(sizeof(T) == 4 && ST % 2 == 0), F2, T>>;
     constexpr int L = VTraits<V>::L;
     // fbuf[NV][EB][D][ST] in element order, gathered through loc_ent in phase 2
-    constexpr int HP = (sizeof(T) == 4 && ST == 4) ? 2 : 1;   // phase-2 threads per occurrence
-    constexpr bool P2DIM = PFEM_P2DIM && sizeof(T) == 4 && ST == 4;   // ... or one per (occurrence, component)
-    constexpr int STH = ST / HP;
-    constexpr int SDH = D * STH;
+    constexpr bool P2DIM = sizeof(T) == 4 && ST == 4;   // phase 2: thread per (occurrence, component)
     const T* staged_src = (OP == OP_TANGENT) ? p.v : p.u;
     // shared layout: rec[2] | mat[2][2][EB] | ust[2][OCAP][D][ST] | fbuf[NV][EB][D][ST]
     const uint32_t srb = p.rec_end - p.rec_base;     // staged bytes of a record
@@ -521,7 +519,7 @@ k_assemble(const AsmParams<T> p) {
     constexpr bool pref = true;
     const int nb = p.n_blocks;
     const int NI = nb * ((S + ST - 1) / ST);
-    constexpr bool cgdot = false;   // CG products are single-sample calls: the direct form
+    // (CG products are single-sample calls: the direct forms carry the fused p.q)
     if (p.cg && ld_relaxed_i(&p.cg->done)) return;     // converged CG: the whole grid exits
 
     if (tid == 0) {
@@ -615,7 +613,6 @@ k_assemble(const AsmParams<T> p) {
             for (int w = 0; w < NT / 32; ++w) r += s_red[cur ^ 1][w][kind * ST + q];
             p.blk_sum[(int64_t)(kind * S + s0_prev + q) * p.n_blocks + b_prev] = r;
         }
-        double dot_acc = 0.0;
         double fsum[ST];
 #pragma unroll
         for (int q = 0; q < ST; ++q) fsum[q] = 0.0;
@@ -755,9 +752,8 @@ k_assemble(const AsmParams<T> p) {
                 cp_commit();
             }
             if (do_p2) {
-                // ---------------- phase 2: block-local CSR gather, HP threads per occurrence
-                // (fp32 ST = 4: two threads, each summing two samples of every entry, so all
-                // warps share the gather and each entry chain is half as long)
+                // ---------------- phase 2: block-local CSR gather, occurrences in descending
+                // entry count (occ_perm), entries in ascending (element, slot) order
                 const uint16_t* sop = reinterpret_cast<const uint16_t*>(sg + p.rec.occ_perm);
                 if constexpr (P2DIM) {
                     // fp32, four samples: one thread per (occurrence, component) sums the four
@@ -824,105 +820,42 @@ k_assemble(const AsmParams<T> p) {
                         }
                     }
                 } else
-                for (int w = tid; w < HP * no; w += NT) {
-                    const int oi = (int)sop[HP == 1 ? w : w / HP];
+                for (int w = tid; w < no; w += NT) {
+                    // other chunk shapes (fp64 pairs, single samples): a thread per occurrence
+                    const int oi = (int)sop[w];
                     PFEM_DCHECK(oi < no);
-                    const int qs = HP == 1 ? 0 : (w % HP) * STH;   // first sample of this thread
                     const int word = socc[oi];
                     const int node = word & OCC_NODE_MASK;
                     if (HAS_FORCE) {
-                        T accs[SDH];   // [D][STH]
+                        T accs[SD];   // [D][ST]
 #pragma unroll
-                        for (int k = 0; k < SDH; ++k) accs[k] = T(0);
+                        for (int k = 0; k < SD; ++k) accs[k] = T(0);
                         const int kb = soe[oi], k1 = soe[oi + 1];
                         PFEM_DCHECK(kb <= k1 && k1 <= NV * ne);
-                        if constexpr (HP == 1) {
-                            for (int k = kb; k < k1; ++k) sacc<T, SDH>(fbuf + (size_t)sle[k] * SD, accs);
-                        } else {
-                            // entries in pairs: both gathers in flight before the adds (the
-                            // adds stay in ascending entry order)
-                            int k = kb;
-#if PFEM_P2U > 2
-                            // PFEM_P2U entries per iteration, all gathers in flight before the
-                            // adds; a short tail re-reads the last entry and skips its add
-                            for (; k < k1; k += PFEM_P2U) {
-                                int j[PFEM_P2U];
-#pragma unroll
-                                for (int u = 0; u < PFEM_P2U; ++u) j[u] = sle[min(k + u, k1 - 1)];
-                                float2 x[PFEM_P2U][D];
-#pragma unroll
-                                for (int u = 0; u < PFEM_P2U; ++u)
-#pragma unroll
-                                    for (int i = 0; i < D; ++i)
-                                        x[u][i] = *reinterpret_cast<const float2*>(fbuf + (size_t)j[u] * SD + qs + i * ST);
-#pragma unroll
-                                for (int u = 0; u < PFEM_P2U; ++u)
-                                    if (k + u < k1) {
-#pragma unroll
-                                        for (int i = 0; i < D; ++i) {
-                                            F2 a0(accs[2 * i], accs[2 * i + 1]);
-                                            a0 = a0 + F2(x[u][i].x, x[u][i].y);
-                                            accs[2 * i] = a0.v.x; accs[2 * i + 1] = a0.v.y;
-                                        }
-                                    }
-                            }
-#endif
-                            for (; k + 1 < k1; k += 2) {
-                                const int j0 = sle[k], j1 = sle[k + 1];
-                                PFEM_DCHECK(j0 % EB < ne && j1 % EB < ne && j0 < NV * EB && j1 < NV * EB);
-                                const T* b0 = fbuf + (size_t)j0 * SD + qs;   // (record loc_ent = slot)
-                                const T* b1 = fbuf + (size_t)j1 * SD + qs;
-                                float2 x0[D], x1[D];
-#pragma unroll
-                                for (int i = 0; i < D; ++i) {
-                                    x0[i] = *reinterpret_cast<const float2*>(b0 + i * ST);
-                                    x1[i] = *reinterpret_cast<const float2*>(b1 + i * ST);
-                                }
-#pragma unroll
-                                for (int i = 0; i < D; ++i) {
-                                    F2 a0(accs[2 * i], accs[2 * i + 1]);
-                                    a0 = (a0 + F2(x0[i].x, x0[i].y)) + F2(x1[i].x, x1[i].y);
-                                    accs[2 * i] = a0.v.x; accs[2 * i + 1] = a0.v.y;
-                                }
-                            }
-                            if (k < k1) {
-                                const T* b0 = fbuf + (size_t)sle[k] * SD + qs;
-#pragma unroll
-                                for (int i = 0; i < D; ++i) {
-                                    const float2 x0 = *reinterpret_cast<const float2*>(b0 + i * ST);
-                                    F2 a0(accs[2 * i], accs[2 * i + 1]);
-                                    a0 = a0 + F2(x0.x, x0.y);
-                                    accs[2 * i] = a0.v.x; accs[2 * i + 1] = a0.v.y;
-                                }
-                            }
-                        }
-                        // accs layout: HP == 1 [D][ST] (sacc over SD contiguous values), HP == 2 [D][2]
+                        for (int k = kb; k < k1; ++k) sacc<T, SD>(fbuf + (size_t)sle[k] * SD, accs);
                         if (word & (OCC_NONOWNER | OCC_EARLIER)) {
                             // this block's segment of a multi-block node: seg[slot][s][d], slots
                             // node-major (a node's segments contiguous, ascending block)
                             const int slot = sseg[oi];
                             PFEM_DCHECK(slot >= 0 && slot < p.n_seg_total);
 #pragma unroll
-                            for (int qq = 0; qq < STH; ++qq) {
-                                const int q = qs + qq;
+                            for (int q = 0; q < ST; ++q) {
                                 if (q >= nq) break;
                                 T* dst = p.partial + ((int64_t)slot * S + s0 + q) * D;
 #pragma unroll
-                                for (int i = 0; i < D; ++i) dst[i] = accs[i * STH + qq];
+                                for (int i = 0; i < D; ++i) dst[i] = accs[i * ST + q];
                             }
                         } else {
 #pragma unroll
-                            for (int qq = 0; qq < STH; ++qq) {
-                                const int q = qs + qq;
+                            for (int q = 0; q < ST; ++q) {
                                 if (q >= nq) break;
                                 const int64_t nb = (int64_t)(s0 + q) * p.sstride + (int64_t)node * D;
 #pragma unroll
                                 for (int i = 0; i < D; ++i) {
-                                    T val = accs[i * STH + qq];
+                                    T val = accs[i * ST + q];
                                     if (OP == OP_TANGENT && MASKED && __ldg(p.mask + (int64_t)node * D + i))
                                         val = __ldg(p.v + nb + i);
                                     p.out[nb + i] = out_value(p, (int64_t)node * D + i, val);
-                                    if (cgdot) dot_acc += (double)__ldg(p.v + nb + i) * (double)val;
                                 }
                             }
                         }
@@ -930,7 +863,7 @@ k_assemble(const AsmParams<T> p) {
                     if (HAS_PSI && FEXT && !(word & OCC_NONOWNER)) {
 #pragma unroll
                         for (int q = 0; q < ST; ++q) {   // (compile-time q: fsum stays in registers)
-                            if (q < qs || q >= qs + STH || q >= nq) continue;
+                            if (q >= nq) continue;
                             const int64_t nb = (int64_t)(s0 + q) * p.sstride + (int64_t)node * D;
                             double w2 = 0.0;
 #pragma unroll

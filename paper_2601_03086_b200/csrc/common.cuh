@@ -11,24 +11,6 @@
 
 #include "../../include/pfem.h"
 
-// staged-kernel shape (A/B builds override with -D): fp32 T4 block capacity, threads and
-// resident CTAs per SM
-#ifndef PFEM_EB3
-#define PFEM_EB3 256
-#endif
-#ifndef PFEM_STAGED_NT
-#define PFEM_STAGED_NT 256
-#endif
-#ifndef PFEM_STAGED_MINB
-#define PFEM_STAGED_MINB 2
-#endif
-#ifndef PFEM_P2DIM
-#define PFEM_P2DIM 1   // fp32 four-sample phase 2: thread per (occurrence, component)
-#endif
-#ifndef PFEM_P2U
-#define PFEM_P2U 2   // phase-2 entries gathered per loop iteration (fp32, four samples)
-#endif
-
 namespace pfem {
 
 // ------------------------------------------------------------------ errors

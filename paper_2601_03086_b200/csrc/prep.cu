@@ -699,7 +699,7 @@ pfem_status prepare_impl(pfem_mesh* m, cudaStream_t s) {
     // defaults: the staged kernel's capacity (T4 256, T3 512); fp64 T4 plans 384 — their calls
     // are single-sample solves (K.v in CG / Newton) served by the direct form, where larger
     // blocks mean fewer multi-block nodes (measured on config 4: 131 -> 123 us)
-    const int eb_default = D == 3 ? (m->dtype == PFEM_F64 ? 384 : PFEM_EB3) : 512;
+    const int eb_default = D == 3 ? (m->dtype == PFEM_F64 ? 384 : 256) : 512;
     int eb = m->block_elems > 0 ? m->block_elems : eb_default;
     eb = std::min(eb, PLAN_MAX_KEYS / nv);
     const int eb_cap = std::max(eb, eb_default);

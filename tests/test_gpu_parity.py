@@ -888,3 +888,16 @@ def test_bitwise_deterministic_all_paths():
     for _ in range(2):
         for a, b in zip(run(), ref):
             assert torch.equal(a, b)
+
+
+def test_fma_peak_diagnostic():
+    """pfem_fma_peak: the measured FMA-pipe rates are positive and below what
+    148 SMs x 128 lanes at 2.2 GHz could issue; the packed FFMA2 form is at least as fast as the
+    scalar FFMA form (measured on B200: both reach the same ~36 T lane-FMA/s, FFMA2 in half the
+    issue slots); fp64 runs at about half the fp32 rate."""
+    import paper_2601_03086_b200 as pf
+    p1, p2, p64 = pf.fma_peak("ffma"), pf.fma_peak("ffma2"), pf.fma_peak("dfma")
+    cap = 148 * 128 * 2.2e9
+    assert 1e12 < p1 < cap and 1e12 < p2 < cap * 1.01
+    assert 0.9 < p2 / p1 < 2.5
+    assert 1e11 < p64 <= p1 * 1.05
