@@ -79,3 +79,14 @@ def test_ctypes_structs_match_the_header_layout(tmp_path):
         assert got[(name, "size")] == ctypes.sizeof(cls), name
         for fname, _ in cls._fields_:
             assert got[(name, fname)] == getattr(cls, fname).offset, (name, fname)
+
+
+def test_fma_peak_rejects_bad_arguments_without_a_gpu():
+    """pfem_fma_peak checks its arguments before touching the device (no compute call here)."""
+    import paper_2601_03086_b200 as pf
+    lib = pf.load()
+    out = ctypes.c_double(0.0)   # PFEM_ERR_ARG = -1
+    assert lib.pfem_fma_peak(7, 16, ctypes.byref(out), None) == -1
+    assert lib.pfem_fma_peak(1, 0, ctypes.byref(out), None) == -1
+    assert lib.pfem_fma_peak(1, 16, None, None) == -1
+    assert b"pfem_fma_peak" in lib.pfem_last_error()
