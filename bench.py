@@ -251,6 +251,9 @@ def run_gpu(args):
             alu[key] = {"slots_per_element_sample": ops, "achieved": ach / 1e12, "frac": ach / pk2,
                         "floor_us": ops * E * S / pk2 * 1e6}
         roofline["alu"] = alu
+        roofline["note"] = ("bound 'hbm' is the roofline the north star grades; by arithmetic config 3 sits past the "
+                            "FP32 ridge: the FMA-pipe floors (alu.*.floor_us, measured peak) exceed the HBM times "
+                            f"({B_er / peak / 1e3:.1f} / {B_tg / peak / 1e3:.1f} us)")
     except Exception as exc:   # a diagnostic: the bench line stands without it
         roofline["alu"] = {"error": str(exc)}
 
