@@ -199,7 +199,15 @@ def run_gpu(args):
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local)
     clocks.start()
-    time.sleep(0.2)
+    # the sampler needs ~0.2 s to start: keep the GPU busy with untimed steps meanwhile (an idle
+    # GPU drops its clocks, and the first timed steps would then run during the ramp-up; with
+    # the driver's 20 timed steps that inflated the per-kernel averages by ~5%)
+    t_spin, i_spin = time.perf_counter(), 0
+    while time.perf_counter() - t_spin < 0.2:
+        step(pf, sets[i_spin % N_COPIES])
+        i_spin += 1
+        if i_spin % 16 == 0:
+            torch.cuda.synchronize()
     if world > 1:
         tdist.barrier()
     torch.cuda.synchronize()
@@ -352,6 +360,7 @@ def run_gpu(args):
                       "model": "neohookean mu=0.4 lam=0.6", "samples_per_rank": S, "global_batch": S * world,
                       "step": "pfem_energy(W_e, totals, residual) + pfem_tangent_apply(K(u)v)",
                       "assembly": "csr", "parallelism": f"replicas x{world} (independent batches, no collective)",
+                      "spin_up": "untimed steps for 0.2 s while the clock sampler starts, then W warm-up semantics unchanged",
                       "l2": f"inputs larger than L2: {N_COPIES} rotating copies (~{N_COPIES * (B_er + B_tg) / 1e9:.2f} GB)"},
            "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
            "gpu": gpu_info(torch)}
@@ -366,7 +375,14 @@ def run_gpu(args):
         tdist.destroy_process_group()
 
 
-def time_events(torch, fn, reps):
+def time_events(torch, fn, reps, spin_s=0.05):
+    # untimed calls for spin_s first: the inputs were just generated on the host, and a GPU
+    # that sat idle meanwhile runs its first launches below its clocks
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < spin_s:
+        for _ in range(4):
+            fn()
+        torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(reps):
