@@ -278,7 +278,7 @@ def run_gpu(args):
                torch.empty(ss[0]["u"].shape, dtype=torch.float32).pin_memory(),
                torch.empty(ss[0]["u"].shape, dtype=torch.float32).pin_memory()) for _ in range(2)]
     tot_h, w_h, r_h, kv_h = outs_h[0]
-    Ke = max(5, min(50, K // 10))
+    Ke = max(20, min(50, K))   # enough steps that the three-stream pipeline's fill and drain do not dominate
     cur = torch.cuda.current_stream()
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
     ev_in = [torch.cuda.Event() for _ in range(2)]        # inputs of set i landed
