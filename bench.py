@@ -240,9 +240,11 @@ def run_gpu(args):
                 "frac": B_er / (er_avg * 1e-3) / 1e9 / peak,
                 "traffic": None if traffic is None else traffic.get("dram_bytes_per_launch"),
                 "kernel": "k_assemble<3,NH,f32,ENERGY_RESIDUAL,ST=4> (pfem_energy)",
-                "algorithmic_bytes": B_er, "avg_launch_us": er_avg * 1e3, "peak_source": peak_src,
+                "algorithmic_bytes": B_er, "avg_launch_us": er_avg * 1e3, "median_launch_us": float(np.median(er_ms)) * 1e3,
+                "min_launch_us": float(er_ms.min()) * 1e3, "peak_source": peak_src,
                 "tangent": {"kernel": "k_assemble<3,NH,f32,TANGENT,ST=4> (pfem_tangent_apply)",
                             "algorithmic_bytes": B_tg, "avg_launch_us": float(tg_ms.mean()) * 1e3,
+                            "median_launch_us": float(np.median(tg_ms)) * 1e3, "min_launch_us": float(tg_ms.min()) * 1e3,
                             "achieved": B_tg / (tg_ms.mean() * 1e-3) / 1e9,
                             "frac": B_tg / (tg_ms.mean() * 1e-3) / 1e9 / peak}}
 
